@@ -1,0 +1,276 @@
+"""Pins for the oracle (oracle/enum.c nested loops and oracle/gf.py generating functions).
+
+Every check here compares the oracle with something other than itself: brute force over
+the whole box prod [0, floor(n/g_i)], closed forms, values printed in the paper (Table 1,
+PAPER.md:266-298), the worked examples of SPEC.md, and the SURVEY.md Sec. 8(c) golden
+hashes (derived there by independent programs).  A dropped term, an off-by-one bound, a
+wrong sign or a transposed coordinate in the oracle fails at least one of them.
+"""
+import hashlib
+import itertools
+import math
+import random
+import struct
+from fractions import Fraction
+
+import pytest
+
+import oracle
+from oracle import gf
+from paper_2405_07989_b200 import workloads as W
+
+
+# ---------------------------------------------------------------- brute force
+def brute(n, g):
+    """All a in prod [0, floor(n/g_i)] with sum a_i g_i = n, sorted decreasing lex."""
+    ranges = [range(n // x + 1) for x in g]
+    sols = [a for a in itertools.product(*ranges) if sum(ai * gi for ai, gi in zip(a, g)) == n]
+    return sorted(sols, reverse=True)
+
+
+def pack(rows, B):
+    fmt = "<" + ("H" if B == 16 else "I") * (len(rows[0]) if rows else 0)
+    return b"".join(struct.pack(fmt, *r) for r in rows)
+
+
+def tiny_instances(count, seed):
+    rng = random.Random(seed)
+    out = []
+    for _ in range(count):
+        d = rng.randint(1, 4)
+        g = tuple(rng.randint(1, 12) for _ in range(d))
+        n = rng.randint(0, 40)
+        out.append((n, g))
+    # hand-picked degenerate cases
+    out += [(0, (5, 7)), (0, (3,)), (7, (2, 4)), (1, (2, 3)), (12, (4, 6)), (12, (6, 4)),
+            (9, (3, 3, 3)), (10, (1,)), (10, (3,)), (5, (1, 1, 1, 1))]
+    return out
+
+
+@pytest.mark.parametrize("n,g", tiny_instances(150, seed=0))
+def test_enum_matches_brute_force(oracle_mod, n, g):
+    want = brute(n, g)
+    for B in (16, 32):
+        raw = oracle.rows(n, g, B=B)
+        assert raw == pack(want, B)
+    assert oracle.count(n, g) == len(want)
+    L = oracle.hist_len_for(n, g)
+    h = [0] * L
+    for a in want:
+        h[sum(a)] += 1
+    assert oracle.hist(n, g) == h
+    assert gf.count(n, g) == len(want)
+    assert gf.hist(n, g) == h
+
+
+@pytest.mark.parametrize("n,g", tiny_instances(60, seed=1))
+def test_any_matches_brute_force(oracle_mod, n, g):
+    want = brute(n, g)
+    lens = [sum(a) for a in want]
+    for pred, arg in [(oracle.PRED_LEN_LE, 3), (oracle.PRED_LEN_GE, 6), (oracle.PRED_LEN_EQ, 5),
+                      (oracle.PRED_COORD_GE, (0 << 32) | 2), (oracle.PRED_COORD_GE, ((len(g) - 1) << 32) | 1)]:
+        found, wit = oracle.any_pred(n, g, pred, arg)
+        expect = any(oracle.pred_holds(a, pred, arg) for a in want)
+        assert found == expect
+        if found:
+            # the oracle stops at the FIRST witness in lex-descending order
+            first = next(a for a in want if oracle.pred_holds(a, pred, arg))
+            assert tuple(wit) == first
+    assert lens == [sum(a) for a in want]
+
+
+# ---------------------------------------------------------------- closed forms
+def test_closed_form_1_2(oracle_mod):
+    for n in range(0, 300):
+        assert oracle.count(n, (1, 2)) == n // 2 + 1
+        assert gf.count(n, (1, 2)) == n // 2 + 1
+
+
+def test_closed_form_all_ones(oracle_mod):
+    for d in range(1, 6):
+        for n in range(0, 25):
+            want = math.comb(n + d - 1, d - 1)
+            assert oracle.count(n, (1,) * d) == want
+            assert gf.count(n, (1,) * d) == want
+
+
+def test_closed_form_all_equal(oracle_mod):
+    # (g,..,g), n = m g  ->  C(m+d-1, d-1);  n not a multiple -> 0
+    for g in (2, 5, 7):
+        for d in (2, 3, 4):
+            for m in range(0, 12):
+                assert oracle.count(m * g, (g,) * d) == math.comb(m + d - 1, d - 1)
+                assert oracle.count(m * g + 1, (g,) * d) == 0
+
+
+def popoviciu(n, a, b):
+    # coprime a, b: n/(ab) - {b' n / a} - {a' n / b} + 1
+    bp = pow(b, -1, a) if a > 1 else 0
+    ap = pow(a, -1, b) if b > 1 else 0
+    frac = lambda x: x - (x.numerator // x.denominator)
+    v = Fraction(n, a * b) - frac(Fraction(bp * n, a)) - frac(Fraction(ap * n, b)) + 1
+    assert v.denominator == 1
+    return int(v)
+
+
+def test_closed_form_popoviciu(oracle_mod):
+    for a, b in [(2, 3), (3, 5), (6, 35), (7, 11), (13, 37), (9, 20)]:
+        for n in range(0, 400, 7):
+            assert oracle.count(n, (a, b)) == popoviciu(n, a, b)
+            assert oracle.count(n, (b, a)) == popoviciu(n, a, b)
+
+
+def test_d1_and_n0_and_gcd(oracle_mod):
+    assert oracle.rows(12, (4,), B=32) == struct.pack("<I", 3)
+    assert oracle.count(13, (4,)) == 0
+    for d in range(1, 7):
+        g = tuple(range(3, 3 + d))
+        assert oracle.rows(0, g, B=16) == b"\x00\x00" * d
+        assert oracle.hist(0, g)[0] == 1
+    assert oracle.count(7, (4, 6)) == 0          # gcd 2 does not divide 7
+    assert oracle.count(7, (2, 4)) == 0
+    assert oracle.count(3, (5, 7)) == 0          # n < min g
+
+
+# ---------------------------------------------------------------- SPEC / paper examples
+def test_spec_worked_examples(oracle_mod):
+    t = lambda n, g: oracle.rows_as_tuples(oracle.rows(n, g, B=32), len(g), 32)
+    assert t(10, (2, 3)) == [(5, 0), (2, 2)]
+    assert t(4, (2, 2)) == [(2, 0), (1, 1), (0, 2)]
+    assert t(1, (2, 3)) == []
+    assert t(0, (5, 7)) == [(0, 0)]
+    assert t(30, (3, 5)) == [(10, 0), (5, 3), (0, 6)]
+    found, wit = oracle.any_pred(10, (2, 3), oracle.PRED_LEN_GE, 5)
+    assert found and wit == [5, 0]
+
+
+def test_mcnugget(oracle_mod):
+    g = (6, 9, 20)
+    assert oracle.count(43, g) == 0                            # Frobenius number 43
+    assert oracle.rows_as_tuples(oracle.rows(44, g, B=32), 3, 32) == [(4, 0, 1), (1, 2, 1)]
+    rows = oracle.rows_as_tuples(oracle.rows(1000, g, B=32), 3, 32)
+    assert len(rows) == 465
+    assert rows[0] == (160, 0, 2) and rows[-1] == (0, 0, 50)
+
+
+# PAPER.md Table 1.  Three printed cells are wrong:
+# exact DP and two brute-force enumerators agree on the corrected values below.
+TABLE1 = {
+    (3, 1000): 30, (3, 20000): 10991, (3, 45000): 55503, (3, 70000): 134209,
+    (3, 150000): 615856, (3, 225000): 1385404, (3, 300000): 2462699, (3, 500000): 6840027,
+    (4, 1000): 274, (4, 5000): 29601, (4, 9000): 169752, (4, 13000): 508263,
+    (4, 17000): 1132667, (4, 20000): 1841247, (4, 23000): 2796813, (4, 27000): 4518931,
+    (4, 45000): 20861676,
+    (5, 1000): 1920, (5, 3000): 125780, (5, 5000): 928872, (5, 7000): 3501274,
+    (5, 9000): 9466814,
+    (6, 1000): 10873, (6, 1500): 70427, (6, 2000): 273456, (6, 3000): 1910466,
+    (7, 1000): 52036, (7, 1500): 473670, (7, 2000): 2369185,
+}
+TABLE1_CORRECTED = {(5, 9000): 9466815, (6, 2000): 273487, (6, 3000): 1910535}
+
+
+def test_table1_generating_function():
+    for (d, n), printed in TABLE1.items():
+        got = gf.count(n, W.TABLE1_GENS[:d])
+        if (d, n) in TABLE1_CORRECTED:
+            assert printed != got and got == TABLE1_CORRECTED[(d, n)]
+            assert got - printed > 0  # the paper undercounts
+        else:
+            assert got == printed, (d, n)
+
+
+@pytest.mark.parametrize("d,n", [(3, 1000), (3, 45000), (4, 1000), (4, 9000), (5, 1000),
+                                 (5, 3000), (6, 1000), (6, 2000), (7, 1000), (5, 9000)])
+def test_table1_enumeration(oracle_mod, d, n):
+    want = TABLE1_CORRECTED.get((d, n), TABLE1[(d, n)])
+    assert oracle.count(n, W.TABLE1_GENS[:d]) == want
+
+
+# ---------------------------------------------------------------- invariants
+@pytest.mark.parametrize("inst", W.random_instances(40, seed=0, d_max=5, g_max=50, n_max=400))
+def test_invariants(oracle_mod, inst):
+    n, g = inst.n, inst.gens
+    if gf.count(n, g) > 200000:
+        pytest.skip("too many rows for a quick invariant check")
+    rows = oracle.rows_as_tuples(oracle.rows(n, g, B=32), len(g), 32)
+    assert len(rows) == gf.count(n, g)
+    for r in rows:
+        assert sum(a * b for a, b in zip(r, g)) == n
+    for x, y in zip(rows, rows[1:]):
+        assert x > y  # strictly decreasing lex => no duplicates
+    h = [0] * oracle.hist_len_for(n, g)
+    for r in rows:
+        h[sum(r)] += 1
+    assert h == gf.hist(n, g)
+
+
+def test_box_restriction(oracle_mod):
+    n, g = 300, (3, 5, 7, 11)
+    rows = oracle.rows_as_tuples(oracle.rows(n, g, B=32), 4, 32)
+    for prefix, lo, hi in [((), 10, 20), ((30,), 0, 5), ((20, 6), 3, 9), ((0, 0, 2), 0, 100)]:
+        sel = [r for r in rows if tuple(r[:len(prefix)]) == tuple(prefix) and lo <= r[len(prefix)] <= hi]
+        got = oracle.rows_as_tuples(oracle.rows(n, g, B=32, box=(prefix, lo, hi)), 4, 32)
+        assert got == sel
+        if sel:
+            # offset of the first row of the box in canonical order, from the GF tables
+            first_prefix = sel[0][:len(prefix) + 1]
+            assert rows.index(sel[0]) == gf.rows_before_prefix(n, g, first_prefix)
+
+
+def test_work_ceiling(oracle_mod):
+    with pytest.raises(oracle.OracleTooLarge):
+        oracle.count(4275, W.C3.gens, ceiling=10 ** 6)
+
+
+# ---------------------------------------------------------------- golden hashes
+def sha(b):
+    return hashlib.sha256(b).hexdigest()
+
+
+def hist_bytes(h):
+    return struct.pack("<%dQ" % len(h), *h)
+
+
+@pytest.mark.parametrize("n,g,r16,hh", [
+    (10, (2, 3), "9bf38df076ec741b", "46df2c1aa650afa2"),
+    (4, (2, 2), "8022a331753a2201", "4d5206539fdafc08"),
+    (44, (6, 9, 20), "68d0ea2730a87658", "cd0e849ec197daba"),
+])
+def test_golden_small(oracle_mod, n, g, r16, hh):
+    assert sha(oracle.rows(n, g, B=16)).startswith(r16)
+    assert sha(hist_bytes(oracle.hist(n, g))).startswith(hh)
+
+
+GOLDEN_FULL = {
+    "C1": ("a582f027a36909d7b42120e660fc67da5634e83deeb0db0110c701f0c40de9d0",
+           "47e69baffe1651cb9792817b1218128bb8d0568843d7d6f6b68611caa4dbfabb",
+           "49612ed76a991a2968f06a110a34a88d99c02da67f60cddfba5dd936cf154fd1"),
+    "C2": ("af101488b41676e1839ebcca06e795af9c2a2d2b278c6f7e0e584315721eb01e",
+           "bf19f5cf473192f1055dba45a72442114f083eb5f912b14b8ee16e513ebf2ffd",
+           "f42facb340c129e12519e6a18459ddc21e5203b307e78456b8f1f683e5a704e3"),
+}
+
+
+@pytest.mark.parametrize("name", ["C1", "C2"])
+def test_golden_full(oracle_mod, name):
+    inst = W.CONFIGS[name]
+    r16, r32, hh = GOLDEN_FULL[name]
+    assert sha(oracle.rows(inst.n, inst.gens, B=16)) == r16
+    assert sha(oracle.rows(inst.n, inst.gens, B=32)) == r32
+    assert sha(hist_bytes(oracle.hist(inst.n, inst.gens))) == hh
+    assert sha(hist_bytes(gf.hist(inst.n, inst.gens))) == hh
+
+
+def test_golden_gf_large():
+    # C3/C4 full histogram and counts of C2-L, C3, C5
+    assert gf.count(12000, W.C2L.gens) == 824598466
+    assert gf.count(16000, W.C2XL.gens) == 2597173872
+    assert gf.count(4275, W.C3.gens) == 100032405189
+    assert gf.count(4274, W.C3.gens) == 99872270553
+    assert gf.count(20000, W.C5.gens) == 4055053706
+    h = gf.hist_u64(4275, W.C3.gens)
+    assert len(h) == 329
+    assert sha(hist_bytes(h)) == "732d09b032db36b6c536250ec753ddae1612ccfae0e19df8ccd8c028897bcdbd"
+    assert max(range(len(h)), key=lambda i: h[i]) == 200 and h[200] == 1636210748
+    h2 = gf.hist_u64(12000, W.C2L.gens)
+    assert sha(hist_bytes(h2)) == "2ca42f377ddc1ad1e41fed67b2246c454a24da2ae7b4f0f2873f62c3179ca5a4"
