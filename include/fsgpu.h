@@ -1,0 +1,190 @@
+/*
+ * fsgpu.h -- C ABI of libfsgpu.so: parallel bounded lexicographic enumeration of the
+ * factorization set on NVIDIA B200 (sm_100a).
+ *
+ * The problem (Sec. 1):
+ *
+ *     Z(n, (g_1..g_d)) = { (a_1..a_d) in N^d : a_1 g_1 + ... + a_d g_d = n }
+ *
+ * for any positive generators g_i, "regardless of order, setwise coprimality, or
+ * minimality, including outright repeated generators" (footnote 1).
+ * Generators are used AS GIVEN: no sorting, dedup or gcd reduction; coordinate i of every
+ * output row belongs to gens[i].
+ *
+ * The stream consumers are those of PAPER.md:55 (Sec. 2): counting the results, a
+ * boolean predicate over the results, and saving the results; plus the length histogram
+ * (length of a = sum_i a_i) named by BASELINE.json's north_star.
+ *
+ * Canonical order: strictly DECREASING lexicographic order in the user's coordinate order
+ * ("We compute candidates in lexicographic decreasing order").
+ *
+ * Execution: every entry point runs on the GPU (one successor stream per thread over
+ * disjoint, DP-sized lexicographic slices).  There is no CPU fallback: with
+ * no usable CUDA device the calls return FS_ENODEV.
+ *
+ * Ownership: `gens` is read during the call only.  `*_dev` pointers are caller-allocated
+ * device memory on the selected device (e.g. torch.empty(..., device="cuda").data_ptr()).
+ * The library allocates only internal scratch (DP tables, a work-queue word, counters),
+ * owned by an fs_plan or freed before the call returns.
+ *
+ * Errors (checked before any GPU work, in this order):
+ *   FS_EINVAL  d < 1 or d > FS_MAX_D; gens == NULL; some g_i == 0 (Z would be infinite);
+ *              B not in {16, 32}; hist_cap too small; unknown predicate or consumer;
+ *              out_dev not 16-byte aligned; world < 1 or rank outside [0, world).
+ *   FS_ERANGE  n + max_i g_i >= 2^31 (device arithmetic is u32 with exact 31-bit magic
+ *              division); B == 16 and some floor(n/g_i) > 65535; a DP total >= 2^63;
+ *              the DP tables would exceed FS_MAX_TABLE_BYTES; order=any with cap < |Z|.
+ *   FS_ENODEV  no CUDA device / driver.
+ *   FS_ECUDA, FS_ENOMEM  CUDA runtime failure / device allocation failure.
+ * Negative return values are these codes; fs_strerror() names them.
+ */
+#ifndef FSGPU_H
+#define FSGPU_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define FS_MAX_D 16
+#define FS_MAX_TABLE_BYTES (8ull << 30)
+
+enum {
+    FS_OK = 0,
+    FS_EINVAL = -1,
+    FS_ERANGE = -2,
+    FS_ECUDA = -3,
+    FS_ENOMEM = -4,
+    FS_ENODEV = -5
+};
+
+/* any-predicates ("a boolean variable based on a predicate's value").
+ * LEN_* compare the length l(a) = sum_i a_i with pred_arg; COORD_GE tests
+ * a_i >= k with pred_arg = (i << 32) | k, i 0-based. */
+enum {
+    FS_PRED_LEN_LE = 1,
+    FS_PRED_LEN_GE = 2,
+    FS_PRED_LEN_EQ = 3,
+    FS_PRED_COORD_GE = 4
+};
+
+/* consumers: what a plan's kernel does with each factorization */
+enum {
+    FS_CONSUMER_COUNT = 0,
+    FS_CONSUMER_HIST = 1,
+    FS_CONSUMER_ANY = 2,
+    FS_CONSUMER_ROWS = 3
+};
+
+/* Execution options for the _ex variants and plans.  Zero-initialise, then set fields.
+ *   device      CUDA device ordinal; -1 = the current device.
+ *   cuda_stream cudaStream_t the work is ordered on; NULL = legacy default stream.
+ *   rank/world  compute only rank's share of a world-way partition of the canonical lex
+ *               order (contiguous, equal DP weight; PAPER.md:196-200 bounds, 230-231
+ *               distributed workers).  world = 0 is treated as 1.
+ *   slice_units target units per slice (0 = automatic); rows per slice for ROWS plans
+ *               (rounded up to a multiple of 8).  Tests force tiny slices with it.
+ *   ctas_per_sm persistent CTAs per SM (0 = occupancy maximum). */
+typedef struct {
+    int device;
+    void *cuda_stream;
+    int rank;
+    int world;
+    uint64_t slice_units;
+    int ctas_per_sm;
+    int reserved[8];
+} fs_exec_t;
+
+/* ---------------------------------------------------------------------------------
+ * north_star entry points: current CUDA device, default stream, whole instance.
+ * All are synchronous: they return after the result is available.
+ * --------------------------------------------------------------------------------- */
+
+/* |Z(n, gens)| into *count_out (host). */
+int fs_count(uint64_t n, const uint32_t *gens, int d, uint64_t *count_out);
+
+/* hist_dev[l] = #{a in Z : sum_i a_i = l} for l = 0 .. floor(n / min g); entries beyond
+ * that up to hist_cap are zeroed.  hist_dev: device uint64[hist_cap],
+ * hist_cap >= floor(n / min g) + 1 (else FS_EINVAL). */
+int fs_length_set(uint64_t n, const uint32_t *gens, int d, uint64_t *hist_dev, uint64_t hist_cap);
+
+/* *found_out = 1 iff some a in Z satisfies pred; if so and witness_or_null != NULL, one
+ * such a (d host uint32; WHICH witness is unspecified) is written there. */
+int fs_any(uint64_t n, const uint32_t *gens, int d, int pred, uint64_t pred_arg,
+           int *found_out, uint32_t *witness_or_null);
+
+/* Writes the first min(cap, |Z|) rows of Z in canonical (decreasing lex) order to
+ * out_dev: row-major, d coordinates per row, little-endian uint16 (B = 16) or uint32
+ * (B = 32), no padding (row r at byte r * d * B/8).  Returns |Z| (>= 0, snprintf
+ * convention: truncation is not an error) or an FS_E* code.  out_dev must be 16-byte
+ * aligned. */
+int64_t fs_enumerate(uint64_t n, const uint32_t *gens, int d, int B, void *out_dev, uint64_t cap);
+
+/* ---------------------------------------------------------------------------------
+ * _ex variants: explicit device/stream, and a rank's share of a world-way partition.
+ * With world > 1 the outputs are the RANK'S PARTIAL results (count, histogram, any flag,
+ * or its contiguous block of rows); the caller combines them (python/dist: NCCL
+ * all_reduce / all_gather).  Still synchronous.
+ * --------------------------------------------------------------------------------- */
+int fs_count_ex(uint64_t n, const uint32_t *gens, int d, const fs_exec_t *ex, uint64_t *count_out);
+int fs_length_set_ex(uint64_t n, const uint32_t *gens, int d, const fs_exec_t *ex,
+                     uint64_t *hist_dev, uint64_t hist_cap);
+int fs_any_ex(uint64_t n, const uint32_t *gens, int d, const fs_exec_t *ex, int pred,
+              uint64_t pred_arg, int *found_out, uint32_t *witness_or_null);
+/* Writes this rank's rows (its contiguous block of the canonical order, at most cap of
+ * them) to out_dev; *global_row_offset_out (may be NULL) receives the canonical index of
+ * the block's first row.  Returns the number of rows in the rank's block (before cap). */
+int64_t fs_enumerate_ex(uint64_t n, const uint32_t *gens, int d, int B, void *out_dev,
+                        uint64_t cap, const fs_exec_t *ex, uint64_t *global_row_offset_out);
+
+/* ---------------------------------------------------------------------------------
+ * Plans: host work (validation, constants, exact DP tables, partition) done once;
+ * kernels enqueued asynchronously on ex->cuda_stream with results left in DEVICE memory,
+ * so a collective (NCCL) can follow on the same stream and the launch can be captured in
+ * a CUDA graph.  A plan's device scratch is reused across runs; runs on one plan must be
+ * stream-ordered (one at a time).
+ * --------------------------------------------------------------------------------- */
+typedef struct fs_plan fs_plan;
+
+typedef struct {
+    uint64_t n;
+    int d;
+    int consumer;
+    int level;                  /* node level L = max(d - 2, 0) */
+    uint64_t total_units;       /* units of the whole instance (entries+rows, or rows) */
+    uint64_t total_rows;        /* |Z(n, gens)| (from the exact DP) */
+    uint64_t unit_begin, unit_end; /* this rank's unit range */
+    uint64_t row_begin, row_end;   /* this rank's rows (ROWS plans; else 0,0) */
+    uint64_t slice_units;
+    uint64_t num_slices;
+    uint64_t hist_len;          /* floor(n / min g) + 1 */
+    uint32_t grid, block;       /* persistent launch shape */
+    uint64_t nodes_per_level[FS_MAX_D]; /* #prefixes (a_1..a_k) with residual >= 0, k = 0..L */
+    uint64_t table_bytes;
+} fs_plan_info_t;
+
+int fs_plan_create(uint64_t n, const uint32_t *gens, int d, int consumer, const fs_exec_t *ex,
+                   fs_plan **plan_out);
+int fs_plan_info(const fs_plan *plan, fs_plan_info_t *info_out);
+/* count_dev: device uint64[1], overwritten with the rank's count. */
+int fs_plan_count_async(fs_plan *plan, uint64_t *count_dev);
+/* hist_dev: device uint64[hist_cap], overwritten with the rank's histogram. */
+int fs_plan_hist_async(fs_plan *plan, uint64_t *hist_dev, uint64_t hist_cap);
+/* found_dev: device int32[1]; witness_dev: device uint32[d] or NULL. */
+int fs_plan_any_async(fs_plan *plan, int pred, uint64_t pred_arg, int *found_dev, uint32_t *witness_dev);
+/* writes min(cap, rank rows) rows of the rank's block to out_dev (16-byte aligned). */
+int fs_plan_enumerate_async(fs_plan *plan, int B, void *out_dev, uint64_t cap);
+/* number of kernel launches the last *_async call enqueued (for launch accounting) */
+int fs_plan_last_launches(const fs_plan *plan);
+void fs_plan_destroy(fs_plan *plan);
+
+const char *fs_strerror(int code);
+/* library version, e.g. 10000 for 1.0.0 */
+int fs_version(void);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* FSGPU_H */

@@ -1,0 +1,50 @@
+/*
+ * fsgpu_debug.h -- TEST/INTROSPECTION entry points of libfsgpu.so.  Not part of the
+ * product path: fs_count/fs_length_set/fs_any/fs_enumerate never call these.
+ *
+ * fsdbg_host_model runs the SAME per-lane successor code the kernels run
+ * (csrc/fs_core.cuh: slice unranking from the DP tables, slice entry, Alg. 3.1 successor
+ * with the modulo skip applied at run entry, consumers) sequentially on the host, slice by
+ * slice.  It exists so that the slicing/successor logic can be checked against the oracle
+ * on a machine without a GPU.  It is slow and single-threaded and is not a fallback: the
+ * python package never routes a user call to it.
+ */
+#ifndef FSGPU_DEBUG_H
+#define FSGPU_DEBUG_H
+
+#include <stdint.h>
+#include "fsgpu.h"
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+/* Runs every slice of the plan (this rank's share) on the host.
+ *   count_out        : rows emitted (all consumers)
+ *   hist (nullable)  : uint64[hist_cap] length histogram
+ *   rows (nullable)  : B-bit rows, rank block order, at most cap rows
+ *   slice_counts     : uint64[num_slices] rows emitted by each slice (nullable)
+ *   slice_first_row  : uint32[num_slices * d] first row (a vector) of each slice that
+ *                      emitted one, else all 0xFFFFFFFF (nullable)
+ * Returns FS_OK or an error. */
+int fsdbg_host_model(const fs_plan *plan, uint64_t *count_out, uint64_t *hist, uint64_t hist_cap,
+                     int B, void *rows, uint64_t cap, uint64_t *slice_counts, uint32_t *slice_first_row);
+
+/* Host unranking: the lane state at unit `unit` (global unit index) -> the prefix vector
+ * a_1..a_L, the row offset within the node (or -1 for the node-entry unit).  Returns
+ * FS_OK.  prefix_out: uint32[d]. */
+int fsdbg_unrank(const fs_plan *plan, uint64_t unit, uint32_t *prefix_out, int64_t *row_in_node_out);
+
+/* The 31-bit magic division constants the kernels use for divisor g (m, sh) and the
+ * quotient they produce for x (x < 2^31). */
+int fsdbg_magic(uint32_t g, uint32_t *m_out, uint32_t *sh_out);
+uint32_t fsdbg_magic_div(uint32_t x, uint32_t g);
+
+/* Device count of the launches the library made since load (all plans). */
+uint64_t fsdbg_total_launches(void);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif

@@ -1,0 +1,311 @@
+// fs_capi.cu -- the extern "C" boundary declared in include/fsgpu.h.
+#include <cuda_runtime.h>
+#include <stdint.h>
+#include <string.h>
+
+#include <new>
+
+#include "../../include/fsgpu.h"
+#include "../../include/fsgpu_debug.h"
+#include "fs_internal.h"
+
+namespace {
+
+// scratch layout (bytes): [0] queue u64, [8] count u64, [16] found i32, [64..128) witness
+constexpr size_t kOffCount = 8, kOffFound = 16, kOffWitness = 64;
+
+struct DeviceGuard {
+  int prev = -1;
+  explicit DeviceGuard(int dev) {
+    if (cudaGetDevice(&prev) != cudaSuccess) {
+      cudaGetLastError();
+      prev = -1;
+    }
+    if (dev >= 0) cudaSetDevice(dev);
+  }
+  ~DeviceGuard() {
+    if (prev >= 0) cudaSetDevice(prev);
+  }
+};
+
+fs::KParams base_params(const fs_plan *p) {
+  fs::KParams kp;
+  memset(&kp, 0, sizeof(kp));
+  kp.c = p->c;
+  kp.c.U = p->U_dev;
+  kp.c.ktab = p->ktab_dev;
+  kp.unit0 = p->unit_begin;
+  kp.unit1 = p->unit_end;
+  kp.T = p->T;
+  kp.num_slices = p->num_slices;
+  kp.num_claims = p->num_slices;
+  kp.queue = p->scratch_dev;
+  kp.hist_len = (uint32_t)p->hist_len;
+  kp.hist_smem = p->hist_len <= fs::kHistSmemMax ? 1u : 0u;
+  return kp;
+}
+
+int prepare(fs_plan *p, bool rows) {
+  if (!p) return FS_EINVAL;
+  if (rows != (p->c.alpha == 0)) return FS_EINVAL;  // row-sliced vs unit-sliced plan
+  int rc = fs_plan_upload_impl(p);
+  if (rc != FS_OK) return rc;
+  if (cudaSetDevice(p->device) != cudaSuccess) return FS_ECUDA;
+  if (cudaMemsetAsync(p->scratch_dev, 0, 8, p->stream) != cudaSuccess) return FS_ECUDA;
+  p->last_launches = 0;
+  return FS_OK;
+}
+
+int finish(fs_plan *p, int rc) {
+  if (rc == FS_OK) p->last_launches = 1;
+  return rc;
+}
+
+int sync_plan(fs_plan *p) {
+  cudaError_t e = cudaStreamSynchronize(p->stream);
+  if (e != cudaSuccess) return FS_ECUDA;
+  return FS_OK;
+}
+
+struct PlanHolder {
+  fs_plan *p = nullptr;
+  ~PlanHolder() { fs_plan_destroy(p); }
+};
+
+}  // namespace
+
+extern "C" {
+
+int fs_version(void) { return 10000; }
+
+const char *fs_strerror(int code) {
+  switch (code) {
+    case FS_OK: return "ok";
+    case FS_EINVAL: return "invalid argument";
+    case FS_ERANGE: return "value out of the supported range";
+    case FS_ECUDA: return "CUDA runtime error";
+    case FS_ENOMEM: return "device out of memory";
+    case FS_ENODEV: return "no CUDA device";
+  }
+  return "unknown error";
+}
+
+int fs_plan_create(uint64_t n, const uint32_t *gens, int d, int consumer, const fs_exec_t *ex, fs_plan **out) {
+  if (!out) return FS_EINVAL;
+  *out = nullptr;
+  fs_plan *p = new (std::nothrow) fs_plan();
+  if (!p) return FS_ENOMEM;
+  int rc = fs_validate_and_build(p, n, gens, d, consumer, ex);
+  if (rc != FS_OK) {
+    delete p;
+    return rc;
+  }
+  *out = p;
+  return FS_OK;
+}
+
+int fs_plan_info(const fs_plan *p, fs_plan_info_t *info) {
+  if (!p || !info) return FS_EINVAL;
+  memset(info, 0, sizeof(*info));
+  info->n = p->n;
+  info->d = p->d;
+  info->consumer = p->consumer;
+  info->level = p->d >= 2 ? p->d - 2 : 0;
+  info->total_units = p->total_units;
+  info->total_rows = p->total_rows;
+  info->unit_begin = p->unit_begin;
+  info->unit_end = p->unit_end;
+  info->row_begin = p->row_begin;
+  info->row_end = p->row_end;
+  info->slice_units = p->T;
+  info->num_slices = p->num_slices;
+  info->hist_len = p->hist_len;
+  info->grid = p->grid;
+  info->block = p->block;
+  for (int i = 0; i < FS_MAX_D; ++i) info->nodes_per_level[i] = p->nodes_per_level[i];
+  info->table_bytes = p->U.size() * 8 + p->ktab.size() * 4;
+  return FS_OK;
+}
+
+void fs_plan_destroy(fs_plan *p) {
+  if (!p) return;
+  fs_plan_free_device(p);
+  delete p;
+}
+
+int fs_plan_last_launches(const fs_plan *p) { return p ? p->last_launches : 0; }
+
+int fs_plan_count_async(fs_plan *p, uint64_t *count_dev) {
+  if (!count_dev) return FS_EINVAL;
+  int rc = prepare(p, false);
+  if (rc != FS_OK) return rc;
+  DeviceGuard g(p->device);
+  if (cudaMemsetAsync(count_dev, 0, 8, p->stream) != cudaSuccess) return FS_ECUDA;
+  fs::KParams kp = base_params(p);
+  kp.count_out = reinterpret_cast<unsigned long long *>(count_dev);
+  return finish(p, fs_launch(p, FS_CONSUMER_COUNT, 16, kp, p->stream));
+}
+
+int fs_plan_hist_async(fs_plan *p, uint64_t *hist_dev, uint64_t hist_cap) {
+  if (!p || !hist_dev || hist_cap < p->hist_len) return FS_EINVAL;
+  int rc = prepare(p, false);
+  if (rc != FS_OK) return rc;
+  DeviceGuard g(p->device);
+  if (cudaMemsetAsync(hist_dev, 0, hist_cap * 8, p->stream) != cudaSuccess) return FS_ECUDA;
+  fs::KParams kp = base_params(p);
+  kp.hist_out = reinterpret_cast<unsigned long long *>(hist_dev);
+  return finish(p, fs_launch(p, FS_CONSUMER_HIST, 16, kp, p->stream));
+}
+
+int fs_plan_any_async(fs_plan *p, int pred, uint64_t pred_arg, int *found_dev, uint32_t *witness_dev) {
+  if (!p || !found_dev) return FS_EINVAL;
+  if (pred < FS_PRED_LEN_LE || pred > FS_PRED_COORD_GE) return FS_EINVAL;
+  int rc = prepare(p, false);
+  if (rc != FS_OK) return rc;
+  DeviceGuard g(p->device);
+  if (cudaMemsetAsync(found_dev, 0, 4, p->stream) != cudaSuccess) return FS_ECUDA;
+  fs::KParams kp = base_params(p);
+  kp.pred = pred;
+  kp.pred_arg = pred_arg;
+  kp.found = found_dev;
+  kp.witness = witness_dev;
+  // bit-reversed claim order: every region of the lex order is sampled early (early exit)
+  uint32_t bits = 0;
+  while ((1ull << bits) < kp.num_slices) ++bits;
+  kp.permute = 1;
+  kp.claim_bits = bits;
+  kp.num_claims = kp.num_slices ? (1ull << bits) : 0;
+  return finish(p, fs_launch(p, FS_CONSUMER_ANY, 16, kp, p->stream));
+}
+
+int fs_plan_enumerate_async(fs_plan *p, int B, void *out_dev, uint64_t cap) {
+  if (!p || (B != 16 && B != 32)) return FS_EINVAL;
+  if (((uintptr_t)out_dev & 15u) != 0) return FS_EINVAL;
+  if (B == 16) {
+    for (int i = 0; i < p->d; ++i)
+      if (p->n / p->g[i] > 65535) return FS_ERANGE;
+  }
+  int rc = prepare(p, true);
+  if (rc != FS_OK) return rc;
+  DeviceGuard g(p->device);
+  fs::KParams kp = base_params(p);
+  const uint64_t span = p->unit_end - p->unit_begin;
+  const uint64_t take = cap < span ? cap : span;
+  if (take == 0) return finish(p, FS_OK);
+  if (!out_dev) return FS_EINVAL;
+  kp.unit1 = p->unit_begin + take;
+  kp.num_slices = (take + p->T - 1) / p->T;
+  kp.num_claims = kp.num_slices;
+  kp.rows_out = reinterpret_cast<unsigned char *>(out_dev);
+  kp.row_bytes = (uint32_t)(p->d * (B / 8));
+  return finish(p, fs_launch(p, FS_CONSUMER_ROWS, B, kp, p->stream));
+}
+
+// ------------------------------------------------------------------ synchronous entry points
+int fs_count_ex(uint64_t n, const uint32_t *gens, int d, const fs_exec_t *ex, uint64_t *count_out) {
+  if (!count_out) return FS_EINVAL;
+  PlanHolder h;
+  int rc = fs_plan_create(n, gens, d, FS_CONSUMER_COUNT, ex, &h.p);
+  if (rc != FS_OK) return rc;
+  rc = fs_plan_upload_impl(h.p);
+  if (rc != FS_OK) return rc;
+  DeviceGuard g(h.p->device);
+  uint64_t *dev = reinterpret_cast<uint64_t *>(reinterpret_cast<char *>(h.p->scratch_dev) + kOffCount);
+  rc = fs_plan_count_async(h.p, dev);
+  if (rc != FS_OK) return rc;
+  if (cudaMemcpyAsync(count_out, dev, 8, cudaMemcpyDeviceToHost, h.p->stream) != cudaSuccess) return FS_ECUDA;
+  return sync_plan(h.p);
+}
+
+int fs_count(uint64_t n, const uint32_t *gens, int d, uint64_t *count_out) {
+  fs_exec_t ex;
+  memset(&ex, 0, sizeof(ex));
+  ex.device = -1;
+  ex.world = 1;
+  return fs_count_ex(n, gens, d, &ex, count_out);
+}
+
+int fs_length_set_ex(uint64_t n, const uint32_t *gens, int d, const fs_exec_t *ex, uint64_t *hist_dev,
+                     uint64_t hist_cap) {
+  PlanHolder h;
+  int rc = fs_plan_create(n, gens, d, FS_CONSUMER_HIST, ex, &h.p);
+  if (rc != FS_OK) return rc;
+  if (!hist_dev || hist_cap < h.p->hist_len) return FS_EINVAL;
+  rc = fs_plan_hist_async(h.p, hist_dev, hist_cap);
+  if (rc != FS_OK) return rc;
+  DeviceGuard g(h.p->device);
+  return sync_plan(h.p);
+}
+
+int fs_length_set(uint64_t n, const uint32_t *gens, int d, uint64_t *hist_dev, uint64_t hist_cap) {
+  fs_exec_t ex;
+  memset(&ex, 0, sizeof(ex));
+  ex.device = -1;
+  ex.world = 1;
+  return fs_length_set_ex(n, gens, d, &ex, hist_dev, hist_cap);
+}
+
+int fs_any_ex(uint64_t n, const uint32_t *gens, int d, const fs_exec_t *ex, int pred, uint64_t pred_arg,
+              int *found_out, uint32_t *witness_or_null) {
+  if (!found_out) return FS_EINVAL;
+  if (pred < FS_PRED_LEN_LE || pred > FS_PRED_COORD_GE) return FS_EINVAL;
+  PlanHolder h;
+  int rc = fs_plan_create(n, gens, d, FS_CONSUMER_ANY, ex, &h.p);
+  if (rc != FS_OK) return rc;
+  rc = fs_plan_upload_impl(h.p);
+  if (rc != FS_OK) return rc;
+  DeviceGuard g(h.p->device);
+  char *base = reinterpret_cast<char *>(h.p->scratch_dev);
+  int *fdev = reinterpret_cast<int *>(base + kOffFound);
+  uint32_t *wdev = reinterpret_cast<uint32_t *>(base + kOffWitness);
+  rc = fs_plan_any_async(h.p, pred, pred_arg, fdev, wdev);
+  if (rc != FS_OK) return rc;
+  if (cudaMemcpyAsync(found_out, fdev, 4, cudaMemcpyDeviceToHost, h.p->stream) != cudaSuccess) return FS_ECUDA;
+  uint32_t wit[FS_MAX_D];
+  if (witness_or_null &&
+      cudaMemcpyAsync(wit, wdev, 4 * d, cudaMemcpyDeviceToHost, h.p->stream) != cudaSuccess)
+    return FS_ECUDA;
+  rc = sync_plan(h.p);
+  if (rc != FS_OK) return rc;
+  if (witness_or_null && *found_out) memcpy(witness_or_null, wit, 4 * d);
+  return FS_OK;
+}
+
+int fs_any(uint64_t n, const uint32_t *gens, int d, int pred, uint64_t pred_arg, int *found_out,
+           uint32_t *witness_or_null) {
+  fs_exec_t ex;
+  memset(&ex, 0, sizeof(ex));
+  ex.device = -1;
+  ex.world = 1;
+  return fs_any_ex(n, gens, d, &ex, pred, pred_arg, found_out, witness_or_null);
+}
+
+int64_t fs_enumerate_ex(uint64_t n, const uint32_t *gens, int d, int B, void *out_dev, uint64_t cap,
+                        const fs_exec_t *ex, uint64_t *global_row_offset_out) {
+  if (B != 16 && B != 32) return FS_EINVAL;
+  PlanHolder h;
+  int rc = fs_plan_create(n, gens, d, FS_CONSUMER_ROWS, ex, &h.p);
+  if (rc != FS_OK) return rc;
+  rc = fs_plan_enumerate_async(h.p, B, out_dev, cap);
+  if (rc != FS_OK) return rc;
+  if (h.p->uploaded) {
+    DeviceGuard g(h.p->device);
+    rc = sync_plan(h.p);
+    if (rc != FS_OK) return rc;
+  }
+  if (global_row_offset_out) *global_row_offset_out = h.p->row_begin;
+  return (int64_t)(h.p->row_end - h.p->row_begin);
+}
+
+int64_t fs_enumerate(uint64_t n, const uint32_t *gens, int d, int B, void *out_dev, uint64_t cap) {
+  fs_exec_t ex;
+  memset(&ex, 0, sizeof(ex));
+  ex.device = -1;
+  ex.world = 1;
+  int64_t r = fs_enumerate_ex(n, gens, d, B, out_dev, cap, &ex, nullptr);
+  return r;
+}
+
+uint64_t fsdbg_total_launches(void) { return g_fs_total_launches; }
+
+}  // extern "C"

@@ -1,0 +1,267 @@
+// fs_core.cuh -- the per-lane successor stream of the factorization-set enumeration.
+//
+// One "lane" (a GPU thread, or the host model in csrc/fs_host.cu) owns one bounded slice of
+// the decreasing-lexicographic order of Z(n, (g_1..g_d)) (Sec. 4: a bound
+// partitions the lex order into disjoint worker slices) and walks it with the successor of
+// PAPER.md Alg. 3.1, state in registers.
+//
+// Notation (0-based arrays, 1-based in comments to match the paper):
+//   d generators g_1..g_d, node level L = d-2.  A "node" is a prefix (a_1..a_L) with residual
+//   R_L = n - sum_{j<=L} a_j g_j >= 0.  Below a node the paper's stream runs the index-(d-1)
+//   candidates a_{d-1} = ceil/floor(R_L/g_{d-1}) .. 0 with a_d solved by division
+//   (decrementAndSolve).  We apply the paper's modulo optimisation at run
+//   entry: the valid a_{d-1} of a node are exactly a*, a*-s, a*-2s, ... >= 0 with
+//   s = g_d / gcd(g_{d-1}, g_d) (the additive order of g_{d-1} mod g_d), and a*
+//   is found from the residue rho = R_L mod g_{d-1} by a table lookup k0(rho), a* = A - k0,
+//   A = floor(R_L / g_{d-1}).  Every valid factorization of the node is then one "row".
+//
+//   The paper's overshoot candidate (.., ceil(R/g), 0, ..) is invalid unless the division is
+//   exact, in which case it equals the floor candidate; its successor is the floor candidate
+//   with one more coordinate solved.  The lane goes straight to the floor
+//   candidate: it visits every node the paper's stream visits, in the same order, and emits
+//   the same factorizations in the same order (Thm. 3.2/3.3).
+//
+// Units and slices: the stream is a sequence of units -- for each node in lex-descending
+// order, one ENTRY unit (alpha = 1; 0 for row-sliced plans) followed by one unit per ROW
+// (beta = 1).  The exact DP tables U[k][r] (units below a level-k node with residual r) let
+// a lane jump to any unit index (unrank) and run exactly `budget` units, so slices are
+// disjoint, gap-free and equal in work (a finer, exact form of the paper's bound splitting,
+// P:196-225, and of the "better work division" of P:316-317).
+#pragma once
+
+#include <stdint.h>
+
+#ifdef __CUDACC__
+#define FS_HD __host__ __device__ __forceinline__
+#else
+#define FS_HD inline
+#endif
+
+#ifndef FS_MAX_D
+#define FS_MAX_D 16
+#endif
+
+namespace fs {
+
+constexpr uint32_t kNone = 0x7FFFFFFFu;  // "no valid a_{d-1} in this node"
+
+// 31-bit magic division: q = floor(x / g) for x < 2^31 via one 32x32->64 multiply and a
+// shift: l = ceil(log2 g), m = floor(2^(31+l)/g) + 1 < 2^32, sh = 31 + l.  (m g = 2^(31+l)
+// + e with 0 < e <= 2^l, so x m / 2^(31+l) = x/g + x e/(g 2^(31+l)) and the error term is
+// < 1/g for x < 2^31.)
+struct Div {
+  uint32_t m, sh;
+};
+
+FS_HD uint32_t divq(uint32_t x, Div v) { return (uint32_t)(((uint64_t)x * v.m) >> v.sh); }
+
+// Instance constants as the lanes see them (passed by value in the kernel parameters).
+struct Consts {
+  uint32_t n;
+  int d;
+  uint32_t g[FS_MAX_D];
+  Div dv[FS_MAX_D];
+  uint32_t gA, gB;       // g_{d-1}, g_d
+  uint32_t h, s, t, inv; // h = gcd(gA,gB), s = gB/h, t = gA/h, inv = t^{-1} mod s
+  Div dvA, dvB, dvH, dvS;
+  uint32_t delta, q;     // g_L mod gA, g_L / gA (L >= 1)
+  uint32_t alpha, beta;  // units per node entry / per row
+  uint32_t ktab_len;     // 0: k0 by arithmetic; else table of gA entries
+  uint32_t _pad;
+  const uint64_t *U;     // DP tables, L rows of (n+1) entries
+  const uint32_t *ktab;  // k0 table (device or host)
+};
+
+#ifdef __CUDA_ARCH__
+FS_HD uint64_t ldU(const uint64_t *p) { return __ldg(p); }
+#else
+FS_HD uint64_t ldU(const uint64_t *p) { return *p; }
+#endif
+
+// smallest k >= 0 with g_d | rho + k g_{d-1}, or kNone (P:172 congruence)
+FS_HD uint32_t k0_arith(uint32_t rho, const Consts &c) {
+  uint32_t rq = divq(rho, c.dvH);
+  if (rq * c.h != rho) return kNone;
+  uint32_t rs = rq - divq(rq, c.dvS) * c.s;
+  uint32_t neg = rs ? c.s - rs : 0u;
+  return (uint32_t)(((uint64_t)neg * c.inv) % c.s);
+}
+
+template <int D>
+struct Lane {
+  static constexpr int L = D - 2;
+  static constexpr int LA = (D - 2) > 0 ? (D - 2) : 1;
+  uint32_t a[LA];  // a_1..a_L
+  uint32_t R[LA];  // R_1..R_L
+  uint32_t A, rho; // floor(R_L / g_{d-1}), R_L mod g_{d-1}
+  int32_t cur;     // current row's a_{d-1} (< 0: none left in this node)
+  uint32_t ad;     // current row's a_d
+  uint32_t lsum;   // a_1 + .. + a_L
+};
+
+// Node entry: solve the first valid a_{d-1} of the node (modulo skip at run entry).
+template <int D, bool NEED_AD>
+FS_HD void entry(Lane<D> &st, const Consts &c, const uint32_t *ktab) {
+  uint32_t k = c.ktab_len ? ktab[st.rho] : k0_arith(st.rho, c);
+  st.cur = (int32_t)st.A - (int32_t)k;  // A <= n < 2^31 - 1, so kNone gives cur < 0
+  if (NEED_AD) st.ad = divq(st.rho + k * c.gA, c.dvB);  // only meaningful if cur >= 0
+}
+
+// Deeper ascend of Alg. 3.1 steps 2-11: rightmost nonzero index i < L, a_i -= 1,
+// re-solve a_{i+1}..a_L greedily (floor) -- returns false at end of stream.
+template <int D>
+FS_HD bool ascend(Lane<D> &st, const Consts &c) {
+  constexpr int L = D - 2;
+  if constexpr (L <= 1) {
+    return false;
+  } else {
+    if (st.a[L - 2] > 0) {  // common case: one level up
+      st.a[L - 2]--;
+      uint32_t r = st.R[L - 2] + c.g[L - 2];
+      st.R[L - 2] = r;
+      uint32_t x = divq(r, c.dv[L - 1]);
+      st.a[L - 1] = x;
+      r -= x * c.g[L - 1];
+      st.R[L - 1] = r;
+      uint32_t A = divq(r, c.dvA);
+      st.A = A;
+      st.rho = r - A * c.gA;
+      st.lsum = st.lsum - 1 + x;
+      return true;
+    }
+    int k = -1;
+#pragma unroll
+    for (int j = 0; j < L - 2; ++j)
+      if (st.a[j] > 0) k = j;
+    if (k < 0) return false;
+#pragma unroll
+    for (int j = 0; j < L - 2; ++j)
+      if (j == k) {
+        st.a[j]--;
+        st.R[j] += c.g[j];
+      }
+    uint32_t lsum = 0;
+#pragma unroll
+    for (int j = 0; j < L; ++j) {
+      if (j > k) {
+        uint32_t r = st.R[j - 1];
+        uint32_t x = divq(r, c.dv[j]);
+        st.a[j] = x;
+        st.R[j] = r - x * c.g[j];
+      }
+      lsum += st.a[j];
+    }
+    uint32_t r = st.R[L - 1];
+    uint32_t A = divq(r, c.dvA);
+    st.A = A;
+    st.rho = r - A * c.gA;
+    st.lsum = lsum;
+    return true;
+  }
+}
+
+// Move to the next node in decreasing lex order; false at end of stream.
+template <int D>
+FS_HD bool advance(Lane<D> &st, const Consts &c) {
+  constexpr int L = D - 2;
+  if constexpr (L == 0) {
+    return false;
+  } else {
+    if (st.a[L - 1] > 0) {
+      st.a[L - 1]--;
+      st.R[L - 1] += c.g[L - 1];
+      uint32_t r2 = st.rho + c.delta;
+      uint32_t carry = r2 >= c.gA ? 1u : 0u;
+      st.rho = carry ? r2 - c.gA : r2;
+      st.A += c.q + carry;
+      st.lsum--;
+      return true;
+    }
+    return ascend<D>(st, c);
+  }
+}
+
+// Position the lane at global unit index u (exact, from the DP tables), perform the node
+// entry, and return the offset of u inside the node's unit list (0 = the entry unit when
+// alpha = 1).
+template <int D, bool NEED_AD>
+FS_HD uint64_t unrank(Lane<D> &st, const Consts &c, const uint32_t *ktab, uint64_t u) {
+  constexpr int L = D - 2;
+  uint32_t R = c.n;
+  uint32_t lsum = 0;
+  const uint64_t stride = (uint64_t)c.n + 1;
+#pragma unroll
+  for (int k = 0; k < L; ++k) {
+    const uint64_t *Uk = c.U + (uint64_t)k * stride;
+    const uint32_t g = c.g[k];
+    uint32_t top = divq(R, c.dv[k]);
+    // cum(x) = U[k][R - x g] = units of the subtrees a_k in [x, top]; nonincreasing in x.
+    uint32_t lo = 0, hi = top + 1;
+    while (hi - lo > 1) {
+      uint32_t mid = (lo + hi) >> 1;
+      if (ldU(Uk + (R - mid * g)) > u)
+        lo = mid;
+      else
+        hi = mid;
+    }
+    if (lo < top) u -= ldU(Uk + (R - (lo + 1) * g));
+    st.a[k] = lo;
+    R -= lo * g;
+    st.R[k] = R;
+    lsum += lo;
+  }
+  uint32_t A = divq(R, c.dvA);
+  st.A = A;
+  st.rho = R - A * c.gA;
+  st.lsum = lsum;
+  entry<D, NEED_AD>(st, c, ktab);
+  return u;
+}
+
+// After unrank(): consume the entry unit or skip to row j of the node.  Returns the units
+// consumed (0 or 1).
+template <int D, bool NEED_AD>
+FS_HD uint32_t position_in_node(Lane<D> &st, const Consts &c, uint64_t off) {
+  uint64_t j;
+  if (c.alpha) {
+    if (off == 0) return 1;
+    j = off - 1;
+  } else {
+    j = off;
+  }
+  st.cur -= (int32_t)((uint32_t)j * c.s);
+  if (NEED_AD) st.ad += (uint32_t)j * c.t;
+  return 0;
+}
+
+// One unit of the stream: emit the current row and step to the next valid a_{d-1}
+// (a_{d-1} -= s, a_d += t: the modulo skip), or -- when the node has no rows
+// left -- move to the next node (Alg. 3.1 step 2-11) and solve its first valid row.
+// ALPHA: units charged for a node entry (1 for count/hist/any slices, 0 for row slices).
+template <int D, bool NEED_AD, int ALPHA, class Emit>
+FS_HD void step(Lane<D> &st, const Consts &c, const uint32_t *ktab, uint32_t &budget, Emit &emit) {
+  if (st.cur >= 0) {
+    emit(st);
+    st.cur -= (int32_t)c.s;
+    if (NEED_AD) st.ad += c.t;
+    budget -= 1;
+  } else {
+    if (!advance<D>(st, c)) {
+      budget = 0;
+      return;
+    }
+    entry<D, NEED_AD>(st, c, ktab);
+    budget -= ALPHA;
+  }
+}
+
+// units below a node with residual r (the DP base): alpha + beta * #valid a_{d-1}
+FS_HD uint64_t node_units_host(uint32_t r, const Consts &c, const uint32_t *ktab) {
+  uint32_t A = r / c.gA, rho = r % c.gA;
+  uint32_t k = c.ktab_len ? ktab[rho] : k0_arith(rho, c);
+  uint64_t rows = 0;
+  if (k != kNone && k <= A) rows = (A - k) / c.s + 1;
+  return (uint64_t)c.alpha + (uint64_t)c.beta * rows;
+}
+
+}  // namespace fs

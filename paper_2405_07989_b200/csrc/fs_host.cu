@@ -1,0 +1,403 @@
+// fs_host.cu -- host side of the CUDA path: instance validation (PAPER.md:28 footnote 1 --
+// generators taken as given), device constants (magic division, modulo-skip congruence
+// constants), the exact DP tables that size the slices (not in the paper; serves
+// its "work division improvement"), the W-way partition of the lex order
+// (P:196-200), device upload, and the host model used by CPU tests.
+#include <cuda_runtime.h>
+#include <stdint.h>
+#include <string.h>
+
+#include <algorithm>
+#include <vector>
+
+#include "../../include/fsgpu.h"
+#include "../../include/fsgpu_debug.h"
+#include "fs_core.cuh"
+#include "fs_internal.h"
+
+using fs::Consts;
+using fs::Div;
+
+typedef unsigned __int128 u128;
+
+
+fs::Div fs_make_div(uint32_t g) {
+  uint32_t l = 0;
+  while (((uint64_t)1 << l) < g) ++l;  // l = ceil(log2 g)
+  uint64_t m = (((uint64_t)1 << (31 + l)) / g) + 1;
+  Div v;
+  v.m = (uint32_t)m;
+  v.sh = 31 + l;
+  return v;
+}
+
+static uint32_t gcd32(uint32_t a, uint32_t b) {
+  while (b) {
+    uint32_t t = a % b;
+    a = b;
+    b = t;
+  }
+  return a;
+}
+
+// inverse of t modulo s (gcd(t, s) = 1); s == 1 -> 0
+static uint32_t inv_mod(uint32_t t, uint32_t s) {
+  if (s == 1) return 0;
+  int64_t r0 = s, r1 = t % s, x0 = 0, x1 = 1;
+  while (r1) {
+    int64_t qq = r0 / r1, tmp = r0 - qq * r1;
+    r0 = r1;
+    r1 = tmp;
+    tmp = x0 - qq * x1;
+    x0 = x1;
+    x1 = tmp;
+  }
+  int64_t v = x0 % (int64_t)s;
+  if (v < 0) v += s;
+  return (uint32_t)v;
+}
+
+static uint64_t ceil_div_u64(uint64_t a, uint64_t b) { return a / b + (a % b ? 1 : 0); }
+
+// target number of resident lanes used to size slices when the caller does not (a B200
+// holds 148 SMs x 2048 threads; the persistent grid uses about half that at ~64 regs)
+static const uint64_t kTargetLanes = 148ull * 1024ull;
+static const uint64_t kSlicesPerLane = 16;
+
+int fs_validate_and_build(fs_plan *p, uint64_t n, const uint32_t *gens, int d, int consumer,
+                          const fs_exec_t *ex) {
+  if (d < 1 || d > FS_MAX_D || gens == nullptr) return FS_EINVAL;
+  if (consumer < FS_CONSUMER_COUNT || consumer > FS_CONSUMER_ROWS) return FS_EINVAL;
+  uint32_t gmax = 0, gmin = 0xFFFFFFFFu;
+  for (int i = 0; i < d; ++i) {
+    if (gens[i] == 0) return FS_EINVAL;
+    gmax = std::max(gmax, gens[i]);
+    gmin = std::min(gmin, gens[i]);
+  }
+  if (n + (uint64_t)gmax >= (1ull << 31)) return FS_ERANGE;
+  fs_exec_t e{};
+  if (ex) e = *ex;
+  if (e.world <= 0) e.world = 1;
+  if (e.rank < 0 || e.rank >= e.world) return FS_EINVAL;
+
+  p->n = n;
+  p->d = d;
+  p->consumer = consumer;
+  p->ex = e;
+  p->g.assign(gens, gens + d);
+  p->hist_len = n / gmin + 1;
+
+  Consts &c = p->c;
+  memset(&c, 0, sizeof(c));
+  c.n = (uint32_t)n;
+  c.d = d;
+  for (int i = 0; i < d; ++i) {
+    c.g[i] = gens[i];
+    c.dv[i] = fs_make_div(gens[i]);
+  }
+  c.alpha = (consumer == FS_CONSUMER_ROWS) ? 0u : 1u;
+  c.beta = 1;
+
+  if (d == 1) {
+    // Z(n,(g)) = {(n/g)} iff g | n: one row or none; no tables, no nodes.
+    p->total_rows = (n % gens[0] == 0) ? 1 : 0;
+    p->total_units = p->total_rows;
+    p->nodes_per_level[0] = 1;
+  } else {
+    const int L = d - 2;
+    c.gA = gens[d - 2];
+    c.gB = gens[d - 1];
+    c.h = gcd32(c.gA, c.gB);
+    c.s = c.gB / c.h;
+    c.t = c.gA / c.h;
+    c.inv = inv_mod(c.t % c.s, c.s);
+    c.dvA = fs_make_div(c.gA);
+    c.dvB = fs_make_div(c.gB);
+    c.dvH = fs_make_div(c.h);
+    c.dvS = fs_make_div(c.s);
+    if (L >= 1) {
+      c.delta = gens[L - 1] % c.gA;
+      c.q = gens[L - 1] / c.gA;
+    }
+    if (c.gA <= fs::kKtabMax) {
+      p->ktab.resize(c.gA);
+      c.ktab_len = 0;  // compute entries with the arithmetic form
+      for (uint32_t rho = 0; rho < c.gA; ++rho) p->ktab[rho] = fs::k0_arith(rho, c);
+      c.ktab_len = c.gA;
+      c.ktab = p->ktab.data();
+    }
+    const uint64_t N1 = n + 1;
+    if (L == 0) {
+      // d = 2: the root is the only node; no tables are needed
+      Consts cr = c;
+      cr.alpha = 0;
+      const uint64_t nr = fs::node_units_host((uint32_t)n, cr, p->ktab.data());
+      p->total_rows = nr;
+      p->total_units = c.alpha + nr;
+      p->nodes_per_level[0] = 1;
+    } else {
+      if ((uint64_t)L * N1 * 8ull > FS_MAX_TABLE_BYTES) return FS_ERANGE;
+      // base: units below a node with residual r; rows-only variant for |Z|.  u64 with an
+      // explicit 2^63 guard (every DP value is a count of an exact subset of the stream).
+      std::vector<uint64_t> arr(N1), rows(N1);
+      for (uint64_t r = 0; r <= n; ++r) {
+        Consts cr = c;
+        cr.alpha = 0;
+        const uint64_t nr = fs::node_units_host((uint32_t)r, cr, p->ktab.data());
+        rows[r] = nr;
+        arr[r] = c.alpha + nr;
+      }
+      p->U.assign((size_t)L * N1, 0);
+      for (int k = L - 1; k >= 0; --k) {
+        const uint64_t gk = gens[k];
+        for (uint64_t r = gk; r <= n; ++r) {
+          arr[r] += arr[r - gk];
+          rows[r] += rows[r - gk];
+          if (arr[r] >= (1ull << 63) || rows[r] >= (1ull << 63)) return FS_ERANGE;
+        }
+        memcpy(&p->U[(size_t)k * N1], arr.data(), N1 * 8);
+      }
+      p->total_units = arr[n];
+      p->total_rows = rows[n];
+      c.U = p->U.data();
+      // nodes per level: #(a_1..a_k) with sum a_j g_j <= n (forward coin DP, prefix sums)
+      std::vector<uint64_t> F(N1, 0);
+      F[0] = 1;
+      p->nodes_per_level[0] = 1;
+      for (int k = 1; k <= L; ++k) {
+        const uint64_t gk = gens[k - 1];
+        for (uint64_t r = gk; r <= n; ++r) F[r] = std::min<uint64_t>(F[r] + F[r - gk], 1ull << 63);
+        u128 s = 0;
+        for (uint64_t r = 0; r <= n; ++r) s += F[r];
+        p->nodes_per_level[k] = s >= ((u128)1 << 64) - 1 ? UINT64_MAX : (uint64_t)s;
+      }
+    }
+  }
+
+  // W-way partition: contiguous, equal units (P:196-200 bounds, P:230-231 workers)
+  const uint64_t U = p->total_units;
+  const uint64_t W = (uint64_t)e.world, r = (uint64_t)e.rank;
+  p->unit_begin = (uint64_t)((u128)U * r / W);
+  p->unit_end = (uint64_t)((u128)U * (r + 1) / W);
+  if (consumer == FS_CONSUMER_ROWS) {
+    p->row_begin = p->unit_begin;
+    p->row_end = p->unit_end;
+  }
+  // slice size
+  const uint64_t span = p->unit_end - p->unit_begin;
+  uint64_t T = e.slice_units;
+  if (T == 0) T = std::max<uint64_t>(1, ceil_div_u64(span, kTargetLanes * kSlicesPerLane));
+  T = std::min<uint64_t>(T, 1ull << 24);
+  if (consumer == FS_CONSUMER_ROWS) T = (T + 7) & ~7ull;
+  p->T = T;
+  p->num_slices = span ? ceil_div_u64(span, T) : 0;
+  return FS_OK;
+}
+
+void fs_plan_free_device(fs_plan *p) {
+  if (!p->uploaded) return;
+  int prev = -1;
+  cudaGetDevice(&prev);
+  cudaSetDevice(p->device);
+  if (p->U_dev) cudaFree(p->U_dev);
+  if (p->ktab_dev) cudaFree(p->ktab_dev);
+  if (p->scratch_dev) cudaFree(p->scratch_dev);
+  p->U_dev = nullptr;
+  p->ktab_dev = nullptr;
+  p->scratch_dev = nullptr;
+  p->uploaded = false;
+  if (prev >= 0) cudaSetDevice(prev);
+}
+
+int fs_plan_upload_impl(fs_plan *p) {
+  if (p->uploaded) return FS_OK;
+  int ndev = 0;
+  if (cudaGetDeviceCount(&ndev) != cudaSuccess || ndev <= 0) {
+    cudaGetLastError();
+    return FS_ENODEV;
+  }
+  int dev = p->ex.device;
+  if (dev < 0) {
+    if (cudaGetDevice(&dev) != cudaSuccess) return FS_ECUDA;
+  }
+  if (dev >= ndev) return FS_EINVAL;
+  if (cudaSetDevice(dev) != cudaSuccess) return FS_ECUDA;
+  p->device = dev;
+  p->stream = (cudaStream_t)p->ex.cuda_stream;
+  if (!p->U.empty()) {
+    if (cudaMalloc(&p->U_dev, p->U.size() * 8) != cudaSuccess) return FS_ENOMEM;
+    if (cudaMemcpyAsync(p->U_dev, p->U.data(), p->U.size() * 8, cudaMemcpyHostToDevice, p->stream) !=
+        cudaSuccess)
+      return FS_ECUDA;
+  }
+  if (!p->ktab.empty()) {
+    if (cudaMalloc(&p->ktab_dev, p->ktab.size() * 4) != cudaSuccess) return FS_ENOMEM;
+    if (cudaMemcpyAsync(p->ktab_dev, p->ktab.data(), p->ktab.size() * 4, cudaMemcpyHostToDevice,
+                        p->stream) != cudaSuccess)
+      return FS_ECUDA;
+  }
+  if (cudaMalloc(&p->scratch_dev, 256) != cudaSuccess) return FS_ENOMEM;
+  p->uploaded = true;
+  return FS_OK;
+}
+
+// ------------------------------------------------------------------ host model (tests only)
+namespace {
+
+struct HostSink {
+  int d = 0;
+  uint64_t count = 0;
+  uint64_t *hist = nullptr;
+  uint64_t hist_cap = 0;
+  int B = 0;
+  unsigned char *rows = nullptr;
+  uint64_t cap = 0;
+  uint64_t slice_rows = 0;
+  uint32_t first[FS_MAX_D];
+  bool have_first = false;
+  void put(const uint32_t *v) {
+    uint64_t len = 0;
+    for (int i = 0; i < d; ++i) len += v[i];
+    if (hist && len < hist_cap) hist[len]++;
+    if (rows && count < cap) {
+      const int w = B / 8;
+      unsigned char *q = rows + count * (uint64_t)d * w;
+      for (int i = 0; i < d; ++i)
+        for (int b = 0; b < w; ++b) q[i * w + b] = (unsigned char)((v[i] >> (8 * b)) & 0xff);
+    }
+    if (!have_first) {
+      memcpy(first, v, sizeof(uint32_t) * d);
+      have_first = true;
+    }
+    ++count;
+    ++slice_rows;
+  }
+};
+
+template <int D>
+struct HostEmit {
+  HostSink *sink;
+  FS_HD void operator()(const fs::Lane<D> &st) {
+#ifndef __CUDA_ARCH__
+    uint32_t v[FS_MAX_D];
+    for (int j = 0; j < D - 2; ++j) v[j] = st.a[j];
+    v[D - 2] = (uint32_t)st.cur;
+    v[D - 1] = st.ad;
+    sink->put(v);
+#endif
+  }
+};
+
+template <int D, int ALPHA>
+void host_model_d(const fs_plan *p, HostSink &sink, uint64_t *slice_counts, uint32_t *slice_first) {
+  const Consts &c = p->c;
+  const uint32_t *ktab = p->ktab.empty() ? nullptr : p->ktab.data();
+  for (uint64_t sl = 0; sl < p->num_slices; ++sl) {
+    uint64_t u = p->unit_begin + sl * p->T;
+    uint32_t budget = (uint32_t)std::min<uint64_t>(p->T, p->unit_end - u);
+    fs::Lane<D> st;
+    uint64_t off = fs::unrank<D, true>(st, c, ktab, u);
+    budget -= fs::position_in_node<D, true>(st, c, off);
+    sink.slice_rows = 0;
+    sink.have_first = false;
+    HostEmit<D> emit{&sink};
+    while (budget > 0) fs::step<D, true, ALPHA>(st, c, ktab, budget, emit);
+    if (slice_counts) slice_counts[sl] = sink.slice_rows;
+    if (slice_first) {
+      for (int i = 0; i < D; ++i) slice_first[sl * D + i] = sink.have_first ? sink.first[i] : 0xFFFFFFFFu;
+    }
+  }
+}
+
+template <int D>
+void host_model_alpha(const fs_plan *p, HostSink &sink, uint64_t *sc, uint32_t *sf) {
+  if (p->c.alpha)
+    host_model_d<D, 1>(p, sink, sc, sf);
+  else
+    host_model_d<D, 0>(p, sink, sc, sf);
+}
+
+}  // namespace
+
+extern "C" int fsdbg_host_model(const fs_plan *p, uint64_t *count_out, uint64_t *hist, uint64_t hist_cap,
+                                int B, void *rows, uint64_t cap, uint64_t *slice_counts,
+                                uint32_t *slice_first_row) {
+  if (!p) return FS_EINVAL;
+  if (rows && B != 16 && B != 32) return FS_EINVAL;
+  HostSink sink;
+  sink.d = p->d;
+  sink.hist = hist;
+  sink.hist_cap = hist_cap;
+  sink.B = B;
+  sink.rows = (unsigned char *)rows;
+  sink.cap = cap;
+  if (hist) memset(hist, 0, hist_cap * 8);
+  if (p->d == 1) {
+    // one slice, one unit at most
+    for (uint64_t sl = 0; sl < p->num_slices; ++sl) {
+      sink.slice_rows = 0;
+      sink.have_first = false;
+      uint32_t v = (uint32_t)(p->n / p->g[0]);
+      sink.put(&v);
+      if (slice_counts) slice_counts[sl] = sink.slice_rows;
+      if (slice_first_row) slice_first_row[sl] = v;
+    }
+  } else {
+    switch (p->d) {
+#define FS_CASE(DD) \
+  case DD:          \
+    host_model_alpha<DD>(p, sink, slice_counts, slice_first_row); \
+    break;
+      FS_CASE(2) FS_CASE(3) FS_CASE(4) FS_CASE(5) FS_CASE(6) FS_CASE(7) FS_CASE(8) FS_CASE(9)
+      FS_CASE(10) FS_CASE(11) FS_CASE(12) FS_CASE(13) FS_CASE(14) FS_CASE(15) FS_CASE(16)
+#undef FS_CASE
+      default:
+        return FS_EINVAL;
+    }
+  }
+  if (count_out) *count_out = sink.count;
+  return FS_OK;
+}
+
+namespace {
+template <int D>
+int unrank_host(const fs_plan *p, uint64_t unit, uint32_t *prefix_out, int64_t *row_out) {
+  fs::Lane<D> st;
+  const uint32_t *ktab = p->ktab.empty() ? nullptr : p->ktab.data();
+  uint64_t off = fs::unrank<D, true>(st, p->c, ktab, unit);
+  for (int j = 0; j < D - 2; ++j) prefix_out[j] = st.a[j];
+  if (p->c.alpha)
+    *row_out = off == 0 ? -1 : (int64_t)(off - 1);
+  else
+    *row_out = (int64_t)off;
+  return FS_OK;
+}
+}  // namespace
+
+extern "C" int fsdbg_unrank(const fs_plan *p, uint64_t unit, uint32_t *prefix_out, int64_t *row_in_node_out) {
+  if (!p || !prefix_out || !row_in_node_out) return FS_EINVAL;
+  if (unit >= p->total_units) return FS_ERANGE;
+  if (p->d == 1) {
+    *row_in_node_out = 0;
+    return FS_OK;
+  }
+  switch (p->d) {
+#define FS_CASE(DD) \
+  case DD:          \
+    return unrank_host<DD>(p, unit, prefix_out, row_in_node_out);
+    FS_CASE(2) FS_CASE(3) FS_CASE(4) FS_CASE(5) FS_CASE(6) FS_CASE(7) FS_CASE(8) FS_CASE(9)
+    FS_CASE(10) FS_CASE(11) FS_CASE(12) FS_CASE(13) FS_CASE(14) FS_CASE(15) FS_CASE(16)
+#undef FS_CASE
+  }
+  return FS_EINVAL;
+}
+
+extern "C" int fsdbg_magic(uint32_t g, uint32_t *m_out, uint32_t *sh_out) {
+  if (g == 0 || g >= (1u << 31)) return FS_EINVAL;
+  Div v = fs_make_div(g);
+  if (m_out) *m_out = v.m;
+  if (sh_out) *sh_out = v.sh;
+  return FS_OK;
+}
+
+extern "C" uint32_t fsdbg_magic_div(uint32_t x, uint32_t g) { return fs::divq(x, fs_make_div(g)); }

@@ -1,0 +1,81 @@
+// fs_internal.h -- plan object and kernel launch parameters shared by the host code
+// (fs_host.cu), the kernels (fs_kernels.cu) and the C ABI (fs_capi.cu).
+#pragma once
+
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include <vector>
+
+#include "../../include/fsgpu.h"
+#include "fs_core.cuh"
+
+namespace fs {
+
+constexpr int kBlock = 256;          // threads per persistent CTA
+constexpr int kStageBytes = 256;     // per-lane staging ring for materialise (2 x 128 B)
+constexpr uint32_t kKtabMax = 8192;  // k0 table in shared memory if g_{d-1} <= this
+constexpr uint32_t kHistSmemMax = 24576;  // u32 histogram bins kept in shared memory
+
+// Everything a kernel needs, by value (fits the 4 KB parameter space comfortably).
+struct KParams {
+  Consts c;
+  uint64_t unit0, unit1;     // this rank's unit range (global unit indices)
+  uint64_t T;                // units per slice
+  uint64_t num_slices;
+  uint64_t num_claims;       // num_slices, or the next power of two when claims are permuted
+  uint32_t claim_bits;       // log2(num_claims) when permuted
+  int permute;               // bit-reversed claim order (any-predicate)
+  unsigned long long *queue; // work-queue head (zeroed before launch)
+  // consumers
+  unsigned long long *count_out;
+  unsigned long long *hist_out;
+  uint32_t hist_len;
+  uint32_t hist_smem;        // 1: bins in shared memory
+  int pred;
+  uint64_t pred_arg;
+  int *found;
+  uint32_t *witness;
+  unsigned char *rows_out;
+  uint32_t row_bytes;
+};
+
+}  // namespace fs
+
+struct fs_plan {
+  uint64_t n = 0;
+  int d = 0;
+  int consumer = 0;
+  fs_exec_t ex{};
+  std::vector<uint32_t> g;
+  fs::Consts c{};                 // host copy (U/ktab point at host vectors)
+  std::vector<uint64_t> U;        // L * (n+1)
+  std::vector<uint32_t> ktab;     // g_{d-1} entries or empty
+  uint64_t total_units = 0, total_rows = 0;
+  uint64_t unit_begin = 0, unit_end = 0;
+  uint64_t row_begin = 0, row_end = 0;
+  uint64_t T = 1, num_slices = 0;
+  uint64_t hist_len = 0;
+  uint64_t nodes_per_level[FS_MAX_D] = {0};
+  // device side
+  int device = -1;
+  cudaStream_t stream = nullptr;
+  uint64_t *U_dev = nullptr;
+  uint32_t *ktab_dev = nullptr;
+  unsigned long long *scratch_dev = nullptr;  // [0] queue head, [1..] spare
+  bool uploaded = false;
+  uint32_t grid = 0, block = fs::kBlock;
+  int last_launches = 0;
+};
+
+// host helpers (fs_host.cu)
+int fs_validate_and_build(fs_plan *p, uint64_t n, const uint32_t *gens, int d, int consumer,
+                          const fs_exec_t *ex);
+int fs_plan_upload_impl(fs_plan *p);
+void fs_plan_free_device(fs_plan *p);
+fs::Div fs_make_div(uint32_t g);
+
+// kernel launchers (fs_kernels.cu); return FS_OK or an error
+int fs_launch(fs_plan *p, int consumer, int B, const fs::KParams &kp_template, cudaStream_t stream);
+int fs_occupancy_grid(fs_plan *p, int consumer, int B, uint32_t *grid_out);
+extern unsigned long long g_fs_total_launches;

@@ -1,0 +1,435 @@
+// fs_kernels.cu -- persistent sm_100a kernels: one successor stream per thread over DP-sized,
+// disjoint lex slices pulled from an atomic work queue (replaces the paper's host-side
+// splitWork + 1024-launch cadence), four consumers:
+//   COUNT  per-lane u32 slice counters -> u64 -> warp shuffle reduction -> 1 atomic / warp
+//   HIST   length histogram in shared-memory u32 bins (overflow-guarded) -> u64 global
+//   ANY    predicate, CAS-published witness, bit-reversed claim order + flag polling for
+//          early exit
+//   ROWS   packed u16/u32 rows at exact canonical offsets: per-lane 256 B shared-memory ring,
+//          completed 128 B halves copied warp-cooperatively with coalesced 16 B stores.
+// All integer ALU work; no tensor cores (the path is not a dense contraction).
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include "../../include/fsgpu.h"
+#include "fs_core.cuh"
+#include "fs_internal.h"
+
+unsigned long long g_fs_total_launches = 0;
+
+namespace fs {
+
+constexpr unsigned kFull = 0xffffffffu;
+
+template <int CONS>
+struct Inner {
+  static constexpr int value = (CONS == FS_CONSUMER_ROWS) ? 8 : 64;
+};
+
+// ---------------------------------------------------------------- consumers
+template <int D>
+struct EmitCount {
+  uint32_t n;
+  __device__ __forceinline__ void operator()(const Lane<D> &) { ++n; }
+};
+
+template <int D>
+struct EmitHist {
+  uint32_t *bins;
+  unsigned long long *gbins;
+  uint32_t smem;
+  uint32_t n;
+  __device__ __forceinline__ void operator()(const Lane<D> &st) {
+    const uint32_t l = st.lsum + (uint32_t)st.cur + st.ad;  // length = sum_i a_i
+    if (smem)
+      atomicAdd(&bins[l], 1u);
+    else
+      atomicAdd(&gbins[l], 1ull);
+    ++n;
+  }
+};
+
+template <int D>
+__device__ __forceinline__ uint32_t coord(const Lane<D> &st, uint32_t i) {
+  uint32_t v = st.ad;
+  if (i == D - 2) v = (uint32_t)st.cur;
+#pragma unroll
+  for (int j = 0; j < D - 2; ++j)
+    if (i == (uint32_t)j) v = st.a[j];
+  return v;
+}
+
+template <int D>
+struct EmitAny {
+  int pred;
+  uint64_t arg;
+  int *found;
+  uint32_t *wit;
+  bool hit;
+  __device__ __forceinline__ void operator()(const Lane<D> &st) {
+    const uint64_t len = (uint64_t)st.lsum + (uint32_t)st.cur + st.ad;
+    bool ok;
+    switch (pred) {
+      case FS_PRED_LEN_LE: ok = len <= arg; break;
+      case FS_PRED_LEN_GE: ok = len >= arg; break;
+      case FS_PRED_LEN_EQ: ok = len == arg; break;
+      default: {
+        const uint32_t i = (uint32_t)(arg >> 32);
+        ok = i < (uint32_t)D && coord<D>(st, i) >= (uint32_t)(arg & 0xffffffffu);
+      }
+    }
+    if (ok && !hit) {
+      hit = true;
+      if (atomicCAS(found, 0, 1) == 0 && wit) {
+#pragma unroll
+        for (int j = 0; j < D - 2; ++j) wit[j] = st.a[j];
+        wit[D - 2] = (uint32_t)st.cur;
+        wit[D - 1] = st.ad;
+      }
+    }
+  }
+};
+
+// Rows are appended to a per-lane 256 B ring in shared memory (lane-rotated by 4 B so that
+// lanes at equal positions hit distinct banks).  When a 128 B half completes it becomes
+// "pending" and the warp copies it to its exact canonical byte offset.
+template <int D, int B>
+struct EmitRows {
+  static constexpr uint32_t kRB = D * (B / 8);
+  unsigned char *ring;
+  uint32_t rot;
+  uint32_t wpos;        // bytes of the current slice written so far
+  uint64_t slice_goff;  // byte offset of the slice in the output
+  bool pend;
+  uint32_t pend_soff;
+  uint64_t pend_goff;
+  __device__ __forceinline__ void put(uint32_t p, int i, uint32_t v) {
+    if (B == 16)
+      *reinterpret_cast<uint16_t *>(ring + ((p + 2 * i + rot) & 255u)) = (uint16_t)v;
+    else
+      *reinterpret_cast<uint32_t *>(ring + ((p + 4 * i + rot) & 255u)) = v;
+  }
+  __device__ __forceinline__ void operator()(const Lane<D> &st) {
+    const uint32_t p = wpos;
+#pragma unroll
+    for (int j = 0; j < D - 2; ++j) put(p, j, st.a[j]);
+    put(p, D - 2, (uint32_t)st.cur);
+    put(p, D - 1, st.ad);
+    const uint32_t np = p + kRB;
+    wpos = np;
+    if ((p >> 7) != (np >> 7)) {
+      pend = true;
+      pend_soff = p & 128u;
+      pend_goff = slice_goff + (uint64_t)(p & ~127u);
+    }
+  }
+};
+
+// Warp-cooperative copy of every lane's pending ring segment: 4 segments per round, 8 lanes
+// x 16 B each -> fully coalesced 128 B stores.  len is a multiple of 16.
+__device__ __forceinline__ void warp_flush(bool &pend, uint32_t soff, uint64_t goff, uint32_t len,
+                                           const unsigned char *warp_stage, unsigned char *out) {
+  unsigned pm = __ballot_sync(kFull, pend);
+  if (!pm) return;
+  const int lane = threadIdx.x & 31, sub = lane >> 3, j = lane & 7;
+  while (pm) {
+    unsigned m = pm;
+#pragma unroll
+    for (int x = 0; x < 3; ++x)
+      if (x < sub) m &= m - 1;
+    const int src = m ? (__ffs(m) - 1) : -1;
+    const int sl = src < 0 ? 0 : src;
+    const uint32_t s_soff = __shfl_sync(kFull, soff, sl);
+    const uint32_t s_len = __shfl_sync(kFull, len, sl);
+    const uint64_t s_goff = __shfl_sync(kFull, goff, sl);
+    if (src >= 0 && (uint32_t)j * 16u < s_len) {
+      const unsigned char *r = warp_stage + src * kStageBytes;
+      const uint32_t base = s_soff + (uint32_t)j * 16u + 4u * (uint32_t)src;
+      uint4 v;
+      v.x = *reinterpret_cast<const uint32_t *>(r + (base & 255u));
+      v.y = *reinterpret_cast<const uint32_t *>(r + ((base + 4u) & 255u));
+      v.z = *reinterpret_cast<const uint32_t *>(r + ((base + 8u) & 255u));
+      v.w = *reinterpret_cast<const uint32_t *>(r + ((base + 12u) & 255u));
+      __stcs(reinterpret_cast<uint4 *>(out + s_goff + (uint64_t)j * 16u), v);
+    }
+#pragma unroll
+    for (int x = 0; x < 4; ++x) pm &= pm ? pm - 1 : 0u;
+  }
+  pend = false;
+}
+
+__device__ __forceinline__ uint64_t bitrev_bits(uint64_t x, uint32_t bits) {
+  return bits ? (__brevll(x) >> (64 - bits)) : 0ull;
+}
+
+template <int D, int CONS, int B>
+__global__ void __launch_bounds__(kBlock) fs_enum_kernel(const KParams P) {
+  constexpr bool NEED_AD = CONS != FS_CONSUMER_COUNT;
+  constexpr int ALPHA = CONS == FS_CONSUMER_ROWS ? 0 : 1;
+  constexpr int INNER = Inner<CONS>::value;
+  extern __shared__ __align__(16) unsigned char smem[];
+  __shared__ unsigned int hist_guard;
+  const Consts &c = P.c;
+
+  uint32_t *ktab_s = reinterpret_cast<uint32_t *>(smem);
+  const uint32_t kt_words = (c.ktab_len + 3u) & ~3u;
+  uint32_t *hist_s = ktab_s + kt_words;
+  const uint32_t hist_words = (CONS == FS_CONSUMER_HIST && P.hist_smem) ? ((P.hist_len + 3u) & ~3u) : 0u;
+  unsigned char *stage = reinterpret_cast<unsigned char *>(hist_s + hist_words);
+
+  for (uint32_t i = threadIdx.x; i < c.ktab_len; i += blockDim.x) ktab_s[i] = c.ktab[i];
+  if (CONS == FS_CONSUMER_HIST) {
+    for (uint32_t i = threadIdx.x; i < hist_words; i += blockDim.x) hist_s[i] = 0u;
+    if (threadIdx.x == 0) hist_guard = 0u;
+  }
+  __syncthreads();
+
+  const uint32_t *kt = ktab_s;
+  const int lane = threadIdx.x & 31;
+  Lane<D> st;
+  st.cur = -1;
+  st.ad = 0;
+  uint32_t budget = 0;
+  bool alive = true;
+  uint64_t acc = 0;
+
+  EmitCount<D> e_count{0};
+  EmitHist<D> e_hist{hist_s, P.hist_out, P.hist_smem, 0};
+  EmitAny<D> e_any{P.pred, P.pred_arg, P.found, P.witness, false};
+  EmitRows<D, B> e_rows;
+  e_rows.ring = stage + threadIdx.x * kStageBytes;
+  e_rows.rot = 4u * (uint32_t)lane;
+  e_rows.wpos = 0;
+  e_rows.slice_goff = 0;
+  e_rows.pend = false;
+  e_rows.pend_soff = 0;
+  e_rows.pend_goff = 0;
+  bool fin = false;
+  uint32_t fin_soff = 0, fin_len = 0;
+  uint64_t fin_goff = 0;
+  const unsigned char *warp_stage = stage + (threadIdx.x & ~31) * kStageBytes;
+
+  for (;;) {
+    const bool need = alive && budget == 0;
+    const unsigned needm = __ballot_sync(kFull, need);
+    if (needm) {
+      if (need) {
+        if (CONS == FS_CONSUMER_COUNT) {
+          acc += e_count.n;
+          e_count.n = 0;
+        } else if (CONS == FS_CONSUMER_HIST) {
+          const uint32_t rows = e_hist.n;
+          e_hist.n = 0;
+          if (P.hist_smem && rows) {
+            // overflow guard: every 2^30 rows added to this CTA, drain the u32 bins
+            const uint32_t old = atomicAdd(&hist_guard, rows);
+            if ((old >> 30) != ((old + rows) >> 30)) {
+              for (uint32_t i = 0; i < P.hist_len; ++i) {
+                const uint32_t v = atomicExch(&hist_s[i], 0u);
+                if (v) atomicAdd(&P.hist_out[i], (unsigned long long)v);
+              }
+            }
+          }
+        }
+      }
+      const int leader = __ffs(needm) - 1;
+      unsigned long long base = 0;
+      if (lane == leader) base = atomicAdd(P.queue, (unsigned long long)__popc(needm));
+      base = __shfl_sync(kFull, base, leader);
+      if (need) {
+        const uint64_t idx = base + (uint64_t)__popc(needm & ((1u << lane) - 1u));
+        if (idx >= P.num_claims) {
+          alive = false;
+        } else {
+          const uint64_t sl = P.permute ? bitrev_bits(idx, P.claim_bits) : idx;
+          if (sl < P.num_slices) {
+            const uint64_t u = P.unit0 + sl * P.T;
+            const uint64_t e = u + P.T < P.unit1 ? u + P.T : P.unit1;
+            budget = (uint32_t)(e - u);
+            const uint64_t off = unrank<D, NEED_AD>(st, c, kt, u);
+            budget -= position_in_node<D, NEED_AD>(st, c, off);
+            if (CONS == FS_CONSUMER_ROWS) {
+              e_rows.slice_goff = (u - P.unit0) * (uint64_t)EmitRows<D, B>::kRB;
+              e_rows.wpos = 0;
+            }
+          }
+        }
+      }
+    }
+    if (CONS == FS_CONSUMER_ANY) {
+      int f = 0;
+      if (lane == 0) f = *reinterpret_cast<volatile int *>(P.found);
+      f = __shfl_sync(kFull, f, 0);
+      if (f) {
+        alive = false;
+        budget = 0;
+      }
+    }
+    if (__ballot_sync(kFull, alive) == 0) break;
+
+#pragma unroll 1
+    for (int it = 0; it < INNER; ++it) {
+      if (budget > 0) {
+        if (CONS == FS_CONSUMER_COUNT) {
+          step<D, NEED_AD, ALPHA>(st, c, kt, budget, e_count);
+        } else if (CONS == FS_CONSUMER_HIST) {
+          step<D, NEED_AD, ALPHA>(st, c, kt, budget, e_hist);
+        } else if (CONS == FS_CONSUMER_ANY) {
+          step<D, NEED_AD, ALPHA>(st, c, kt, budget, e_any);
+          if (e_any.hit) {
+            budget = 0;
+            alive = false;
+          }
+        } else {
+          step<D, NEED_AD, ALPHA>(st, c, kt, budget, e_rows);
+          if (budget == 0) {
+            // slice done: flush the partial half (16 B-aligned part cooperatively, the
+            // ragged tail -- only at the end of the rank's block -- byte by byte)
+            const uint32_t w = e_rows.wpos;
+            const uint32_t hstart = w & ~127u;
+            const uint32_t plen = w - hstart;
+            const uint32_t alen = plen & ~15u;
+            for (uint32_t b = alen; b < plen; ++b)
+              P.rows_out[e_rows.slice_goff + hstart + b] = e_rows.ring[(hstart + b + e_rows.rot) & 255u];
+            if (alen) {
+              fin = true;
+              fin_soff = hstart & 128u;
+              fin_goff = e_rows.slice_goff + hstart;
+              fin_len = alen;
+            }
+          }
+        }
+      }
+      if (CONS == FS_CONSUMER_ROWS) {
+        warp_flush(e_rows.pend, e_rows.pend_soff, e_rows.pend_goff, 128u, warp_stage, P.rows_out);
+        warp_flush(fin, fin_soff, fin_goff, fin_len, warp_stage, P.rows_out);
+      }
+    }
+  }
+
+  // ---------------------------------------------------------------- epilogue
+  if (CONS == FS_CONSUMER_COUNT) {
+    acc += e_count.n;
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) acc += __shfl_xor_sync(kFull, acc, o);
+    if (lane == 0 && acc) atomicAdd(P.count_out, (unsigned long long)acc);
+  }
+  if (CONS == FS_CONSUMER_HIST && P.hist_smem) {
+    __syncthreads();
+    for (uint32_t i = threadIdx.x; i < P.hist_len; i += blockDim.x) {
+      const uint32_t v = hist_s[i];
+      if (v) atomicAdd(&P.hist_out[i], (unsigned long long)v);
+    }
+  }
+}
+
+// d = 1: Z(n,(g)) = {(n/g)} iff g | n.  One thread; the rank owning unit 0 emits it.
+template <int CONS, int B>
+__global__ void fs_d1_kernel(const KParams P) {
+  if (threadIdx.x != 0 || blockIdx.x != 0) return;
+  if (!(P.unit0 == 0 && P.unit1 > 0)) return;
+  const uint32_t x = P.c.n / P.c.g[0];
+  if (CONS == FS_CONSUMER_COUNT) atomicAdd(P.count_out, 1ull);
+  if (CONS == FS_CONSUMER_HIST) atomicAdd(&P.hist_out[x], 1ull);
+  if (CONS == FS_CONSUMER_ANY) {
+    bool ok;
+    switch (P.pred) {
+      case FS_PRED_LEN_LE: ok = x <= P.pred_arg; break;
+      case FS_PRED_LEN_GE: ok = x >= P.pred_arg; break;
+      case FS_PRED_LEN_EQ: ok = x == P.pred_arg; break;
+      default: ok = (P.pred_arg >> 32) == 0 && x >= (uint32_t)(P.pred_arg & 0xffffffffu);
+    }
+    if (ok && atomicCAS(P.found, 0, 1) == 0 && P.witness) P.witness[0] = x;
+  }
+  if (CONS == FS_CONSUMER_ROWS) {
+    if (B == 16)
+      *reinterpret_cast<uint16_t *>(P.rows_out) = (uint16_t)x;
+    else
+      *reinterpret_cast<uint32_t *>(P.rows_out) = x;
+  }
+}
+
+static size_t smem_bytes(const KParams &kp, int consumer) {
+  size_t b = (size_t)((kp.c.ktab_len + 3u) & ~3u) * 4;
+  if (consumer == FS_CONSUMER_HIST && kp.hist_smem) b += (size_t)((kp.hist_len + 3u) & ~3u) * 4;
+  if (consumer == FS_CONSUMER_ROWS) b += (size_t)kBlock * kStageBytes;
+  return b;
+}
+
+template <int D, int CONS, int B>
+static int launch_t(fs_plan *p, const KParams &kp, cudaStream_t stream, bool query_only, uint32_t *grid_out) {
+  auto kern = fs_enum_kernel<D, CONS, B>;
+  const size_t smem = smem_bytes(kp, CONS);
+  if (cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem) != cudaSuccess)
+    return FS_ECUDA;
+  int per_sm = 0;
+  if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, kBlock, smem) != cudaSuccess) return FS_ECUDA;
+  if (per_sm < 1) return FS_ECUDA;
+  if (p->ex.ctas_per_sm > 0 && p->ex.ctas_per_sm < per_sm) per_sm = p->ex.ctas_per_sm;
+  int sms = 0;
+  if (cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, p->device) != cudaSuccess) return FS_ECUDA;
+  uint64_t grid = (uint64_t)sms * (uint64_t)per_sm;
+  // never more CTAs than the slices can feed
+  const uint64_t need_ctas = (kp.num_claims + kBlock - 1) / kBlock;
+  if (grid > need_ctas) grid = need_ctas ? need_ctas : 1;
+  if (grid_out) *grid_out = (uint32_t)grid;
+  if (query_only) return FS_OK;
+  kern<<<(unsigned)grid, kBlock, smem, stream>>>(kp);
+  if (cudaGetLastError() != cudaSuccess) return FS_ECUDA;
+  ++g_fs_total_launches;
+  return FS_OK;
+}
+
+template <int CONS, int B>
+static int launch_d1(const KParams &kp, cudaStream_t stream, bool query_only, uint32_t *grid_out) {
+  if (grid_out) *grid_out = 1;
+  if (query_only) return FS_OK;
+  fs_d1_kernel<CONS, B><<<1, 32, 0, stream>>>(kp);
+  if (cudaGetLastError() != cudaSuccess) return FS_ECUDA;
+  ++g_fs_total_launches;
+  return FS_OK;
+}
+
+template <int CONS, int B>
+static int dispatch_d(fs_plan *p, const KParams &kp, cudaStream_t s, bool q, uint32_t *g) {
+  switch (p->d) {
+    case 1: return launch_d1<CONS, B>(kp, s, q, g);
+#define FS_CASE(DD) \
+  case DD:          \
+    return launch_t<DD, CONS, B>(p, kp, s, q, g);
+    FS_CASE(2) FS_CASE(3) FS_CASE(4) FS_CASE(5) FS_CASE(6) FS_CASE(7) FS_CASE(8) FS_CASE(9)
+    FS_CASE(10) FS_CASE(11) FS_CASE(12) FS_CASE(13) FS_CASE(14) FS_CASE(15) FS_CASE(16)
+#undef FS_CASE
+  }
+  return FS_EINVAL;
+}
+
+static int dispatch(fs_plan *p, int consumer, int B, const KParams &kp, cudaStream_t s, bool q, uint32_t *g) {
+  switch (consumer) {
+    case FS_CONSUMER_COUNT: return dispatch_d<FS_CONSUMER_COUNT, 16>(p, kp, s, q, g);
+    case FS_CONSUMER_HIST: return dispatch_d<FS_CONSUMER_HIST, 16>(p, kp, s, q, g);
+    case FS_CONSUMER_ANY: return dispatch_d<FS_CONSUMER_ANY, 16>(p, kp, s, q, g);
+    case FS_CONSUMER_ROWS:
+      return B == 16 ? dispatch_d<FS_CONSUMER_ROWS, 16>(p, kp, s, q, g)
+                     : dispatch_d<FS_CONSUMER_ROWS, 32>(p, kp, s, q, g);
+  }
+  return FS_EINVAL;
+}
+
+}  // namespace fs
+
+int fs_launch(fs_plan *p, int consumer, int B, const fs::KParams &kp, cudaStream_t stream) {
+  uint32_t grid = 0;
+  int rc = fs::dispatch(p, consumer, B, kp, stream, false, &grid);
+  if (rc == FS_OK) p->grid = grid;
+  return rc;
+}
+
+int fs_occupancy_grid(fs_plan *p, int consumer, int B, uint32_t *grid_out) {
+  fs::KParams kp{};
+  kp.c = p->c;
+  kp.num_claims = p->num_slices;
+  kp.hist_len = (uint32_t)p->hist_len;
+  kp.hist_smem = p->hist_len <= fs::kHistSmemMax;
+  return fs::dispatch(p, consumer, B, kp, nullptr, true, grid_out);
+}

@@ -1,0 +1,242 @@
+"""GPU parity: the CUDA path, called through the C ABI (python binding), against the oracle
+on the same seeded inputs.  Integer results must be bit-exact; rows byte-identical."""
+import hashlib
+import json
+import os
+import random
+import struct
+
+import pytest
+
+import oracle
+from oracle import gf
+from paper_2405_07989_b200 import _lib as L
+from paper_2405_07989_b200 import api
+from paper_2405_07989_b200 import workloads as W
+
+torch = pytest.importorskip("torch")
+pytestmark = pytest.mark.gpu
+
+GOLD = os.path.join(os.path.dirname(os.path.abspath(__file__)), "golden")
+
+
+def gold(name):
+    with open(os.path.join(GOLD, name + ".json")) as f:
+        return json.load(f)
+
+
+def rows_bytes(t):
+    return t.contiguous().cpu().numpy().tobytes()
+
+
+def hist_list(t, L_):
+    return [int(x) for x in t[:L_].cpu().tolist()]
+
+
+def suite(count, seed, d_max, g_max, n_max, max_rows):
+    out = []
+    for inst in W.random_instances(count * 4, seed=seed, d_max=d_max, g_max=g_max, n_max=n_max):
+        if gf.count(inst.n, inst.gens) <= max_rows:
+            out.append(inst)
+        if len(out) == count:
+            break
+    return out
+
+
+EDGE = [W.Instance("n0", 0, (3, 5, 7)), W.Instance("n0d1", 0, (4,)), W.Instance("d1", 12, (4,)),
+        W.Instance("d1x", 13, (4,)), W.Instance("d2", 1000, (6, 10)), W.Instance("d2c", 997, (1, 1)),
+        W.Instance("rep", 30, (2, 2, 2, 2)), W.Instance("empty", 7, (4, 6)), W.Instance("lt", 2, (3, 5, 7)),
+        W.Instance("ones", 12, (1, 1, 1, 1, 1)), W.Instance("unsorted", 200, (20, 6, 9)),
+        W.Instance("biglast", 500, (3, 7, 499)), W.Instance("g1last", 40, (5, 7, 1)),
+        W.Instance("d16", 40, tuple(range(2, 18))), W.Instance("d16b", 120, (3,) * 8 + (5,) * 8),
+        W.Instance("huge_gA", 60000, (7, 9000, 11)), W.Instance("huge_s", 70000, (3, 5, 65537)),
+        W.Instance("C1", 1000, (6, 9, 20)), W.Instance("McN44", 44, (6, 9, 20))]
+RAND = suite(50, seed=0, d_max=8, g_max=40, n_max=400, max_rows=300000)
+ALL = EDGE + RAND
+ids = lambda i: "%s_%d_%s" % (i.name, i.n, "-".join(map(str, i.gens)))
+
+
+@pytest.mark.parametrize("inst", ALL, ids=ids)
+def test_count_hist_rows(oracle_mod, inst):
+    n, g = inst.n, inst.gens
+    want = oracle.run(n, g, hist_len=oracle.hist_len_for(n, g))
+    assert api.fs_count(n, g) == want["count"]
+    h = api.fs_length_set(n, g)
+    assert hist_list(h, len(want["hist"])) == want["hist"]
+    for B in (16, 32):
+        if B == 16 and max(n // x for x in g) > 65535:
+            with pytest.raises(OverflowError):
+                api.fs_enumerate(n, g, B=B)
+            continue
+        total, rows = api.fs_enumerate(n, g, B=B)
+        assert total == want["count"]
+        assert rows_bytes(rows) == oracle.rows(n, g, B=B)
+
+
+@pytest.mark.parametrize("inst", ALL[:30], ids=ids)
+@pytest.mark.parametrize("T", [1, 5])
+def test_tiny_slices(oracle_mod, inst, T):
+    """Force many tiny slices: per-slice boundaries must neither lose nor duplicate rows."""
+    n, g = inst.n, inst.gens
+    want = oracle.run(n, g, hist_len=oracle.hist_len_for(n, g))
+    assert api.fs_count_ex(n, g, slice_units=T) == want["count"]
+    h = api.fs_length_set_ex(n, g, slice_units=T)
+    assert hist_list(h, len(want["hist"])) == want["hist"]
+    rows, off, t = api.fs_enumerate_ex(n, g, B=32, slice_units=8 * T)
+    assert rows == want["count"] and off == 0
+    assert rows_bytes(t) == oracle.rows(n, g, B=32)
+
+
+@pytest.mark.parametrize("inst", ALL[:40], ids=ids)
+def test_any(oracle_mod, inst):
+    n, g = inst.n, inst.gens
+    rows = oracle.rows_as_tuples(oracle.rows(n, g, B=32), len(g), 32)
+    lens = sorted(sum(r) for r in rows)
+    preds = [(L.FS_PRED_LEN_LE, lens[0] if lens else 0), (L.FS_PRED_LEN_LE, max(0, (lens[0] if lens else 1) - 1)),
+             (L.FS_PRED_LEN_GE, lens[-1] if lens else 0), (L.FS_PRED_LEN_EQ, lens[len(lens) // 2] if lens else 3),
+             (L.FS_PRED_COORD_GE, ((len(g) - 1) << 32) | 2), (L.FS_PRED_COORD_GE, (0 << 32) | 1)]
+    for pred, arg in preds:
+        want = any(oracle.pred_holds(r, pred, arg) for r in rows)
+        found, wit = api.fs_any(n, g, pred, arg)
+        assert found == want, (pred, arg)
+        if found:
+            assert sum(a * b for a, b in zip(wit, g)) == n
+            assert oracle.pred_holds(wit, pred, arg)
+            assert tuple(wit) in set(rows)
+
+
+def test_cap_truncation(oracle_mod):
+    n, g = W.C2.n, W.C2.gens
+    full = oracle.rows(n, g, B=16)
+    rb = 2 * len(g)
+    for cap in (0, 1, 7, 8, 9, 1000, 12345, 681151):
+        total, t = api.fs_enumerate(n, g, B=16, cap=cap)
+        assert total == 681152
+        assert rows_bytes(t) == full[: cap * rb]
+
+
+def test_c2_rows_golden(oracle_mod):
+    n, g = W.C2.n, W.C2.gens
+    for B, sha in ((16, "af101488b41676e1839ebcca06e795af9c2a2d2b278c6f7e0e584315721eb01e"),
+                   (32, "bf19f5cf473192f1055dba45a72442114f083eb5f912b14b8ee16e513ebf2ffd")):
+        total, t = api.fs_enumerate(n, g, B=B)
+        b = rows_bytes(t)
+        assert b == oracle.rows(n, g, B=B)
+        assert hashlib.sha256(b).hexdigest() == sha
+
+
+def test_c1_all_consumers(oracle_mod):
+    n, g = W.C1.n, W.C1.gens
+    assert api.fs_count(n, g) == 465
+    h = api.fs_length_set(n, g)
+    assert hist_list(h, 167) == gold("C1")["hist"]
+    total, t = api.fs_enumerate(n, g, B=16)
+    assert rows_bytes(t) == oracle.rows(n, g, B=16)
+
+
+@pytest.mark.parametrize("world", [2, 3, 8])
+def test_virtual_ranks(oracle_mod, world):
+    """Rank r of W run one after another on one GPU: partials combine to the whole."""
+    for inst in [W.C1, W.C2] + RAND[:8]:
+        n, g = inst.n, inst.gens
+        want = oracle.run(n, g, hist_len=oracle.hist_len_for(n, g))
+        assert sum(api.fs_count_ex(n, g, rank=r, world=world) for r in range(world)) == want["count"]
+        hs = [api.fs_length_set_ex(n, g, rank=r, world=world) for r in range(world)]
+        assert hist_list(sum(hs), len(want["hist"])) == want["hist"]
+        blob, nxt = b"", 0
+        for r in range(world):
+            rows, off, t = api.fs_enumerate_ex(n, g, B=16, rank=r, world=world)
+            assert off == nxt
+            nxt += rows
+            blob += rows_bytes(t)
+        assert blob == oracle.rows(n, g, B=16)
+
+
+# ------------------------------------------------------------------ full-size configs
+def test_c3_count_full():
+    assert api.fs_count(W.C3.n, W.C3.gens) == gold("C3")["count"] == 100032405189
+
+
+def test_c4_hist_full():
+    h = api.fs_length_set(W.C4.n, W.C4.gens)
+    assert hist_list(h, 329) == gold("C3")["hist"]
+
+
+@pytest.mark.parametrize("world", [2, 8])
+def test_c4_virtual_ranks(world):
+    hs = [api.fs_length_set_ex(W.C4.n, W.C4.gens, rank=r, world=world) for r in range(world)]
+    assert hist_list(sum(hs), 329) == gold("C3")["hist"]
+
+
+def test_c5_count_hist_full():
+    g = gold("C5")
+    assert api.fs_count(W.C5.n, W.C5.gens) == g["count"] == 4055053706
+    h = api.fs_length_set(W.C5.n, W.C5.gens)
+    assert hist_list(h, 20001) == g["hist"]
+
+
+def test_c5_any_predicates():
+    n, g = W.C5.n, W.C5.gens
+    found, wit = api.fs_any(n, g, L.FS_PRED_LEN_LE, 20)      # P_late: unique witness, lex-last row
+    assert found and wit == [0, 0, 0, 0, 20]
+    found, wit = api.fs_any(n, g, L.FS_PRED_LEN_LE, 19)      # P_none
+    assert not found and wit is None
+    found, wit = api.fs_any(n, g, L.FS_PRED_LEN_GE, 19995)   # P_first
+    assert found and sum(wit) >= 19995 and sum(a * b for a, b in zip(wit, g)) == n
+
+
+def test_c2l_rows_sampled(oracle_mod):
+    """C2-L (824,598,466 rows, 8.25 GB of u16): sampled prefix boxes equal the oracle's box
+    rows at the GF-computed canonical offsets; global invariants checked on the device."""
+    n, g = W.C2L.n, W.C2L.gens
+    total, t = api.fs_enumerate(n, g, B=16)
+    assert total == 824598466 and t.shape == (total, 5)
+    rng = random.Random(0)
+    for _ in range(6):
+        a1 = rng.randint(0, n // g[0])
+        a2 = rng.randint(0, (n - a1 * g[0]) // g[1])
+        box = ((a1,), a2, a2)
+        want = oracle.rows(n, g, B=16, box=box)
+        off = gf.rows_before_prefix(n, g, (a1, a2))
+        cnt = len(want) // 10
+        assert rows_bytes(t[off:off + cnt]) == want
+    # every row sums to n; strictly decreasing lex (checked in chunks on the GPU)
+    gt = torch.tensor(g, dtype=torch.int64, device="cuda")
+    chunk = 1 << 26
+    prev = None
+    for s in range(0, total, chunk):
+        x = t[s:s + chunk].to(torch.int64)
+        assert bool(((x * gt).sum(1) == n).all())
+        if prev is not None:
+            x = torch.cat([prev, x])
+        key = x[:, 0] * (1 << 48) + x[:, 1] * (1 << 36) + x[:, 2] * (1 << 24) + x[:, 3] * (1 << 12) + x[:, 4]
+        assert bool((key[1:] < key[:-1]).all())
+        prev = x[-1:]
+    del t
+    torch.cuda.empty_cache()
+
+
+def test_plan_async_and_launch_count():
+    p = api.Plan(W.C2.n, W.C2.gens, L.FS_CONSUMER_COUNT)
+    out = torch.zeros(1, dtype=torch.int64, device="cuda")
+    before = L.lib().fsdbg_total_launches()
+    for _ in range(3):
+        p.count_async(out)
+        assert p.last_launches() == 1
+    torch.cuda.synchronize()
+    assert int(out.item()) == 681152
+    assert L.lib().fsdbg_total_launches() - before == 3
+
+
+def test_errors_on_gpu():
+    with pytest.raises(ValueError):
+        api.fs_count(10, (2, 0))
+    with pytest.raises(OverflowError):
+        api.fs_enumerate(70000, (1, 2), B=16)
+    t = torch.empty(100, dtype=torch.uint8, device="cuda")
+    with pytest.raises(ValueError):  # misaligned output
+        L.check(L.lib().fs_enumerate(10, (api.ctypes.c_uint32 * 2)(2, 3), 2, 16,
+                                     api.ctypes.c_void_p(t.data_ptr() + 2), 2))
+    h = torch.empty(3, dtype=torch.int64, device="cuda")
+    with pytest.raises(ValueError):  # hist_cap too small
+        api.fs_length_set(100, (3, 5), hist=h)

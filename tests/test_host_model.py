@@ -1,0 +1,173 @@
+"""CPU checks of the CUDA path's host logic: the exact DP tables, slice unranking, the
+per-lane successor (csrc/fs_core.cuh, executed on the host by fsdbg_host_model) and the
+W-way partition, all against the oracle.  No GPU needed; no kernel is launched."""
+import random
+
+import pytest
+
+import oracle
+from oracle import gf
+from paper_2405_07989_b200 import _lib as L
+from paper_2405_07989_b200 import workloads as W
+from paper_2405_07989_b200.api import Plan
+
+from .fsdbg import host_model, magic, unrank
+
+
+def small_instances(count, seed, d_max=6, g_max=30, n_max=300, max_rows=20000):
+    out = []
+    for inst in W.random_instances(count * 3, seed=seed, d_max=d_max, g_max=g_max, n_max=n_max):
+        if gf.count(inst.n, inst.gens) <= max_rows:
+            out.append(inst)
+        if len(out) == count:
+            break
+    out += [W.Instance("n0", 0, (3, 5, 7)), W.Instance("d1", 12, (4,)), W.Instance("d1x", 13, (4,)),
+            W.Instance("d2", 100, (6, 10)), W.Instance("rep", 30, (2, 2, 2, 2)),
+            W.Instance("empty", 7, (4, 6)), W.Instance("ones", 12, (1, 1, 1, 1, 1)),
+            W.Instance("unsorted", 200, (20, 6, 9)), W.Instance("big_last", 500, (3, 7, 499)),
+            W.Instance("g1_last", 40, (5, 7, 1)), W.Instance("C1", 1000, (6, 9, 20))]
+    return out
+
+
+INSTANCES = small_instances(60, seed=0)
+
+
+def test_library_exports_every_declared_symbol():
+    import re
+    import os
+    lib = L.lib()
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    names = set()
+    for h in ("fsgpu.h", "fsgpu_debug.h"):
+        src = open(os.path.join(root, "include", h)).read()
+        names |= set(re.findall(r"\b((?:fs|fsdbg)_[a-z0-9_]+)\s*\(", src))
+    assert len(names) >= 20
+    for nm in sorted(names):
+        assert hasattr(lib, nm), nm
+    assert lib.fs_version() == 10000
+    assert set(L.EXPORTS) <= names
+
+
+@pytest.mark.parametrize("inst", INSTANCES, ids=lambda i: "%s_%d_%s" % (i.name, i.n, "-".join(map(str, i.gens))))
+def test_host_model_matches_oracle(oracle_mod, inst):
+    n, g = inst.n, inst.gens
+    want_rows = oracle.rows(n, g, B=32)
+    want_hist = oracle.hist(n, g)
+    for T in (0, 1, 3):
+        r = host_model(n, g, L.FS_CONSUMER_COUNT, slice_units=T, want_hist=True, want_rows=True, B=32)
+        assert r["count"] == len(want_rows) // (4 * len(g))
+        assert r["info"]["total_rows"] == r["count"]
+        assert r["hist"] == want_hist
+        # count-sliced plans visit slices in order, so rows come out canonical too
+        assert r["rows"] == want_rows
+    for T in (8, 16):
+        r = host_model(n, g, L.FS_CONSUMER_ROWS, slice_units=T, want_rows=True, B=32)
+        assert r["rows"] == want_rows
+
+
+@pytest.mark.parametrize("inst", INSTANCES[:30], ids=lambda i: "%s" % i.name)
+def test_slices_exact_and_gap_free(oracle_mod, inst):
+    """Per-slice row counts equal the oracle's rows in that lex range: no gaps, no overlap."""
+    n, g = inst.n, inst.gens
+    rows = oracle.rows_as_tuples(oracle.rows(n, g, B=32), len(g), 32)
+    r = host_model(n, g, L.FS_CONSUMER_COUNT, slice_units=2, want_slices=True, want_rows=True, B=32)
+    assert sum(r["slice_counts"]) == len(rows)
+    pos = 0
+    for cnt, first in zip(r["slice_counts"], r["slice_first"]):
+        if cnt:
+            assert rows[pos] == first
+        pos += cnt
+    # row-sliced plans: every slice holds exactly T rows except the last
+    rr = host_model(n, g, L.FS_CONSUMER_ROWS, slice_units=8, want_slices=True)
+    sc = rr["slice_counts"]
+    assert all(c == 8 for c in sc[:-1]) and (not sc or 1 <= sc[-1] <= 8)
+
+
+@pytest.mark.parametrize("world", [2, 3, 8])
+def test_partition_concatenates(oracle_mod, world):
+    for inst in INSTANCES[:25]:
+        n, g = inst.n, inst.gens
+        want = oracle.rows(n, g, B=16)
+        got = b""
+        total = 0
+        for rank in range(world):
+            r = host_model(n, g, L.FS_CONSUMER_ROWS, rank=rank, world=world, want_rows=True, B=16)
+            info = r["info"]
+            assert info["row_begin"] == total
+            total += r["count"]
+            got += r["rows"]
+        assert got == want
+        # count plans: partial counts sum to |Z|
+        s = sum(host_model(n, g, L.FS_CONSUMER_COUNT, rank=k, world=world)["count"] for k in range(world))
+        assert s == gf.count(n, g)
+
+
+def test_unrank_rows_equals_oracle_row(oracle_mod):
+    rng = random.Random(0)
+    for inst in INSTANCES[:30]:
+        n, g = inst.n, inst.gens
+        d = len(g)
+        if d < 2:
+            continue
+        rows = oracle.rows_as_tuples(oracle.rows(n, g, B=32), d, 32)
+        if not rows:
+            continue
+        p = Plan(n, g, L.FS_CONSUMER_ROWS)
+        for r in rng.sample(range(len(rows)), min(10, len(rows))):
+            prefix, j = unrank(p, r)
+            assert tuple(prefix) == rows[r][: d - 2]
+            # row j of the node: the valid a_{d-1} values are a*, a*-s, ...
+            same = [x for x in rows if x[: d - 2] == rows[r][: d - 2]]
+            assert same[j] == rows[r]
+
+
+def test_dp_totals_and_nodes(oracle_mod):
+    for inst in INSTANCES:
+        n, g = inst.n, inst.gens
+        info = Plan(n, g).info
+        assert info["total_rows"] == gf.count(n, g)
+        d = len(g)
+        if d >= 2:
+            # nodes at level k = #(a_1..a_k) with sum <= n = sum_{r<=n} |Z(r, g_1..g_k)|
+            for k, nk in enumerate(info["nodes_per_level"]):
+                assert nk == sum(gf.count_table(n, g[:k])) if k else nk == 1
+            assert info["total_units"] == info["nodes_per_level"][d - 2] + info["total_rows"]
+
+
+def test_full_size_plans():
+    """Plans of the full-size configs: exact totals (vs oracle.gf) and slice sizing."""
+    for name in ("C2", "C2L", "C2XL", "C3", "C5"):
+        inst = W.CONFIGS[name]
+        info = Plan(inst.n, inst.gens).info
+        assert info["total_rows"] == gf.count(inst.n, inst.gens)
+        assert info["num_slices"] >= 1
+        ri = Plan(inst.n, inst.gens, L.FS_CONSUMER_ROWS).info
+        assert ri["total_units"] == ri["total_rows"] == info["total_rows"]
+        assert ri["slice_units"] % 8 == 0
+
+
+def test_magic_division():
+    rng = random.Random(1)
+    gs = list(range(1, 2000)) + [rng.randint(2, 2 ** 31 - 1) for _ in range(300)] + [2 ** k for k in range(31)] + \
+         [2 ** k + 1 for k in range(30)] + [2 ** k - 1 for k in range(2, 31)]
+    xs_fixed = [0, 1, 2, 3, 2 ** 31 - 1, 2 ** 31 - 2, 2 ** 30, 2 ** 30 - 1]
+    for g in gs:
+        m, sh = magic(g)
+        assert 0 < m < 2 ** 32
+        xs = xs_fixed + [rng.randint(0, 2 ** 31 - 1) for _ in range(40)] + [g * k + r for k in (1, 7, 1000) for r in (-1, 0, 1) if 0 <= g * k + r < 2 ** 31]
+        for x in xs:
+            assert (x * m) >> sh == x // g, (g, x)
+
+
+def test_validation_errors():
+    with pytest.raises(ValueError):
+        Plan(10, (2, 0, 3))
+    with pytest.raises(ValueError):
+        Plan(10, ())
+    with pytest.raises(ValueError):
+        Plan(10, tuple(range(1, 18)))
+    with pytest.raises(OverflowError):
+        Plan(2 ** 31 - 10, (3, 20))
+    Plan(2 ** 31 - 21, (20, 3))  # n + max g = 2^31 - 1: accepted (d = 2, no tables)
+    with pytest.raises(ValueError):
+        Plan(10, (2, 3), rank=2, world=2)
