@@ -1,0 +1,395 @@
+#!/usr/bin/env python
+"""bench.py -- factorizations/s of the hot path on B200 (BASELINE.json metric), vs the
+INT32-ALU roofline (count) and the HBM roofline (store), with the CPU oracle beside it.
+
+  python bench.py [--gpus N] [--steps K] [--warmup W] [--workload c3count] [--impl fsgpu|reference]
+  torchrun --nproc-per-node N bench.py --gpus N ...
+
+A step = one full pass of the hot path over the workload instance: plan constants/DP tables
+are resident in HBM, the persistent kernel enumerates every factorization of the rank's
+block of the lex order (count consumer) and, for N > 1, one NCCL all_reduce combines the
+partial counts.  Default workload: C3 = Z(4275, (13,14,20,22,23,24,35,39)),
+|Z| = 100,032,405,189 (BASELINE.json configs[2]).  Strong scaling (fixed instance).
+Extra keys: the store path (C2-XL materialise, 26 GB of u16 rows) with its HBM roofline and
+the C4 length histogram, each measured in the same run.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+from paper_2405_07989_b200 import workloads as W  # noqa: E402
+
+METRIC = "factorizations/sec (count, store) at 1/2/4/8 B200 vs INT-ALU/HBM roofline"
+UNIT = "factorizations/s"
+
+# Algorithmic integer-op model per unit of the method:
+#   node entry (advance to the next level-L prefix + solve its first valid a_{d-1}) : 10
+#   row (one valid factorization consumed + modulo-skip step)                      :  4
+#   deeper node (ascend to a level-k prefix, k < L, greedy re-solve)               : 12
+OPS_NODE, OPS_ROW, OPS_DEEP = 10, 4, 12
+INT_LANES_PER_CLK_PER_SM = 128  # 4 SMSPs x 32 lanes, one warp-instruction / clk each
+NUM_SMS = 148
+
+
+def load_peaks():
+    p = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    if os.path.exists(p):
+        with open(p) as f:
+            return json.load(f), "measured"
+    return {"hbm_gbs": 6650.0, "sm_max_mhz": 1965.0}, "fallback"
+
+
+class ClockSampler:
+    """nvidia-smi clocks + throttle reasons sampled every 200 ms during the timed region."""
+
+    FIELDS = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+              "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+              "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index: int):
+        self.index = index
+        self.proc = None
+        self.lines = []
+
+    def start(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", "-i", str(self.index), "--query-gpu=" + self.FIELDS, "--format=csv,noheader,nounits",
+                 "-lms", "200"], stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.t = threading.Thread(target=self._read, daemon=True)
+            self.t.start()
+        except Exception:
+            self.proc = None
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.lines.append(line.strip())
+
+    def stop(self):
+        if self.proc is None:
+            return None
+        self.proc.terminate()
+        try:
+            self.proc.wait(timeout=5)
+        except Exception:
+            self.proc.kill()
+        self.t.join(timeout=2)
+        sm, mx, reasons = [], None, set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for ln in self.lines:
+            parts = [x.strip() for x in ln.split(",")]
+            if len(parts) < 9:
+                continue
+            try:
+                sm.append(float(parts[1]))
+                mx = float(parts[2])
+            except ValueError:
+                continue
+            for nm, v in zip(names, parts[5:9]):
+                if v.lower().startswith("active"):
+                    reasons.add(nm)
+        if not sm:
+            return None
+        return {"sm_mhz": statistics.median(sm), "sm_max_mhz": mx, "reasons": sorted(reasons),
+                "samples": len(sm)}
+
+
+def ops_model(info) -> float:
+    """algorithmic integer ops of the whole instance."""
+    nodes = info["nodes_per_level"]
+    L = info["level"]
+    deep = sum(nodes[1:L]) if L >= 2 else 0
+    return OPS_NODE * nodes[L] + OPS_ROW * info["total_rows"] + OPS_DEEP * deep
+
+
+# ------------------------------------------------------------------ CPU oracle (baseline arm)
+def oracle_sample(inst, seconds: float, seed: int = 0):
+    """Time the nested-loop oracle (as it stands) on a bounded, row-weighted sample of prefix
+    boxes (a_1, a_2) of the instance.  Returns (rows, secs, boxes)."""
+    import random
+
+    import oracle
+    from oracle import gf
+
+    oracle.build()
+    n, g = inst.n, inst.gens
+    S = gf.suffix_tables(n, g)
+    rng = random.Random(seed)
+    # row-weighted draw of (a1, a2): P ~ |Z(n - a1 g1 - a2 g2, g3..)|
+    pairs, weights = [], []
+    for a1 in range(n // g[0] + 1):
+        r1 = n - a1 * g[0]
+        for a2 in range(r1 // g[1] + 1):
+            w = S[2][r1 - a2 * g[1]]
+            if w:
+                pairs.append((a1, a2))
+                weights.append(w)
+    rows = 0
+    t0 = time.perf_counter()
+    boxes = 0
+    while time.perf_counter() - t0 < seconds:
+        a1, a2 = rng.choices(pairs, weights=weights, k=1)[0]
+        rows += oracle.run(n, g, box=((a1,), a2, a2))["count"]
+        boxes += 1
+    return rows, time.perf_counter() - t0, boxes
+
+
+def run_reference(args, inst):
+    rank = int(os.environ.get("RANK", "0"))
+    if rank != 0:
+        return 0
+    per_step = max(1.0, float(os.environ.get("FS_REF_STEP_SECONDS", "6")))
+    for _ in range(args.warmup):
+        oracle_sample(inst, min(per_step, 2.0), seed=1)
+    vals = []
+    tot_rows, tot_s = 0, 0.0
+    for k in range(args.steps):
+        rows, secs, boxes = oracle_sample(inst, per_step, seed=100 + k)
+        vals.append(rows / secs)
+        tot_rows += rows
+        tot_s += secs
+    value = tot_rows / tot_s
+    line = {
+        "impl": "reference", "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": args.gpus,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1000.0 * tot_s / args.steps,
+        "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "u64",
+        "data": "synthetic", "config": {"workload": args.workload, "n": inst.n, "gens": list(inst.gens)},
+        "cpu_baseline": {"value": value, "unit": UNIT, "cores": 1, "kind": "oracle",
+                         "sample": "row-weighted prefix boxes (a1,a2) of %s, seeds 100..%d, %.0f s per step, "
+                                   "%d rows total" % (inst.name, 99 + args.steps, per_step, tot_rows)},
+        "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+    return 0
+
+
+# ------------------------------------------------------------------ GPU arm
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=5)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="fsgpu", choices=["fsgpu", "reference"])
+    ap.add_argument("--workload", default="c3count", choices=["c3count", "c5count", "c2count"])
+    ap.add_argument("--no-extra", action="store_true", help="skip the store/hist extra measurements")
+    ap.add_argument("--cpu-seconds", type=float, default=10.0)
+    args = ap.parse_args()
+    args.warmup = max(3, args.warmup)
+    inst = {"c3count": W.C3, "c5count": W.C5, "c2count": W.C2}[args.workload]
+    if args.impl == "reference":
+        return run_reference(args, inst)
+
+    import torch
+    import torch.distributed as dist
+
+    from paper_2405_07989_b200 import _lib as L
+    from paper_2405_07989_b200 import api
+    from paper_2405_07989_b200 import dist as fsdist
+
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=dev)
+    stream = torch.cuda.current_stream()
+    peaks, peaks_kind = load_peaks()
+
+    def barrier():
+        if world > 1:
+            dist.barrier()
+        torch.cuda.synchronize()
+
+    def max_over_ranks(x: float) -> float:
+        if world == 1:
+            return x
+        t = torch.tensor([x], dtype=torch.float64, device=dev)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        return float(t.item())
+
+    # ---- plan: constants + DP tables resident in HBM before the timed region
+    plan = api.Plan(inst.n, inst.gens, L.FS_CONSUMER_COUNT, device=local, stream=stream.cuda_stream,
+                    rank=rank, world=world)
+    info = plan.info
+    out = torch.zeros(1, dtype=torch.int64, device=dev)
+    flush = torch.empty(256 << 20, dtype=torch.uint8, device=dev)  # > 126 MB L2
+
+    def step():
+        plan.count_async(out)
+        if world > 1:
+            dist.all_reduce(out, op=dist.ReduceOp.SUM)
+
+    for _ in range(args.warmup):
+        step()
+    torch.cuda.synchronize()
+    assert int(out.item()) == info["total_rows"], ("count mismatch", int(out.item()), info["total_rows"])
+
+    sampler = ClockSampler(local)
+    ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(args.steps)]
+    kev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(args.steps)]
+    launches0 = L.lib().fsdbg_total_launches()
+    barrier()
+    sampler.start()
+    time.sleep(0.3)
+    for k in range(args.steps):
+        flush.zero_()  # L2 flush between steps (outside the step events)
+        ev[k][0].record(stream)
+        kev[k][0].record(stream)
+        plan.count_async(out)
+        kev[k][1].record(stream)
+        if world > 1:
+            dist.all_reduce(out, op=dist.ReduceOp.SUM)
+        ev[k][1].record(stream)
+    barrier()
+    clocks = sampler.stop()
+    launches = L.lib().fsdbg_total_launches() - launches0
+    step_ms = [a.elapsed_time(b) for a, b in ev]
+    kern_ms = [a.elapsed_time(b) for a, b in kev]
+    ms_step = max_over_ranks(sum(step_ms) / len(step_ms))
+    ms_kern = max_over_ranks(sum(kern_ms) / len(kern_ms))
+    total = int(out.item())
+    assert total == info["total_rows"]
+    value = total / (ms_step / 1e3)
+
+    # roofline of the dominant kernel (count): INT32 issue
+    sm_max = float((clocks or {}).get("sm_max_mhz") or peaks.get("sm_max_mhz", 1965.0))
+    peak_tops = INT_LANES_PER_CLK_PER_SM * NUM_SMS * sm_max * 1e6 / 1e12
+    share = (info["unit_end"] - info["unit_begin"]) / max(1, info["total_units"])
+    ops = ops_model(info) * share
+    achieved = ops / (ms_kern / 1e3) / 1e12
+    traffic = None
+    prof = os.path.join(ROOT, "profiles", "traffic.json")
+    if os.path.exists(prof):
+        try:
+            traffic = json.load(open(prof)).get(args.workload)
+        except Exception:
+            traffic = None
+
+    line = {
+        "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
+        "warmup": args.warmup, "ms_per_step": ms_step, "higher_is_better": True, "scaling": "strong",
+        "vs_baseline": None, "dtype": "u32", "data": "synthetic",
+        "config": {"workload": "%s: Z(%d, %s) count, |Z| = %d" % (inst.name, inst.n, list(inst.gens), total),
+                   "instance": inst.name, "n": inst.n, "gens": list(inst.gens), "consumer": "count",
+                   "parallelism": "lex-slice dp%d" % world, "l2": "flushed between steps (256 MB write)",
+                   "slice_units": info["slice_units"], "num_slices": info["num_slices"],
+                   "grid": info["grid"], "block": info["block"]},
+        "roofline": {"bound": "alu", "achieved": achieved, "peak": peak_tops, "unit": "Tops/s (int32 lane-ops)",
+                     "frac": achieved / peak_tops, "traffic": traffic,
+                     "peak_source": "derived: 128 int lane-ops/clk/SM x 148 SMs x %.0f MHz (sm max)" % sm_max,
+                     "ops_per_launch": ops, "kernel_ms": ms_kern},
+        "gpu_launches": int(launches),
+        "clocks": clocks,
+        "cand_per_s": None,
+    }
+
+    # ---- e2e: through the public API with host buffers (DP + H2D + kernel + D2H per step)
+    e2e_t = []
+    for k in range(max(2, min(args.steps, 3))):
+        barrier()
+        t0 = time.perf_counter()
+        if world > 1:
+            c = fsdist.count(inst.n, inst.gens)
+        else:
+            c = api.fs_count(inst.n, inst.gens)
+        torch.cuda.synchronize()
+        e2e_t.append(max_over_ranks(time.perf_counter() - t0))
+        assert c == total
+    e2e_s = statistics.median(e2e_t)
+    line["e2e"] = {"value": total / e2e_s, "unit": UNIT, "h2d_bytes_per_step": int(info["table_bytes"]),
+                   "d2h_bytes_per_step": 8, "seconds": e2e_s}
+
+    # ---- extras (same run): store (materialise C2-XL) and C4 length histogram
+    if not args.no_extra:
+        line["extra"] = extras(args, world, rank, local, dev, stream, peaks, peaks_kind, barrier, max_over_ranks)
+
+    # ---- CPU oracle beside it (rank 0, N = 1 only)
+    if world == 1:
+        rows, secs, boxes = oracle_sample(inst, args.cpu_seconds)
+        line["cpu_baseline"] = {"value": rows / secs, "unit": UNIT, "cores": 1, "kind": "oracle",
+                                "sample": "%d row-weighted prefix boxes (a1,a2) of %s (seed 0): %d rows in %.1f s, "
+                                          "1 thread" % (boxes, inst.name, rows, secs)}
+    if rank == 0:
+        print(json.dumps(line), flush=True)
+    if world > 1:
+        dist.barrier()
+        dist.destroy_process_group()
+    return 0
+
+
+def extras(args, world, rank, local, dev, stream, peaks, peaks_kind, barrier, max_over_ranks):
+    import torch
+    import torch.distributed as dist
+
+    from paper_2405_07989_b200 import _lib as L
+    from paper_2405_07989_b200 import api
+
+    ex = {}
+    # store: C2-XL rows, u16, canonical order at exact offsets
+    inst = W.C2XL
+    p = api.Plan(inst.n, inst.gens, L.FS_CONSUMER_ROWS, device=local, stream=stream.cuda_stream, rank=rank,
+                 world=world)
+    info = p.info
+    rows = info["row_end"] - info["row_begin"]
+    out = torch.empty((rows, inst.d), dtype=torch.uint16, device=dev)
+    for _ in range(2):
+        p.enumerate_async(16, out, rows)
+    ts = []
+    barrier()
+    for _ in range(3):
+        a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        a.record(stream)
+        p.enumerate_async(16, out, rows)
+        b.record(stream)
+        torch.cuda.synchronize()
+        ts.append(a.elapsed_time(b))
+    ms = max_over_ranks(statistics.median(ts))
+    total_rows = info["total_rows"]
+    bytes_ = total_rows * inst.d * 2
+    gbs = (rows * inst.d * 2) / (statistics.median(ts) / 1e3) / 1e9
+    gbs_all = bytes_ / (ms / 1e3) / 1e9
+    ex["store"] = {"workload": "C2XL: Z(16000, (11,13,17,19,23)) materialise u16 rows (canonical order)",
+                   "rows": total_rows, "bytes": bytes_, "ms": ms, "value": total_rows / (ms / 1e3), "unit": UNIT,
+                   "roofline": {"bound": "hbm", "achieved": gbs_all, "peak": peaks["hbm_gbs"] * world,
+                                "unit": "GB/s", "frac": gbs_all / (peaks["hbm_gbs"] * world),
+                                "peak_source": "MEASURED_PEAKS.json hbm_gbs (%s, copy r+w)" % peaks_kind,
+                                "per_gpu_gbs": gbs}}
+    del out
+    torch.cuda.empty_cache()
+    # C4 length histogram
+    inst = W.C4
+    p = api.Plan(inst.n, inst.gens, L.FS_CONSUMER_HIST, device=local, stream=stream.cuda_stream, rank=rank,
+                 world=world)
+    h = torch.zeros(api.hist_len(inst.n, inst.gens), dtype=torch.int64, device=dev)
+    p.hist_async(h)
+    ts = []
+    barrier()
+    for _ in range(2):
+        a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        a.record(stream)
+        p.hist_async(h)
+        if world > 1:
+            dist.all_reduce(h, op=dist.ReduceOp.SUM)
+        b.record(stream)
+        torch.cuda.synchronize()
+        ts.append(a.elapsed_time(b))
+    ms = max_over_ranks(statistics.median(ts))
+    total = int(h.sum().item())
+    ex["hist"] = {"workload": "C4: Z(4275, C3 gens) length histogram (329 bins)", "rows": total, "ms": ms,
+                  "value": total / (ms / 1e3), "unit": UNIT}
+    return ex
+
+
+if __name__ == "__main__":
+    sys.exit(main())

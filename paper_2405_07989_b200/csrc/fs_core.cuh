@@ -99,10 +99,20 @@ struct Lane {
   uint32_t lsum;   // a_1 + .. + a_L
 };
 
+// k0 lookups: the table of k0(rho) for rho in [0, g_{d-1}) (host vector, or a shared-memory
+// copy on the device), or the arithmetic form when g_{d-1} is too large for a table.
+struct KTabPtr {
+  const uint32_t *p;
+  FS_HD uint32_t operator()(uint32_t rho, const Consts &) const { return p[rho]; }
+};
+struct KTabArith {
+  FS_HD uint32_t operator()(uint32_t rho, const Consts &c) const { return k0_arith(rho, c); }
+};
+
 // Node entry: solve the first valid a_{d-1} of the node (modulo skip at run entry).
-template <int D, bool NEED_AD>
-FS_HD void entry(Lane<D> &st, const Consts &c, const uint32_t *ktab) {
-  uint32_t k = c.ktab_len ? ktab[st.rho] : k0_arith(st.rho, c);
+template <int D, bool NEED_AD, class KT>
+FS_HD void entry(Lane<D> &st, const Consts &c, const KT &kt) {
+  const uint32_t k = kt(st.rho, c);
   st.cur = (int32_t)st.A - (int32_t)k;  // A <= n < 2^31 - 1, so kNone gives cur < 0
   if (NEED_AD) st.ad = divq(st.rho + k * c.gA, c.dvB);  // only meaningful if cur >= 0
 }
@@ -184,8 +194,8 @@ FS_HD bool advance(Lane<D> &st, const Consts &c) {
 // Position the lane at global unit index u (exact, from the DP tables), perform the node
 // entry, and return the offset of u inside the node's unit list (0 = the entry unit when
 // alpha = 1).
-template <int D, bool NEED_AD>
-FS_HD uint64_t unrank(Lane<D> &st, const Consts &c, const uint32_t *ktab, uint64_t u) {
+template <int D, bool NEED_AD, class KT>
+FS_HD uint64_t unrank(Lane<D> &st, const Consts &c, const KT &kt, uint64_t u) {
   constexpr int L = D - 2;
   uint32_t R = c.n;
   uint32_t lsum = 0;
@@ -214,7 +224,7 @@ FS_HD uint64_t unrank(Lane<D> &st, const Consts &c, const uint32_t *ktab, uint64
   st.A = A;
   st.rho = R - A * c.gA;
   st.lsum = lsum;
-  entry<D, NEED_AD>(st, c, ktab);
+  entry<D, NEED_AD>(st, c, kt);
   return u;
 }
 
@@ -234,31 +244,85 @@ FS_HD uint32_t position_in_node(Lane<D> &st, const Consts &c, uint64_t off) {
   return 0;
 }
 
-// One unit of the stream: emit the current row and step to the next valid a_{d-1}
-// (a_{d-1} -= s, a_d += t: the modulo skip), or -- when the node has no rows
-// left -- move to the next node (Alg. 3.1 step 2-11) and solve its first valid row.
+// One step of the stream.  If the current node has no rows left, move to the next node
+// (Alg. 3.1 steps 2-11) and solve its first valid row (one ENTRY unit); then, if a row is
+// pending and the slice still has budget, emit it and step to the next valid a_{d-1}
+// (a_{d-1} -= s, a_d += t: the modulo skip) -- one ROW unit.
 // ALPHA: units charged for a node entry (1 for count/hist/any slices, 0 for row slices).
-template <int D, bool NEED_AD, int ALPHA, class Emit>
-FS_HD void step(Lane<D> &st, const Consts &c, const uint32_t *ktab, uint32_t &budget, Emit &emit) {
-  if (st.cur >= 0) {
-    emit(st);
-    st.cur -= (int32_t)c.s;
-    if (NEED_AD) st.ad += c.t;
-    budget -= 1;
-  } else {
+template <int D, bool NEED_AD, int ALPHA, class KT, class Emit>
+FS_HD void step(Lane<D> &st, const Consts &c, const KT &kt, uint32_t &budget, Emit &emit) {
+  if (st.cur < 0) {
     if (!advance<D>(st, c)) {
       budget = 0;
       return;
     }
-    entry<D, NEED_AD>(st, c, ktab);
-    budget -= ALPHA;
+    entry<D, NEED_AD>(st, c, kt);
+    if (ALPHA) {
+      budget -= 1;
+      if (budget == 0) return;  // the node's first row belongs to the next slice
+    }
   }
+  if (st.cur >= 0) {
+    emit.cond(true, st);
+    st.cur -= (int32_t)c.s;
+    if (NEED_AD) st.ad += c.t;
+    budget -= 1;
+  }
+}
+
+// Branch-free fast step for SIMT lanes.  Every active lane does, under predicates:
+//   - a row lane (cur >= 0) emits its row and steps a_{d-1} -= s;
+//   - a lane whose node is exhausted and whose level-L coordinate a_L > 0 advances to the next
+//     node (a_L -= 1, residual += g_L, incremental floor/residue of R_L by g_{d-1}), solves the
+//     node's first valid row through k0 (ENTRY unit) and, budget permitting, emits it.
+// Lanes that need the rare ascend (a_L = 0) or end of stream do nothing here and are left for
+// the generic step() (needs_slow()).  Same units and order as step().
+template <int D, bool NEED_AD, int ALPHA, class KT, class Emit>
+FS_HD void fast_step(Lane<D> &st, const Consts &c, const KT &kt, uint32_t &budget, Emit &emit) {
+  constexpr int L = D - 2;
+  const bool act = budget != 0;
+  const bool has = st.cur >= 0;
+  bool fa = false;
+  if constexpr (L >= 1) {
+    const uint32_t al = st.a[L - 1];
+    fa = act && !has && al != 0;
+    uint32_t r2 = st.rho + c.delta;
+    const uint32_t cy = r2 >= c.gA ? 1u : 0u;
+    r2 = cy ? r2 - c.gA : r2;
+    const uint32_t A2 = st.A + c.q + cy;
+    st.rho = fa ? r2 : st.rho;
+    st.A = fa ? A2 : st.A;
+    st.a[L - 1] = al - (fa ? 1u : 0u);
+    st.lsum -= fa ? 1u : 0u;
+    const uint32_t k = kt(st.rho, c);
+    const int32_t nc = (int32_t)st.A - (int32_t)k;
+    st.cur = fa ? nc : st.cur;
+    if (NEED_AD) {
+      const uint32_t ad2 = divq(st.rho + k * c.gA, c.dvB);
+      st.ad = fa ? ad2 : st.ad;
+    }
+    if (ALPHA) budget -= fa ? 1u : 0u;
+  }
+  const bool em = (has || fa) && st.cur >= 0 && budget != 0;
+  emit.cond(em, st);
+  st.cur -= em ? (int32_t)c.s : 0;
+  if (NEED_AD) st.ad += em ? c.t : 0u;
+  budget -= em ? 1u : 0u;
+}
+
+template <int D>
+FS_HD bool needs_slow(const Lane<D> &st, uint32_t budget) {
+  constexpr int L = D - 2;
+  if constexpr (L >= 1)
+    return budget != 0 && st.cur < 0 && st.a[L - 1] == 0;
+  else
+    return budget != 0 && st.cur < 0;
 }
 
 // units below a node with residual r (the DP base): alpha + beta * #valid a_{d-1}
 FS_HD uint64_t node_units_host(uint32_t r, const Consts &c, const uint32_t *ktab) {
   uint32_t A = r / c.gA, rho = r % c.gA;
-  uint32_t k = c.ktab_len ? ktab[rho] : k0_arith(rho, c);
+  uint32_t k = ktab ? ktab[rho] : k0_arith(rho, c);
   uint64_t rows = 0;
   if (k != kNone && k <= A) rows = (A - k) / c.s + 1;
   return (uint64_t)c.alpha + (uint64_t)c.beta * rows;

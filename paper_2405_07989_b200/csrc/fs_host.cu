@@ -131,7 +131,7 @@ int fs_validate_and_build(fs_plan *p, uint64_t n, const uint32_t *gens, int d, i
       // d = 2: the root is the only node; no tables are needed
       Consts cr = c;
       cr.alpha = 0;
-      const uint64_t nr = fs::node_units_host((uint32_t)n, cr, p->ktab.data());
+      const uint64_t nr = fs::node_units_host((uint32_t)n, cr, p->ktab.empty() ? nullptr : p->ktab.data());
       p->total_rows = nr;
       p->total_units = c.alpha + nr;
       p->nodes_per_level[0] = 1;
@@ -143,7 +143,7 @@ int fs_validate_and_build(fs_plan *p, uint64_t n, const uint32_t *gens, int d, i
       for (uint64_t r = 0; r <= n; ++r) {
         Consts cr = c;
         cr.alpha = 0;
-        const uint64_t nr = fs::node_units_host((uint32_t)r, cr, p->ktab.data());
+        const uint64_t nr = fs::node_units_host((uint32_t)r, cr, p->ktab.empty() ? nullptr : p->ktab.data());
         rows[r] = nr;
         arr[r] = c.alpha + nr;
       }
@@ -277,8 +277,9 @@ struct HostSink {
 template <int D>
 struct HostEmit {
   HostSink *sink;
-  FS_HD void operator()(const fs::Lane<D> &st) {
+  FS_HD void cond(bool em, const fs::Lane<D> &st) {
 #ifndef __CUDA_ARCH__
+    if (!em) return;
     uint32_t v[FS_MAX_D];
     for (int j = 0; j < D - 2; ++j) v[j] = st.a[j];
     v[D - 2] = (uint32_t)st.cur;
@@ -288,10 +289,9 @@ struct HostEmit {
   }
 };
 
-template <int D, int ALPHA>
-void host_model_d(const fs_plan *p, HostSink &sink, uint64_t *slice_counts, uint32_t *slice_first) {
+template <int D, int ALPHA, class KT>
+void host_model_d(const fs_plan *p, const KT &ktab, HostSink &sink, uint64_t *slice_counts, uint32_t *slice_first) {
   const Consts &c = p->c;
-  const uint32_t *ktab = p->ktab.empty() ? nullptr : p->ktab.data();
   for (uint64_t sl = 0; sl < p->num_slices; ++sl) {
     uint64_t u = p->unit_begin + sl * p->T;
     uint32_t budget = (uint32_t)std::min<uint64_t>(p->T, p->unit_end - u);
@@ -301,7 +301,11 @@ void host_model_d(const fs_plan *p, HostSink &sink, uint64_t *slice_counts, uint
     sink.slice_rows = 0;
     sink.have_first = false;
     HostEmit<D> emit{&sink};
-    while (budget > 0) fs::step<D, true, ALPHA>(st, c, ktab, budget, emit);
+    // the kernels' schedule: branch-free fast steps, generic step() for lanes needing an ascend
+    while (budget > 0) {
+      fs::fast_step<D, true, ALPHA>(st, c, ktab, budget, emit);
+      if (fs::needs_slow<D>(st, budget)) fs::step<D, true, ALPHA>(st, c, ktab, budget, emit);
+    }
     if (slice_counts) slice_counts[sl] = sink.slice_rows;
     if (slice_first) {
       for (int i = 0; i < D; ++i) slice_first[sl * D + i] = sink.have_first ? sink.first[i] : 0xFFFFFFFFu;
@@ -309,12 +313,20 @@ void host_model_d(const fs_plan *p, HostSink &sink, uint64_t *slice_counts, uint
   }
 }
 
+template <int D, class KT>
+void host_model_kt(const fs_plan *p, const KT &kt, HostSink &sink, uint64_t *sc, uint32_t *sf) {
+  if (p->c.alpha)
+    host_model_d<D, 1>(p, kt, sink, sc, sf);
+  else
+    host_model_d<D, 0>(p, kt, sink, sc, sf);
+}
+
 template <int D>
 void host_model_alpha(const fs_plan *p, HostSink &sink, uint64_t *sc, uint32_t *sf) {
-  if (p->c.alpha)
-    host_model_d<D, 1>(p, sink, sc, sf);
+  if (!p->ktab.empty())
+    host_model_kt<D>(p, fs::KTabPtr{p->ktab.data()}, sink, sc, sf);
   else
-    host_model_d<D, 0>(p, sink, sc, sf);
+    host_model_kt<D>(p, fs::KTabArith{}, sink, sc, sf);
 }
 
 }  // namespace
@@ -363,8 +375,8 @@ namespace {
 template <int D>
 int unrank_host(const fs_plan *p, uint64_t unit, uint32_t *prefix_out, int64_t *row_out) {
   fs::Lane<D> st;
-  const uint32_t *ktab = p->ktab.empty() ? nullptr : p->ktab.data();
-  uint64_t off = fs::unrank<D, true>(st, p->c, ktab, unit);
+  uint64_t off = p->ktab.empty() ? fs::unrank<D, true>(st, p->c, fs::KTabArith{}, unit)
+                                 : fs::unrank<D, true>(st, p->c, fs::KTabPtr{p->ktab.data()}, unit);
   for (int j = 0; j < D - 2; ++j) prefix_out[j] = st.a[j];
   if (p->c.alpha)
     *row_out = off == 0 ? -1 : (int64_t)(off - 1);

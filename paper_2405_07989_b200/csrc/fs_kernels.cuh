@@ -1,4 +1,4 @@
-// fs_kernels.cu -- persistent sm_100a kernels: one successor stream per thread over DP-sized,
+// fs_kernels.cuh -- persistent sm_100a kernels: one successor stream per thread over DP-sized,
 // disjoint lex slices pulled from an atomic work queue (replaces the paper's host-side
 // splitWork + 1024-launch cadence), four consumers:
 //   COUNT  per-lane u32 slice counters -> u64 -> warp shuffle reduction -> 1 atomic / warp
@@ -11,13 +11,23 @@
 #include <cuda_runtime.h>
 #include <stdint.h>
 
+#include <type_traits>
+
 #include "../../include/fsgpu.h"
 #include "fs_core.cuh"
 #include "fs_internal.h"
 
-unsigned long long g_fs_total_launches = 0;
-
 namespace fs {
+
+// k0 table in shared memory (copied once per CTA)
+struct KTabSmem {
+  uint32_t base;  // shared-window address of the table
+  __device__ __forceinline__ uint32_t operator()(uint32_t rho, const Consts &) const {
+    uint32_t v;
+    asm("ld.shared.u32 %0, [%1];" : "=r"(v) : "r"(base + rho * 4u));
+    return v;
+  }
+};
 
 constexpr unsigned kFull = 0xffffffffu;
 
@@ -30,7 +40,7 @@ struct Inner {
 template <int D>
 struct EmitCount {
   uint32_t n;
-  __device__ __forceinline__ void operator()(const Lane<D> &) { ++n; }
+  __device__ __forceinline__ void cond(bool em, const Lane<D> &) { n += em ? 1u : 0u; }
 };
 
 template <int D>
@@ -39,7 +49,8 @@ struct EmitHist {
   unsigned long long *gbins;
   uint32_t smem;
   uint32_t n;
-  __device__ __forceinline__ void operator()(const Lane<D> &st) {
+  __device__ __forceinline__ void cond(bool em, const Lane<D> &st) {
+    if (!em) return;
     const uint32_t l = st.lsum + (uint32_t)st.cur + st.ad;  // length = sum_i a_i
     if (smem)
       atomicAdd(&bins[l], 1u);
@@ -66,7 +77,8 @@ struct EmitAny {
   int *found;
   uint32_t *wit;
   bool hit;
-  __device__ __forceinline__ void operator()(const Lane<D> &st) {
+  __device__ __forceinline__ void cond(bool em, const Lane<D> &st) {
+    if (!em) return;
     const uint64_t len = (uint64_t)st.lsum + (uint32_t)st.cur + st.ad;
     bool ok;
     switch (pred) {
@@ -109,7 +121,8 @@ struct EmitRows {
     else
       *reinterpret_cast<uint32_t *>(ring + ((p + 4 * i + rot) & 255u)) = v;
   }
-  __device__ __forceinline__ void operator()(const Lane<D> &st) {
+  __device__ __forceinline__ void cond(bool em, const Lane<D> &st) {
+    if (!em) return;
     const uint32_t p = wpos;
 #pragma unroll
     for (int j = 0; j < D - 2; ++j) put(p, j, st.a[j]);
@@ -158,15 +171,35 @@ __device__ __forceinline__ void warp_flush(bool &pend, uint32_t soff, uint64_t g
   pend = false;
 }
 
+// ROWS: the lane's slice is complete -- copy the ragged tail of its last half byte by byte
+// (only at the end of the rank's block) and mark the 16 B-aligned part for the warp flush.
+template <int D, int B>
+__device__ __forceinline__ void rows_slice_done(const KParams &P, EmitRows<D, B> &er, bool &fin, uint32_t &fin_soff,
+                                                uint64_t &fin_goff, uint32_t &fin_len) {
+  const uint32_t w = er.wpos;
+  const uint32_t hstart = w & ~127u;
+  const uint32_t plen = w - hstart;
+  const uint32_t alen = plen & ~15u;
+  for (uint32_t b = alen; b < plen; ++b)
+    P.rows_out[er.slice_goff + hstart + b] = er.ring[(hstart + b + er.rot) & 255u];
+  if (alen) {
+    fin = true;
+    fin_soff = hstart & 128u;
+    fin_goff = er.slice_goff + hstart;
+    fin_len = alen;
+  }
+}
+
 __device__ __forceinline__ uint64_t bitrev_bits(uint64_t x, uint32_t bits) {
   return bits ? (__brevll(x) >> (64 - bits)) : 0ull;
 }
 
-template <int D, int CONS, int B>
+template <int D, int CONS, int B, bool KTAB>
 __global__ void __launch_bounds__(kBlock) fs_enum_kernel(const KParams P) {
   constexpr bool NEED_AD = CONS != FS_CONSUMER_COUNT;
   constexpr int ALPHA = CONS == FS_CONSUMER_ROWS ? 0 : 1;
   constexpr int INNER = Inner<CONS>::value;
+  constexpr int UNROLL = CONS == FS_CONSUMER_ROWS ? 1 : 4;
   extern __shared__ __align__(16) unsigned char smem[];
   __shared__ unsigned int hist_guard;
   const Consts &c = P.c;
@@ -184,11 +217,21 @@ __global__ void __launch_bounds__(kBlock) fs_enum_kernel(const KParams P) {
   }
   __syncthreads();
 
-  const uint32_t *kt = ktab_s;
+  using KT = typename std::conditional<KTAB, KTabSmem, KTabArith>::type;
+  KT kt;
+  if constexpr (KTAB) kt.base = (uint32_t)__cvta_generic_to_shared(ktab_s);
   const int lane = threadIdx.x & 31;
   Lane<D> st;
+#pragma unroll
+  for (int j = 0; j < Lane<D>::LA; ++j) {
+    st.a[j] = 0;
+    st.R[j] = 0;
+  }
+  st.A = 0;
+  st.rho = 0;  // keeps k0 lookups of idle lanes inside the table
   st.cur = -1;
   st.ad = 0;
+  st.lsum = 0;
   uint32_t budget = 0;
   bool alive = true;
   uint64_t acc = 0;
@@ -268,41 +311,47 @@ __global__ void __launch_bounds__(kBlock) fs_enum_kernel(const KParams P) {
     if (__ballot_sync(kFull, alive) == 0) break;
 
 #pragma unroll 1
-    for (int it = 0; it < INNER; ++it) {
-      if (budget > 0) {
+    for (int it = 0; it < INNER; it += UNROLL) {
+      // UNROLL branch-free fast steps, then one (warp-uniform) check for lanes parked on an
+      // ascend; the rare slow lanes run the generic successor step together.
+#pragma unroll
+      for (int u = 0; u < UNROLL; ++u) {
         if (CONS == FS_CONSUMER_COUNT) {
-          step<D, NEED_AD, ALPHA>(st, c, kt, budget, e_count);
+          fast_step<D, NEED_AD, ALPHA>(st, c, kt, budget, e_count);
         } else if (CONS == FS_CONSUMER_HIST) {
-          step<D, NEED_AD, ALPHA>(st, c, kt, budget, e_hist);
+          fast_step<D, NEED_AD, ALPHA>(st, c, kt, budget, e_hist);
         } else if (CONS == FS_CONSUMER_ANY) {
-          step<D, NEED_AD, ALPHA>(st, c, kt, budget, e_any);
-          if (e_any.hit) {
-            budget = 0;
-            alive = false;
-          }
+          fast_step<D, NEED_AD, ALPHA>(st, c, kt, budget, e_any);
         } else {
-          step<D, NEED_AD, ALPHA>(st, c, kt, budget, e_rows);
-          if (budget == 0) {
-            // slice done: flush the partial half (16 B-aligned part cooperatively, the
-            // ragged tail -- only at the end of the rank's block -- byte by byte)
-            const uint32_t w = e_rows.wpos;
-            const uint32_t hstart = w & ~127u;
-            const uint32_t plen = w - hstart;
-            const uint32_t alen = plen & ~15u;
-            for (uint32_t b = alen; b < plen; ++b)
-              P.rows_out[e_rows.slice_goff + hstart + b] = e_rows.ring[(hstart + b + e_rows.rot) & 255u];
-            if (alen) {
-              fin = true;
-              fin_soff = hstart & 128u;
-              fin_goff = e_rows.slice_goff + hstart;
-              fin_len = alen;
-            }
-          }
+          const bool was = budget != 0;
+          fast_step<D, NEED_AD, ALPHA>(st, c, kt, budget, e_rows);
+          if (was && budget == 0) rows_slice_done(P, e_rows, fin, fin_soff, fin_goff, fin_len);
+          warp_flush(e_rows.pend, e_rows.pend_soff, e_rows.pend_goff, 128u, warp_stage, P.rows_out);
+          warp_flush(fin, fin_soff, fin_goff, fin_len, warp_stage, P.rows_out);
         }
       }
-      if (CONS == FS_CONSUMER_ROWS) {
-        warp_flush(e_rows.pend, e_rows.pend_soff, e_rows.pend_goff, 128u, warp_stage, P.rows_out);
-        warp_flush(fin, fin_soff, fin_goff, fin_len, warp_stage, P.rows_out);
+      const bool slow = needs_slow<D>(st, budget);
+      if (__any_sync(kFull, slow)) {
+        if (slow) {
+          if (CONS == FS_CONSUMER_COUNT) {
+            step<D, NEED_AD, ALPHA>(st, c, kt, budget, e_count);
+          } else if (CONS == FS_CONSUMER_HIST) {
+            step<D, NEED_AD, ALPHA>(st, c, kt, budget, e_hist);
+          } else if (CONS == FS_CONSUMER_ANY) {
+            step<D, NEED_AD, ALPHA>(st, c, kt, budget, e_any);
+          } else {
+            step<D, NEED_AD, ALPHA>(st, c, kt, budget, e_rows);
+            if (budget == 0) rows_slice_done(P, e_rows, fin, fin_soff, fin_goff, fin_len);
+          }
+        }
+        if (CONS == FS_CONSUMER_ROWS) {
+          warp_flush(e_rows.pend, e_rows.pend_soff, e_rows.pend_goff, 128u, warp_stage, P.rows_out);
+          warp_flush(fin, fin_soff, fin_goff, fin_len, warp_stage, P.rows_out);
+        }
+      }
+      if (CONS == FS_CONSUMER_ANY && e_any.hit) {
+        budget = 0;
+        alive = false;
       }
     }
   }
@@ -356,9 +405,9 @@ static size_t smem_bytes(const KParams &kp, int consumer) {
   return b;
 }
 
-template <int D, int CONS, int B>
+template <int D, int CONS, int B, bool KTAB>
 static int launch_t(fs_plan *p, const KParams &kp, cudaStream_t stream, bool query_only, uint32_t *grid_out) {
-  auto kern = fs_enum_kernel<D, CONS, B>;
+  auto kern = fs_enum_kernel<D, CONS, B, KTAB>;
   const size_t smem = smem_bytes(kp, CONS);
   if (cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem) != cudaSuccess)
     return FS_ECUDA;
@@ -376,7 +425,6 @@ static int launch_t(fs_plan *p, const KParams &kp, cudaStream_t stream, bool que
   if (query_only) return FS_OK;
   kern<<<(unsigned)grid, kBlock, smem, stream>>>(kp);
   if (cudaGetLastError() != cudaSuccess) return FS_ECUDA;
-  ++g_fs_total_launches;
   return FS_OK;
 }
 
@@ -386,17 +434,16 @@ static int launch_d1(const KParams &kp, cudaStream_t stream, bool query_only, ui
   if (query_only) return FS_OK;
   fs_d1_kernel<CONS, B><<<1, 32, 0, stream>>>(kp);
   if (cudaGetLastError() != cudaSuccess) return FS_ECUDA;
-  ++g_fs_total_launches;
   return FS_OK;
 }
 
-template <int CONS, int B>
+template <int CONS, int B, bool KTAB>
 static int dispatch_d(fs_plan *p, const KParams &kp, cudaStream_t s, bool q, uint32_t *g) {
   switch (p->d) {
     case 1: return launch_d1<CONS, B>(kp, s, q, g);
 #define FS_CASE(DD) \
   case DD:          \
-    return launch_t<DD, CONS, B>(p, kp, s, q, g);
+    return launch_t<DD, CONS, B, KTAB>(p, kp, s, q, g);
     FS_CASE(2) FS_CASE(3) FS_CASE(4) FS_CASE(5) FS_CASE(6) FS_CASE(7) FS_CASE(8) FS_CASE(9)
     FS_CASE(10) FS_CASE(11) FS_CASE(12) FS_CASE(13) FS_CASE(14) FS_CASE(15) FS_CASE(16)
 #undef FS_CASE
@@ -404,32 +451,9 @@ static int dispatch_d(fs_plan *p, const KParams &kp, cudaStream_t s, bool q, uin
   return FS_EINVAL;
 }
 
-static int dispatch(fs_plan *p, int consumer, int B, const KParams &kp, cudaStream_t s, bool q, uint32_t *g) {
-  switch (consumer) {
-    case FS_CONSUMER_COUNT: return dispatch_d<FS_CONSUMER_COUNT, 16>(p, kp, s, q, g);
-    case FS_CONSUMER_HIST: return dispatch_d<FS_CONSUMER_HIST, 16>(p, kp, s, q, g);
-    case FS_CONSUMER_ANY: return dispatch_d<FS_CONSUMER_ANY, 16>(p, kp, s, q, g);
-    case FS_CONSUMER_ROWS:
-      return B == 16 ? dispatch_d<FS_CONSUMER_ROWS, 16>(p, kp, s, q, g)
-                     : dispatch_d<FS_CONSUMER_ROWS, 32>(p, kp, s, q, g);
-  }
-  return FS_EINVAL;
+template <int CONS, int B>
+static int dispatch_kt(fs_plan *p, const KParams &kp, cudaStream_t s, bool q, uint32_t *g) {
+  return kp.c.ktab_len ? dispatch_d<CONS, B, true>(p, kp, s, q, g) : dispatch_d<CONS, B, false>(p, kp, s, q, g);
 }
 
 }  // namespace fs
-
-int fs_launch(fs_plan *p, int consumer, int B, const fs::KParams &kp, cudaStream_t stream) {
-  uint32_t grid = 0;
-  int rc = fs::dispatch(p, consumer, B, kp, stream, false, &grid);
-  if (rc == FS_OK) p->grid = grid;
-  return rc;
-}
-
-int fs_occupancy_grid(fs_plan *p, int consumer, int B, uint32_t *grid_out) {
-  fs::KParams kp{};
-  kp.c = p->c;
-  kp.num_claims = p->num_slices;
-  kp.hist_len = (uint32_t)p->hist_len;
-  kp.hist_smem = p->hist_len <= fs::kHistSmemMax;
-  return fs::dispatch(p, consumer, B, kp, nullptr, true, grid_out);
-}

@@ -1,0 +1,41 @@
+// fs_launch.cu -- consumer dispatch and launch accounting for the persistent kernels.
+#include <cuda_runtime.h>
+
+#include "../../include/fsgpu.h"
+#include "fs_internal.h"
+
+unsigned long long g_fs_total_launches = 0;
+
+int fs_dispatch_count(fs_plan *p, int B, const fs::KParams &kp, cudaStream_t s, bool q, uint32_t *g);
+int fs_dispatch_hist(fs_plan *p, int B, const fs::KParams &kp, cudaStream_t s, bool q, uint32_t *g);
+int fs_dispatch_any(fs_plan *p, int B, const fs::KParams &kp, cudaStream_t s, bool q, uint32_t *g);
+int fs_dispatch_rows(fs_plan *p, int B, const fs::KParams &kp, cudaStream_t s, bool q, uint32_t *g);
+
+static int dispatch(fs_plan *p, int consumer, int B, const fs::KParams &kp, cudaStream_t s, bool q, uint32_t *g) {
+  switch (consumer) {
+    case FS_CONSUMER_COUNT: return fs_dispatch_count(p, B, kp, s, q, g);
+    case FS_CONSUMER_HIST: return fs_dispatch_hist(p, B, kp, s, q, g);
+    case FS_CONSUMER_ANY: return fs_dispatch_any(p, B, kp, s, q, g);
+    case FS_CONSUMER_ROWS: return fs_dispatch_rows(p, B, kp, s, q, g);
+  }
+  return FS_EINVAL;
+}
+
+int fs_launch(fs_plan *p, int consumer, int B, const fs::KParams &kp, cudaStream_t stream) {
+  uint32_t grid = 0;
+  int rc = dispatch(p, consumer, B, kp, stream, false, &grid);
+  if (rc == FS_OK) {
+    p->grid = grid;
+    ++g_fs_total_launches;
+  }
+  return rc;
+}
+
+int fs_occupancy_grid(fs_plan *p, int consumer, int B, uint32_t *grid_out) {
+  fs::KParams kp{};
+  kp.c = p->c;
+  kp.num_claims = p->num_slices;
+  kp.hist_len = (uint32_t)p->hist_len;
+  kp.hist_smem = p->hist_len <= fs::kHistSmemMax;
+  return dispatch(p, consumer, B, kp, nullptr, true, grid_out);
+}
