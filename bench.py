@@ -104,6 +104,24 @@ class ClockSampler:
                 "samples": len(sm)}
 
 
+def microbench():
+    """Measured roofline denominators on this GPU (csrc/fs_micro.cu): INT32 lane-op rates of
+    IADD3 / IMAD / 1:1 mix / LOP3 chains and coalesced 16 B streaming-store bandwidth."""
+    import ctypes
+
+    from paper_2405_07989_b200 import _lib as L
+
+    out = {}
+    for kind, name in [(0, "iadd"), (1, "imad"), (2, "mix"), (3, "lop3")]:
+        r, a = ctypes.c_double(0), ctypes.c_double(0)
+        L.check(L.lib().fsdbg_microbench(kind, 0, ctypes.byref(r), ctypes.byref(a)), "microbench")
+        out[name] = {"ops_per_clk_per_sm": r.value, "tops": a.value}
+    r, a = ctypes.c_double(0), ctypes.c_double(0)
+    L.check(L.lib().fsdbg_microbench(4, 8 << 30, ctypes.byref(r), ctypes.byref(a)), "microbench")
+    out["hbm_write_gbs"] = r.value
+    return out
+
+
 def ops_model(info) -> float:
     """algorithmic integer ops of the whole instance."""
     nodes = info["nodes_per_level"]
@@ -262,9 +280,14 @@ def main():
     assert total == info["total_rows"]
     value = total / (ms_step / 1e3)
 
-    # roofline of the dominant kernel (count): INT32 issue
+    # roofline of the dominant kernel (count): INT32 issue.  Denominator: the best measured
+    # INT32 microbenchmark rate on this GPU (csrc/fs_micro.cu); the derived issue limit
+    # (128 lane-ops/clk/SM x 148 x sm max clock) is reported beside it.
     sm_max = float((clocks or {}).get("sm_max_mhz") or peaks.get("sm_max_mhz", 1965.0))
-    peak_tops = INT_LANES_PER_CLK_PER_SM * NUM_SMS * sm_max * 1e6 / 1e12
+    derived_tops = INT_LANES_PER_CLK_PER_SM * NUM_SMS * sm_max * 1e6 / 1e12
+    mb = microbench() if rank == 0 or world > 1 else None
+    measured_tops = max(v["tops"] for k, v in mb.items() if isinstance(v, dict)) if mb else None
+    peak_tops = measured_tops or derived_tops
     share = (info["unit_end"] - info["unit_begin"]) / max(1, info["total_units"])
     ops = ops_model(info) * share
     achieved = ops / (ms_kern / 1e3) / 1e12
@@ -287,9 +310,12 @@ def main():
                    "grid": info["grid"], "block": info["block"]},
         "roofline": {"bound": "alu", "achieved": achieved, "peak": peak_tops, "unit": "Tops/s (int32 lane-ops)",
                      "frac": achieved / peak_tops, "traffic": traffic,
-                     "peak_source": "derived: 128 int lane-ops/clk/SM x 148 SMs x %.0f MHz (sm max)" % sm_max,
+                     "peak_source": ("measured: best INT32 microbenchmark (fs_micro.cu)" if measured_tops else
+                                     "derived: 128 int lane-ops/clk/SM x 148 SMs x %.0f MHz" % sm_max),
+                     "derived_issue_peak": derived_tops, "frac_of_derived": achieved / derived_tops,
                      "ops_per_launch": ops, "kernel_ms": ms_kern},
         "gpu_launches": int(launches),
+        "microbench": mb,
         "clocks": clocks,
         "cand_per_s": None,
     }
@@ -312,7 +338,8 @@ def main():
 
     # ---- extras (same run): store (materialise C2-XL) and C4 length histogram
     if not args.no_extra:
-        line["extra"] = extras(args, world, rank, local, dev, stream, peaks, peaks_kind, barrier, max_over_ranks)
+        line["extra"] = extras(args, world, rank, local, dev, stream, peaks, peaks_kind, barrier, max_over_ranks,
+                               mb)
 
     # ---- CPU oracle beside it (rank 0, N = 1 only)
     if world == 1:
@@ -328,7 +355,7 @@ def main():
     return 0
 
 
-def extras(args, world, rank, local, dev, stream, peaks, peaks_kind, barrier, max_over_ranks):
+def extras(args, world, rank, local, dev, stream, peaks, peaks_kind, barrier, max_over_ranks, mb):
     import torch
     import torch.distributed as dist
 
@@ -364,7 +391,8 @@ def extras(args, world, rank, local, dev, stream, peaks, peaks_kind, barrier, ma
                    "roofline": {"bound": "hbm", "achieved": gbs_all, "peak": peaks["hbm_gbs"] * world,
                                 "unit": "GB/s", "frac": gbs_all / (peaks["hbm_gbs"] * world),
                                 "peak_source": "MEASURED_PEAKS.json hbm_gbs (%s, copy r+w)" % peaks_kind,
-                                "per_gpu_gbs": gbs}}
+                                "per_gpu_gbs": gbs,
+                                "frac_of_write_microbench": (gbs / mb["hbm_write_gbs"]) if mb else None}}
     del out
     torch.cuda.empty_cache()
     # C4 length histogram

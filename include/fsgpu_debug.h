@@ -40,6 +40,12 @@ int fsdbg_unrank(const fs_plan *plan, uint64_t unit, uint32_t *prefix_out, int64
 int fsdbg_magic(uint32_t g, uint32_t *m_out, uint32_t *sh_out);
 uint32_t fsdbg_magic_div(uint32_t x, uint32_t g);
 
+/* Roofline microbenchmarks on the current device.  kind 0: IADD3 chains, 1: IMAD chains,
+ * 2: 1:1 IADD3/IMAD mix, 3: LOP3 chains -> *result_out = INT32 lane-ops per clock per SM
+ * (from clock64), *aux_out = Tops/s (from CUDA events).  kind 4: coalesced 16 B streaming
+ * stores over `param` bytes (0 = 8 GiB) -> *result_out = GB/s (best of 5), *aux_out = bytes. */
+int fsdbg_microbench(int kind, uint64_t param, double *result_out, double *aux_out);
+
 /* Device count of the launches the library made since load (all plans). */
 uint64_t fsdbg_total_launches(void);
 
