@@ -127,3 +127,26 @@ def rows_before_prefix(n: int, gens: Sequence[int], prefix: Sequence[int]) -> in
         if R < 0:
             raise ValueError("prefix overshoots n")
     return before
+
+
+def work_tables(n: int, gens: Sequence[int]) -> List[List[int]]:
+    """Wk[k][r] = #(a_k..a_{d-2}) with sum_j a_j g_j <= r (0-based k), i.e. the number of
+    innermost-loop iterations the nested-loop oracle performs below a level-k prefix with
+    residual r.  Wk[d-1][r] = 1."""
+    d = len(gens)
+    out: List[List[int]] = [None] * d  # type: ignore
+    cur = [1] * (n + 1)  # below level d-1: the single last-coordinate test
+    out[d - 1] = list(cur)
+    # Z-counts of the suffix (g_k..g_{d-2}) summed over residual <= r
+    z = [0] * (n + 1)
+    z[0] = 1
+    for k in range(d - 2, -1, -1):
+        g = int(gens[k])
+        for r in range(g, n + 1):
+            z[r] += z[r - g]
+        acc, pref = 0, [0] * (n + 1)
+        for r in range(n + 1):
+            acc += z[r]
+            pref[r] = acc
+        out[k] = pref
+    return out
