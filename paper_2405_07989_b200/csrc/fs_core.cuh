@@ -244,30 +244,18 @@ FS_HD uint32_t position_in_node(Lane<D> &st, const Consts &c, uint64_t off) {
   return 0;
 }
 
-// One step of the stream.  If the current node has no rows left, move to the next node
-// (Alg. 3.1 steps 2-11) and solve its first valid row (one ENTRY unit); then, if a row is
-// pending and the slice still has budget, emit it and step to the next valid a_{d-1}
-// (a_{d-1} -= s, a_d += t: the modulo skip) -- one ROW unit.
-// ALPHA: units charged for a node entry (1 for count/hist/any slices, 0 for row slices).
-template <int D, bool NEED_AD, int ALPHA, class KT, class Emit>
-FS_HD void step(Lane<D> &st, const Consts &c, const KT &kt, uint32_t &budget, Emit &emit) {
-  if (st.cur < 0) {
-    if (!advance<D>(st, c)) {
-      budget = 0;
-      return;
-    }
-    entry<D, NEED_AD>(st, c, kt);
-    if (ALPHA) {
-      budget -= 1;
-      if (budget == 0) return;  // the node's first row belongs to the next slice
-    }
+// Slow step, for a lane whose node is exhausted and whose level-L coordinate is 0: Alg. 3.1
+// steps 2-11 at an index i < L (ascend() re-solves a_{i+1}..a_L greedily), then the new
+// node's entry (one ENTRY unit).  It never emits: the node's first row, if any, is emitted
+// by the next fast_step, so every emission happens with the warp converged.
+template <int D, bool NEED_AD, int ALPHA, class KT>
+FS_HD void slow_step(Lane<D> &st, const Consts &c, const KT &kt, uint32_t &budget) {
+  if (!advance<D>(st, c)) {
+    budget = 0;  // end of stream
+    return;
   }
-  if (st.cur >= 0) {
-    emit.cond(true, st);
-    st.cur -= (int32_t)c.s;
-    if (NEED_AD) st.ad += c.t;
-    budget -= 1;
-  }
+  entry<D, NEED_AD>(st, c, kt);
+  budget -= ALPHA;
 }
 
 // Branch-free fast step for SIMT lanes.  Every active lane does, under predicates:
@@ -276,7 +264,7 @@ FS_HD void step(Lane<D> &st, const Consts &c, const KT &kt, uint32_t &budget, Em
 //     node (a_L -= 1, residual += g_L, incremental floor/residue of R_L by g_{d-1}), solves the
 //     node's first valid row through k0 (ENTRY unit) and, budget permitting, emits it.
 // Lanes that need the rare ascend (a_L = 0) or end of stream do nothing here and are left for
-// the generic step() (needs_slow()).  Same units and order as step().
+// slow_step() (needs_slow()).
 template <int D, bool NEED_AD, int ALPHA, class KT, class Emit>
 FS_HD void fast_step(Lane<D> &st, const Consts &c, const KT &kt, uint32_t &budget, Emit &emit) {
   constexpr int L = D - 2;

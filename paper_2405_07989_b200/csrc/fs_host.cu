@@ -304,7 +304,7 @@ void host_model_d(const fs_plan *p, const KT &ktab, HostSink &sink, uint64_t *sl
     // the kernels' schedule: branch-free fast steps, generic step() for lanes needing an ascend
     while (budget > 0) {
       fs::fast_step<D, true, ALPHA>(st, c, ktab, budget, emit);
-      if (fs::needs_slow<D>(st, budget)) fs::step<D, true, ALPHA>(st, c, ktab, budget, emit);
+      if (fs::needs_slow<D>(st, budget)) fs::slow_step<D, true, ALPHA>(st, c, ktab, budget);
     }
     if (slice_counts) slice_counts[sl] = sink.slice_rows;
     if (slice_first) {

@@ -333,16 +333,8 @@ __global__ void __launch_bounds__(kBlock) fs_enum_kernel(const KParams P) {
       const bool slow = needs_slow<D>(st, budget);
       if (__any_sync(kFull, slow)) {
         if (slow) {
-          if (CONS == FS_CONSUMER_COUNT) {
-            step<D, NEED_AD, ALPHA>(st, c, kt, budget, e_count);
-          } else if (CONS == FS_CONSUMER_HIST) {
-            step<D, NEED_AD, ALPHA>(st, c, kt, budget, e_hist);
-          } else if (CONS == FS_CONSUMER_ANY) {
-            step<D, NEED_AD, ALPHA>(st, c, kt, budget, e_any);
-          } else {
-            step<D, NEED_AD, ALPHA>(st, c, kt, budget, e_rows);
-            if (budget == 0) rows_slice_done(P, e_rows, fin, fin_soff, fin_goff, fin_len);
-          }
+          slow_step<D, NEED_AD, ALPHA>(st, c, kt, budget);
+          if (CONS == FS_CONSUMER_ROWS && budget == 0) rows_slice_done(P, e_rows, fin, fin_soff, fin_goff, fin_len);
         }
         if (CONS == FS_CONSUMER_ROWS) {
           warp_flush(e_rows.pend, e_rows.pend_soff, e_rows.pend_goff, 128u, warp_stage, P.rows_out);
