@@ -85,7 +85,11 @@ enum {
  *               distributed workers).  world = 0 is treated as 1.
  *   slice_units target units per slice (0 = automatic); rows per slice for ROWS plans
  *               (rounded up to a multiple of 8).  Tests force tiny slices with it.
- *   ctas_per_sm persistent CTAs per SM (0 = occupancy maximum). */
+ *   ctas_per_sm persistent CTAs per SM (0 = occupancy maximum).
+ *   order       materialise layout: FS_ORDER_CANONICAL (0, default) writes every row at its
+ *               exact canonical offset; FS_ORDER_ANY (1) compacts rows per warp with
+ *               warp-aggregated atomics into an arbitrary order (the same multiset of rows;
+ *               requires cap >= the rank's rows, else FS_ERANGE). */
 typedef struct {
     int device;
     void *cuda_stream;
@@ -93,8 +97,11 @@ typedef struct {
     int world;
     uint64_t slice_units;
     int ctas_per_sm;
-    int reserved[8];
+    int order;
+    int reserved[7];
 } fs_exec_t;
+
+enum { FS_ORDER_CANONICAL = 0, FS_ORDER_ANY = 1 };
 
 /* ---------------------------------------------------------------------------------
  * north_star entry points: current CUDA device, default stream, whole instance.

@@ -15,6 +15,7 @@ FS_OK, FS_EINVAL, FS_ERANGE, FS_ECUDA, FS_ENOMEM, FS_ENODEV = 0, -1, -2, -3, -4,
 FS_PRED_LEN_LE, FS_PRED_LEN_GE, FS_PRED_LEN_EQ, FS_PRED_COORD_GE = 1, 2, 3, 4
 FS_CONSUMER_COUNT, FS_CONSUMER_HIST, FS_CONSUMER_ANY, FS_CONSUMER_ROWS = 0, 1, 2, 3
 FS_MAX_D = 16
+FS_ORDER_CANONICAL, FS_ORDER_ANY = 0, 1
 
 u64 = ctypes.c_uint64
 i64 = ctypes.c_int64
@@ -31,7 +32,8 @@ class ExecT(ctypes.Structure):
         ("world", ctypes.c_int),
         ("slice_units", ctypes.c_uint64),
         ("ctas_per_sm", ctypes.c_int),
-        ("reserved", ctypes.c_int * 8),
+        ("order", ctypes.c_int),
+        ("reserved", ctypes.c_int * 7),
     ]
 
 

@@ -19,7 +19,7 @@ def _torch():
 
 
 def _exec(device: Optional[int] = None, stream=None, rank: int = 0, world: int = 1,
-          slice_units: int = 0, ctas_per_sm: int = 0) -> L.ExecT:
+          slice_units: int = 0, ctas_per_sm: int = 0, order: int = 0) -> L.ExecT:
     ex = L.ExecT()
     ex.device = -1 if device is None else int(device)
     ex.cuda_stream = None if stream is None else ctypes.c_void_p(int(stream))
@@ -27,6 +27,7 @@ def _exec(device: Optional[int] = None, stream=None, rank: int = 0, world: int =
     ex.world = int(world)
     ex.slice_units = int(slice_units)
     ex.ctas_per_sm = int(ctas_per_sm)
+    ex.order = int(order)
     return ex
 
 
@@ -122,11 +123,12 @@ def fs_any_ex(n, gens, pred, pred_arg, *, device=None, stream=None, rank=0, worl
 
 
 def fs_enumerate_ex(n, gens, B=16, cap=None, out=None, *, device=None, stream=None, rank=0, world=1,
-                    slice_units=0, ctas_per_sm=0):
-    """This rank's block of rows.  Returns (rank_rows, global_row_offset, rows_tensor)."""
+                    slice_units=0, ctas_per_sm=0, order=L.FS_ORDER_CANONICAL):
+    """This rank's block of rows.  Returns (rank_rows, global_row_offset, rows_tensor).
+    order=FS_ORDER_ANY: warp-compacted (M2) layout, same multiset of rows, arbitrary order."""
     torch = _torch()
     g, d = L.gens_array(gens)
-    ex = _exec(device, _stream_handle(stream), rank, world, slice_units, ctas_per_sm)
+    ex = _exec(device, _stream_handle(stream), rank, world, slice_units, ctas_per_sm, order)
     if cap is None:
         info = Plan(n, gens, L.FS_CONSUMER_ROWS, rank=rank, world=world).info
         cap = info["row_end"] - info["row_begin"]
@@ -147,13 +149,13 @@ class Plan:
 
     def __init__(self, n: int, gens: Sequence[int], consumer: int = L.FS_CONSUMER_COUNT, *,
                  device: Optional[int] = None, stream=None, rank: int = 0, world: int = 1,
-                 slice_units: int = 0, ctas_per_sm: int = 0):
+                 slice_units: int = 0, ctas_per_sm: int = 0, order: int = 0):
         self.n = int(n)
         self.gens = tuple(int(x) for x in gens)
         self.consumer = consumer
         g, d = L.gens_array(gens)
         self._stream = stream
-        ex = _exec(device, _stream_handle(stream), rank, world, slice_units, ctas_per_sm)
+        ex = _exec(device, _stream_handle(stream), rank, world, slice_units, ctas_per_sm, order)
         h = ctypes.c_void_p()
         L.check(L.lib().fs_plan_create(self.n, g, d, int(consumer), ctypes.byref(ex), ctypes.byref(h)),
                 "fs_plan_create")
@@ -198,3 +200,15 @@ class Plan:
 
     def last_launches(self) -> int:
         return int(L.lib().fs_plan_last_launches(self._h))
+
+
+def sort_rows_desc(rows):
+    """Canonical (decreasing lex) order of a [N, d] row tensor on the device -- used to
+    verify the order=any (M2) layout.  Stable sorts from the last coordinate to the first."""
+    torch = _torch()
+    x = rows.to(torch.int64)
+    idx = torch.arange(x.shape[0], device=x.device)
+    for j in range(x.shape[1] - 1, -1, -1):
+        order = torch.sort(x[idx, j], descending=True, stable=True).indices
+        idx = idx[order]
+    return rows[idx]

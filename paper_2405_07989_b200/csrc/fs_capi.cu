@@ -12,7 +12,7 @@
 namespace {
 
 // scratch layout (bytes): [0] queue u64, [8] count u64, [16] found i32, [64..128) witness
-constexpr size_t kOffCount = 8, kOffFound = 16, kOffWitness = 64;
+constexpr size_t kOffCount = 8, kOffFound = 16, kOffFront = 24, kOffBack = 32, kOffWitness = 64;
 
 struct DeviceGuard {
   int prev = -1;
@@ -198,6 +198,15 @@ int fs_plan_enumerate_async(fs_plan *p, int B, void *out_dev, uint64_t cap) {
   kp.num_claims = kp.num_slices;
   kp.rows_out = reinterpret_cast<unsigned char *>(out_dev);
   kp.row_bytes = (uint32_t)(p->d * (B / 8));
+  if (p->ex.order == FS_ORDER_ANY) {
+    if (take < span) return FS_ERANGE;  // compaction writes all of the rank's rows
+    char *base = reinterpret_cast<char *>(p->scratch_dev);
+    if (cudaMemsetAsync(base + kOffFront, 0, 16, p->stream) != cudaSuccess) return FS_ECUDA;
+    kp.front = reinterpret_cast<unsigned long long *>(base + kOffFront);
+    kp.back = reinterpret_cast<unsigned long long *>(base + kOffBack);
+    kp.rank_rows = span;
+    return finish(p, fs_launch(p, fs::kConsRowsAny, B, kp, p->stream));
+  }
   return finish(p, fs_launch(p, FS_CONSUMER_ROWS, B, kp, p->stream));
 }
 
@@ -292,6 +301,14 @@ int64_t fs_enumerate_ex(uint64_t n, const uint32_t *gens, int d, int B, void *ou
     DeviceGuard g(h.p->device);
     rc = sync_plan(h.p);
     if (rc != FS_OK) return rc;
+    if (h.p->ex.order == FS_ORDER_ANY && h.p->row_end > h.p->row_begin) {
+      // M2 exactness check: the front and back cursors must meet at the rank's row count
+      unsigned long long cur[2] = {0, 0};
+      if (cudaMemcpy(cur, reinterpret_cast<char *>(h.p->scratch_dev) + kOffFront, 16, cudaMemcpyDeviceToHost) !=
+          cudaSuccess)
+        return FS_ECUDA;
+      if (cur[0] + cur[1] != h.p->row_end - h.p->row_begin) return FS_ECUDA;
+    }
   }
   if (global_row_offset_out) *global_row_offset_out = h.p->row_begin;
   return (int64_t)(h.p->row_end - h.p->row_begin);

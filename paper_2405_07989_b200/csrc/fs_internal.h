@@ -16,6 +16,8 @@ constexpr int kBlock = 256;          // threads per persistent CTA
 constexpr int kStageBytes = 256;     // per-lane staging ring for materialise (2 x 128 B)
 constexpr uint32_t kKtabMax = 8192;  // k0 table in shared memory if g_{d-1} <= this
 constexpr uint32_t kHistSmemMax = 24576;  // u32 histogram bins kept in shared memory
+constexpr int kConsRowsAny = 4;           // internal consumer: materialise, order = any (M2)
+constexpr uint32_t kWarpBuf = 4096;       // M2 per-warp compaction buffer (bytes)
 
 // Everything a kernel needs, by value (fits the 4 KB parameter space comfortably).
 struct KParams {
@@ -38,6 +40,11 @@ struct KParams {
   uint32_t *witness;
   unsigned char *rows_out;
   uint32_t row_bytes;
+  // M2 (order = any): front cursor (rows, grows up in 8-row blocks) and back cursor (rows,
+  // grows down from rank_rows for each warp's final < 8 rows); must meet exactly.
+  unsigned long long *front;
+  unsigned long long *back;
+  uint64_t rank_rows;
 };
 
 }  // namespace fs

@@ -138,6 +138,76 @@ struct EmitRows {
   }
 };
 
+__device__ __forceinline__ uint32_t lanemask_lt() {
+  uint32_t m;
+  asm("mov.u32 %0, %%lanemask_lt;" : "=r"(m));
+  return m;
+}
+
+// M2 (order = any): warp-aggregated compaction.  Each fast step, the warp's valid rows are
+// ranked with one ballot and appended contiguously to the warp's shared buffer; when the
+// buffer is nearly full the warp reserves a block of 8k rows with ONE atomicAdd on the front
+// cursor (8 rows keep every block 16 B aligned) and writes it with coalesced 16 B stores.
+template <int D, int B>
+struct EmitCompact {
+  static constexpr uint32_t kRB = D * (B / 8);
+  static constexpr uint32_t kCap = kWarpBuf / kRB;
+  unsigned char *buf;
+  uint32_t wrows;  // warp-uniform
+  __device__ __forceinline__ void put(unsigned char *q, int i, uint32_t v) {
+    if (B == 16)
+      *reinterpret_cast<uint16_t *>(q + 2 * i) = (uint16_t)v;
+    else
+      *reinterpret_cast<uint32_t *>(q + 4 * i) = v;
+  }
+  __device__ __forceinline__ void cond(bool em, const Lane<D> &st) {
+    const unsigned m = __ballot_sync(kFull, em);
+    if (em) {
+      unsigned char *q = buf + (wrows + (uint32_t)__popc(m & lanemask_lt())) * kRB;
+#pragma unroll
+      for (int j = 0; j < D - 2; ++j) put(q, j, st.a[j]);
+      put(q, D - 2, (uint32_t)st.cur);
+      put(q, D - 1, st.ad);
+    }
+    wrows += (uint32_t)__popc(m);
+  }
+  // converged; flush 8k rows when the buffer cannot take another full warp of rows
+  __device__ __forceinline__ void flush(const KParams &P, bool final) {
+    if (!final && wrows + 32 <= kCap) return;
+    const uint32_t k = wrows & ~7u;
+    if (k == 0) return;
+    __syncwarp();
+    const int lane = threadIdx.x & 31;
+    unsigned long long off = 0;
+    if (lane == 0) off = atomicAdd(P.front, (unsigned long long)k);
+    off = __shfl_sync(kFull, off, 0);
+    const uint32_t bytes = k * kRB;  // multiple of 16
+    uint4 *dst = reinterpret_cast<uint4 *>(P.rows_out + off * kRB);
+    const uint4 *src = reinterpret_cast<const uint4 *>(buf);
+    for (uint32_t i = lane; i < bytes / 16; i += 32) __stcs(dst + i, src[i]);
+    __syncwarp();
+    const uint32_t rem = (wrows - k) * kRB;  // < 8 rows; source and destination do not overlap
+    for (uint32_t i = 2u * lane; i < rem; i += 64u)
+      *reinterpret_cast<uint16_t *>(buf + i) = *reinterpret_cast<const uint16_t *>(buf + bytes + i);
+    __syncwarp();
+    wrows -= k;
+  }
+  // converged, at warp exit: the final < 8 rows go to the back cursor with plain stores
+  __device__ __forceinline__ void finish(const KParams &P) {
+    flush(P, true);
+    if (wrows == 0) return;
+    const int lane = threadIdx.x & 31;
+    unsigned long long b = 0;
+    if (lane == 0) b = atomicAdd(P.back, (unsigned long long)wrows);
+    b = __shfl_sync(kFull, b, 0);
+    const uint64_t pos = P.rank_rows - b - wrows;
+    unsigned char *dst = P.rows_out + pos * kRB;
+    for (uint32_t i = 2u * lane; i < wrows * kRB; i += 64u)
+      *reinterpret_cast<uint16_t *>(dst + i) = *reinterpret_cast<const uint16_t *>(buf + i);
+    wrows = 0;
+  }
+};
+
 // Warp-cooperative copy of every lane's pending ring segment: 4 segments per round, 8 lanes
 // x 16 B each -> fully coalesced 128 B stores.  len is a multiple of 16.
 __device__ __forceinline__ void warp_flush(bool &pend, uint32_t soff, uint64_t goff, uint32_t len,
@@ -197,7 +267,7 @@ __device__ __forceinline__ uint64_t bitrev_bits(uint64_t x, uint32_t bits) {
 template <int D, int CONS, int B, bool KTAB>
 __global__ void __launch_bounds__(kBlock) fs_enum_kernel(const KParams P) {
   constexpr bool NEED_AD = CONS != FS_CONSUMER_COUNT;
-  constexpr int ALPHA = CONS == FS_CONSUMER_ROWS ? 0 : 1;
+  constexpr int ALPHA = (CONS == FS_CONSUMER_ROWS || CONS == kConsRowsAny) ? 0 : 1;
   constexpr int INNER = Inner<CONS>::value;
   constexpr int UNROLL = CONS == FS_CONSUMER_ROWS ? 1 : 4;
   extern __shared__ __align__(16) unsigned char smem[];
@@ -251,6 +321,9 @@ __global__ void __launch_bounds__(kBlock) fs_enum_kernel(const KParams P) {
   uint32_t fin_soff = 0, fin_len = 0;
   uint64_t fin_goff = 0;
   const unsigned char *warp_stage = stage + (threadIdx.x & ~31) * kStageBytes;
+  EmitCompact<D, B> e_cmp;
+  e_cmp.buf = stage + (threadIdx.x >> 5) * kWarpBuf;
+  e_cmp.wrows = 0;
 
   for (;;) {
     const bool need = alive && budget == 0;
@@ -322,6 +395,9 @@ __global__ void __launch_bounds__(kBlock) fs_enum_kernel(const KParams P) {
           fast_step<D, NEED_AD, ALPHA>(st, c, kt, budget, e_hist);
         } else if (CONS == FS_CONSUMER_ANY) {
           fast_step<D, NEED_AD, ALPHA>(st, c, kt, budget, e_any);
+        } else if (CONS == kConsRowsAny) {
+          fast_step<D, NEED_AD, ALPHA>(st, c, kt, budget, e_cmp);
+          e_cmp.flush(P, false);
         } else {
           const bool was = budget != 0;
           fast_step<D, NEED_AD, ALPHA>(st, c, kt, budget, e_rows);
@@ -349,6 +425,7 @@ __global__ void __launch_bounds__(kBlock) fs_enum_kernel(const KParams P) {
   }
 
   // ---------------------------------------------------------------- epilogue
+  if (CONS == kConsRowsAny) e_cmp.finish(P);
   if (CONS == FS_CONSUMER_COUNT) {
     acc += e_count.n;
 #pragma unroll
@@ -382,7 +459,8 @@ __global__ void fs_d1_kernel(const KParams P) {
     }
     if (ok && atomicCAS(P.found, 0, 1) == 0 && P.witness) P.witness[0] = x;
   }
-  if (CONS == FS_CONSUMER_ROWS) {
+  if (CONS == FS_CONSUMER_ROWS || CONS == kConsRowsAny) {
+    if (CONS == kConsRowsAny) atomicAdd(P.front, 1ull);
     if (B == 16)
       *reinterpret_cast<uint16_t *>(P.rows_out) = (uint16_t)x;
     else
@@ -394,6 +472,7 @@ static size_t smem_bytes(const KParams &kp, int consumer) {
   size_t b = (size_t)((kp.c.ktab_len + 3u) & ~3u) * 4;
   if (consumer == FS_CONSUMER_HIST && kp.hist_smem) b += (size_t)((kp.hist_len + 3u) & ~3u) * 4;
   if (consumer == FS_CONSUMER_ROWS) b += (size_t)kBlock * kStageBytes;
+  if (consumer == kConsRowsAny) b += (size_t)(kBlock / 32) * kWarpBuf;
   return b;
 }
 
