@@ -89,7 +89,11 @@ enum {
  *   order       materialise layout: FS_ORDER_CANONICAL (0, default) writes every row at its
  *               exact canonical offset; FS_ORDER_ANY (1) compacts rows per warp with
  *               warp-aggregated atomics into an arbitrary order (the same multiset of rows;
- *               requires cap >= the rank's rows, else FS_ERANGE). */
+ *               requires cap >= the rank's rows, else FS_ERANGE).
+ *   tail        count consumer only: FS_TAIL_ROWS (0, default) steps through every valid
+ *               factorization of a node (one modulo-skip step per row); FS_TAIL_CLOSED (1)
+ *               counts a node's rows in O(1) as floor(a* / s) + 1 (the
+ *               closed form of the paper's suffix-set idea).  Same result. */
 typedef struct {
     int device;
     void *cuda_stream;
@@ -98,10 +102,12 @@ typedef struct {
     uint64_t slice_units;
     int ctas_per_sm;
     int order;
-    int reserved[7];
+    int tail;
+    int reserved[6];
 } fs_exec_t;
 
 enum { FS_ORDER_CANONICAL = 0, FS_ORDER_ANY = 1 };
+enum { FS_TAIL_ROWS = 0, FS_TAIL_CLOSED = 1 };
 
 /* ---------------------------------------------------------------------------------
  * north_star entry points: current CUDA device, default stream, whole instance.

@@ -16,6 +16,7 @@ FS_PRED_LEN_LE, FS_PRED_LEN_GE, FS_PRED_LEN_EQ, FS_PRED_COORD_GE = 1, 2, 3, 4
 FS_CONSUMER_COUNT, FS_CONSUMER_HIST, FS_CONSUMER_ANY, FS_CONSUMER_ROWS = 0, 1, 2, 3
 FS_MAX_D = 16
 FS_ORDER_CANONICAL, FS_ORDER_ANY = 0, 1
+FS_TAIL_ROWS, FS_TAIL_CLOSED = 0, 1
 
 u64 = ctypes.c_uint64
 i64 = ctypes.c_int64
@@ -33,7 +34,8 @@ class ExecT(ctypes.Structure):
         ("slice_units", ctypes.c_uint64),
         ("ctas_per_sm", ctypes.c_int),
         ("order", ctypes.c_int),
-        ("reserved", ctypes.c_int * 7),
+        ("tail", ctypes.c_int),
+        ("reserved", ctypes.c_int * 6),
     ]
 
 

@@ -19,7 +19,7 @@ def _torch():
 
 
 def _exec(device: Optional[int] = None, stream=None, rank: int = 0, world: int = 1,
-          slice_units: int = 0, ctas_per_sm: int = 0, order: int = 0) -> L.ExecT:
+          slice_units: int = 0, ctas_per_sm: int = 0, order: int = 0, tail: int = 0) -> L.ExecT:
     ex = L.ExecT()
     ex.device = -1 if device is None else int(device)
     ex.cuda_stream = None if stream is None else ctypes.c_void_p(int(stream))
@@ -28,6 +28,7 @@ def _exec(device: Optional[int] = None, stream=None, rank: int = 0, world: int =
     ex.slice_units = int(slice_units)
     ex.ctas_per_sm = int(ctas_per_sm)
     ex.order = int(order)
+    ex.tail = int(tail)
     return ex
 
 
@@ -90,9 +91,10 @@ def fs_enumerate(n: int, gens: Sequence[int], B: int = 16, cap: Optional[int] = 
 
 
 # ------------------------------------------------------------------ _ex variants
-def fs_count_ex(n, gens, *, device=None, stream=None, rank=0, world=1, slice_units=0, ctas_per_sm=0) -> int:
+def fs_count_ex(n, gens, *, device=None, stream=None, rank=0, world=1, slice_units=0, ctas_per_sm=0,
+                tail=L.FS_TAIL_ROWS) -> int:
     g, d = L.gens_array(gens)
-    ex = _exec(device, _stream_handle(stream), rank, world, slice_units, ctas_per_sm)
+    ex = _exec(device, _stream_handle(stream), rank, world, slice_units, ctas_per_sm, 0, tail)
     out = ctypes.c_uint64(0)
     L.check(L.lib().fs_count_ex(int(n), g, d, ctypes.byref(ex), ctypes.byref(out)), "fs_count_ex")
     return int(out.value)
@@ -149,13 +151,13 @@ class Plan:
 
     def __init__(self, n: int, gens: Sequence[int], consumer: int = L.FS_CONSUMER_COUNT, *,
                  device: Optional[int] = None, stream=None, rank: int = 0, world: int = 1,
-                 slice_units: int = 0, ctas_per_sm: int = 0, order: int = 0):
+                 slice_units: int = 0, ctas_per_sm: int = 0, order: int = 0, tail: int = 0):
         self.n = int(n)
         self.gens = tuple(int(x) for x in gens)
         self.consumer = consumer
         g, d = L.gens_array(gens)
         self._stream = stream
-        ex = _exec(device, _stream_handle(stream), rank, world, slice_units, ctas_per_sm, order)
+        ex = _exec(device, _stream_handle(stream), rank, world, slice_units, ctas_per_sm, order, tail)
         h = ctypes.c_void_p()
         L.check(L.lib().fs_plan_create(self.n, g, d, int(consumer), ctypes.byref(ex), ctypes.byref(h)),
                 "fs_plan_create")

@@ -143,7 +143,8 @@ int fs_plan_count_async(fs_plan *p, uint64_t *count_dev) {
   if (cudaMemsetAsync(count_dev, 0, 8, p->stream) != cudaSuccess) return FS_ECUDA;
   fs::KParams kp = base_params(p);
   kp.count_out = reinterpret_cast<unsigned long long *>(count_dev);
-  return finish(p, fs_launch(p, FS_CONSUMER_COUNT, 16, kp, p->stream));
+  const int cons = p->ex.tail == FS_TAIL_CLOSED ? fs::kConsCountClosed : FS_CONSUMER_COUNT;
+  return finish(p, fs_launch(p, cons, 16, kp, p->stream));
 }
 
 int fs_plan_hist_async(fs_plan *p, uint64_t *hist_dev, uint64_t hist_cap) {

@@ -298,6 +298,41 @@ FS_HD void fast_step(Lane<D> &st, const Consts &c, const KT &kt, uint32_t &budge
   budget -= em ? 1u : 0u;
 }
 
+// NEXT-1 of SURVEY Sec. 8(f) (the paper's "dynamic behavior" future work, in its
+// cheapest closed form): for the COUNT consumer a node's valid a_{d-1} form the progression
+// a*, a*-s, ..., so its rows are counted in O(1) as floor(a*/s) + 1 (one magic division)
+// instead of one step per row.  Same units and slice boundaries as fast_step: a slice that
+// ends inside a node takes exactly its remaining budget of that node's rows.
+template <int D, class KT>
+FS_HD void fast_step_closed(Lane<D> &st, const Consts &c, const KT &kt, uint32_t &budget, uint32_t &cnt) {
+  constexpr int L = D - 2;
+  const bool act = budget != 0;
+  const bool has = st.cur >= 0;
+  bool fa = false;
+  if constexpr (L >= 1) {
+    const uint32_t al = st.a[L - 1];
+    fa = act && !has && al != 0;
+    uint32_t r2 = st.rho + c.delta;
+    const uint32_t cy = r2 >= c.gA ? 1u : 0u;
+    r2 = cy ? r2 - c.gA : r2;
+    const uint32_t A2 = st.A + c.q + cy;
+    st.rho = fa ? r2 : st.rho;
+    st.A = fa ? A2 : st.A;
+    st.a[L - 1] = al - (fa ? 1u : 0u);
+    const uint32_t k = kt(st.rho, c);
+    const int32_t nc = (int32_t)st.A - (int32_t)k;
+    st.cur = fa ? nc : st.cur;
+    budget -= fa ? 1u : 0u;
+  }
+  const bool em = (has || fa) && st.cur >= 0 && budget != 0;
+  const uint32_t rem = divq((uint32_t)(st.cur < 0 ? 0 : st.cur), c.dvS) + 1u;
+  uint32_t take = rem < budget ? rem : budget;
+  take = em ? take : 0u;
+  cnt += take;
+  budget -= take;
+  st.cur = em ? -1 : st.cur;
+}
+
 template <int D>
 FS_HD bool needs_slow(const Lane<D> &st, uint32_t budget) {
   constexpr int L = D - 2;

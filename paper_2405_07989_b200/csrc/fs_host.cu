@@ -301,10 +301,20 @@ void host_model_d(const fs_plan *p, const KT &ktab, HostSink &sink, uint64_t *sl
     sink.slice_rows = 0;
     sink.have_first = false;
     HostEmit<D> emit{&sink};
-    // the kernels' schedule: branch-free fast steps, generic step() for lanes needing an ascend
-    while (budget > 0) {
-      fs::fast_step<D, true, ALPHA>(st, c, ktab, budget, emit);
-      if (fs::needs_slow<D>(st, budget)) fs::slow_step<D, true, ALPHA>(st, c, ktab, budget);
+    // the kernels' schedule: branch-free fast steps, slow_step() for lanes needing an ascend
+    if (ALPHA && p->consumer == FS_CONSUMER_COUNT && p->ex.tail == FS_TAIL_CLOSED) {
+      uint32_t cnt = 0;
+      while (budget > 0) {
+        fs::fast_step_closed<D>(st, c, ktab, budget, cnt);
+        if (fs::needs_slow<D>(st, budget)) fs::slow_step<D, true, ALPHA>(st, c, ktab, budget);
+      }
+      sink.count += cnt;
+      sink.slice_rows = cnt;
+    } else {
+      while (budget > 0) {
+        fs::fast_step<D, true, ALPHA>(st, c, ktab, budget, emit);
+        if (fs::needs_slow<D>(st, budget)) fs::slow_step<D, true, ALPHA>(st, c, ktab, budget);
+      }
     }
     if (slice_counts) slice_counts[sl] = sink.slice_rows;
     if (slice_first) {

@@ -18,6 +18,7 @@ constexpr uint32_t kKtabMax = 8192;  // k0 table in shared memory if g_{d-1} <= 
 constexpr uint32_t kHistSmemMax = 24576;  // u32 histogram bins kept in shared memory
 constexpr int kConsRowsAny = 4;           // internal consumer: materialise, order = any (M2)
 constexpr uint32_t kWarpBuf = 4096;       // M2 per-warp compaction buffer (bytes)
+constexpr int kConsCountClosed = 5;       // internal consumer: count with the closed-form tail
 
 // Everything a kernel needs, by value (fits the 4 KB parameter space comfortably).
 struct KParams {

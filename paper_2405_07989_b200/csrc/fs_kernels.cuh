@@ -266,7 +266,7 @@ __device__ __forceinline__ uint64_t bitrev_bits(uint64_t x, uint32_t bits) {
 
 template <int D, int CONS, int B, bool KTAB>
 __global__ void __launch_bounds__(kBlock) fs_enum_kernel(const KParams P) {
-  constexpr bool NEED_AD = CONS != FS_CONSUMER_COUNT;
+  constexpr bool NEED_AD = CONS != FS_CONSUMER_COUNT && CONS != kConsCountClosed;
   constexpr int ALPHA = (CONS == FS_CONSUMER_ROWS || CONS == kConsRowsAny) ? 0 : 1;
   constexpr int INNER = Inner<CONS>::value;
   constexpr int UNROLL = CONS == FS_CONSUMER_ROWS ? 1 : 4;
@@ -330,7 +330,7 @@ __global__ void __launch_bounds__(kBlock) fs_enum_kernel(const KParams P) {
     const unsigned needm = __ballot_sync(kFull, need);
     if (needm) {
       if (need) {
-        if (CONS == FS_CONSUMER_COUNT) {
+        if (CONS == FS_CONSUMER_COUNT || CONS == kConsCountClosed) {
           acc += e_count.n;
           e_count.n = 0;
         } else if (CONS == FS_CONSUMER_HIST) {
@@ -391,6 +391,8 @@ __global__ void __launch_bounds__(kBlock) fs_enum_kernel(const KParams P) {
       for (int u = 0; u < UNROLL; ++u) {
         if (CONS == FS_CONSUMER_COUNT) {
           fast_step<D, NEED_AD, ALPHA>(st, c, kt, budget, e_count);
+        } else if (CONS == kConsCountClosed) {
+          fast_step_closed<D>(st, c, kt, budget, e_count.n);
         } else if (CONS == FS_CONSUMER_HIST) {
           fast_step<D, NEED_AD, ALPHA>(st, c, kt, budget, e_hist);
         } else if (CONS == FS_CONSUMER_ANY) {
@@ -426,7 +428,7 @@ __global__ void __launch_bounds__(kBlock) fs_enum_kernel(const KParams P) {
 
   // ---------------------------------------------------------------- epilogue
   if (CONS == kConsRowsAny) e_cmp.finish(P);
-  if (CONS == FS_CONSUMER_COUNT) {
+  if (CONS == FS_CONSUMER_COUNT || CONS == kConsCountClosed) {
     acc += e_count.n;
 #pragma unroll
     for (int o = 16; o > 0; o >>= 1) acc += __shfl_xor_sync(kFull, acc, o);
@@ -447,7 +449,7 @@ __global__ void fs_d1_kernel(const KParams P) {
   if (threadIdx.x != 0 || blockIdx.x != 0) return;
   if (!(P.unit0 == 0 && P.unit1 > 0)) return;
   const uint32_t x = P.c.n / P.c.g[0];
-  if (CONS == FS_CONSUMER_COUNT) atomicAdd(P.count_out, 1ull);
+  if (CONS == FS_CONSUMER_COUNT || CONS == kConsCountClosed) atomicAdd(P.count_out, 1ull);
   if (CONS == FS_CONSUMER_HIST) atomicAdd(&P.hist_out[x], 1ull);
   if (CONS == FS_CONSUMER_ANY) {
     bool ok;

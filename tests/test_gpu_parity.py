@@ -88,6 +88,14 @@ def test_tiny_slices(oracle_mod, inst, T):
     assert rows_bytes(t) == oracle.rows(n, g, B=32)
 
 
+@pytest.mark.parametrize("inst", ALL, ids=ids)
+def test_count_closed_tail(oracle_mod, inst):
+    n, g = inst.n, inst.gens
+    want = oracle.count(n, g)
+    for T in (0, 1, 5):
+        assert api.fs_count_ex(n, g, slice_units=T, tail=L.FS_TAIL_CLOSED) == want
+
+
 @pytest.mark.parametrize("inst", ALL[:40], ids=ids)
 def test_any(oracle_mod, inst):
     n, g = inst.n, inst.gens
@@ -177,6 +185,7 @@ def test_virtual_ranks(oracle_mod, world):
 # ------------------------------------------------------------------ full-size configs
 def test_c3_count_full():
     assert api.fs_count(W.C3.n, W.C3.gens) == gold("C3")["count"] == 100032405189
+    assert api.fs_count_ex(W.C3.n, W.C3.gens, tail=L.FS_TAIL_CLOSED) == 100032405189
 
 
 def test_c4_hist_full():

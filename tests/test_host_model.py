@@ -65,6 +65,18 @@ def test_host_model_matches_oracle(oracle_mod, inst):
         assert r["rows"] == want_rows
 
 
+@pytest.mark.parametrize("inst", INSTANCES, ids=lambda i: "%s" % i.name)
+def test_closed_tail_count(oracle_mod, inst):
+    """NEXT-1 closed-form tail: same count, and the same per-slice counts, as the row steps."""
+    n, g = inst.n, inst.gens
+    want = oracle.count(n, g)
+    for T in (0, 1, 2, 7):
+        a = host_model(n, g, L.FS_CONSUMER_COUNT, slice_units=T, want_slices=True, tail=L.FS_TAIL_CLOSED)
+        b = host_model(n, g, L.FS_CONSUMER_COUNT, slice_units=T, want_slices=True)
+        assert a["count"] == want
+        assert a["slice_counts"] == b["slice_counts"]
+
+
 @pytest.mark.parametrize("inst", INSTANCES[:30], ids=lambda i: "%s" % i.name)
 def test_slices_exact_and_gap_free(oracle_mod, inst):
     """Per-slice row counts equal the oracle's rows in that lex range: no gaps, no overlap."""
