@@ -376,7 +376,23 @@ def main():
     return 0
 
 
+def _time_ms(fn, stream, reps, barrier, max_over_ranks):
+    import torch
+
+    ts = []
+    barrier()
+    for _ in range(reps):
+        a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        a.record(stream)
+        fn()
+        b.record(stream)
+        torch.cuda.synchronize()
+        ts.append(a.elapsed_time(b))
+    return max_over_ranks(statistics.median(ts))
+
+
 def extras(args, world, rank, local, dev, stream, peaks, peaks_kind, barrier, max_over_ranks, mb):
+    """Same-run measurements of the other hot-path consumers (each on its BASELINE config)."""
     import torch
     import torch.distributed as dist
 
@@ -384,59 +400,84 @@ def extras(args, world, rank, local, dev, stream, peaks, peaks_kind, barrier, ma
     from paper_2405_07989_b200 import api
 
     ex = {}
-    # store: C2-XL rows, u16, canonical order at exact offsets
-    inst = W.C2XL
-    p = api.Plan(inst.n, inst.gens, L.FS_CONSUMER_ROWS, device=local, stream=stream.cuda_stream, rank=rank,
-                 world=world)
-    info = p.info
-    rows = info["row_end"] - info["row_begin"]
-    out = torch.empty((rows, inst.d), dtype=torch.uint16, device=dev)
-    for _ in range(2):
-        p.enumerate_async(16, out, rows)
-    ts = []
-    barrier()
-    for _ in range(3):
-        a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-        a.record(stream)
-        p.enumerate_async(16, out, rows)
-        b.record(stream)
-        torch.cuda.synchronize()
-        ts.append(a.elapsed_time(b))
-    ms = max_over_ranks(statistics.median(ts))
-    total_rows = info["total_rows"]
-    bytes_ = total_rows * inst.d * 2
-    gbs = (rows * inst.d * 2) / (statistics.median(ts) / 1e3) / 1e9
-    gbs_all = bytes_ / (ms / 1e3) / 1e9
-    ex["store"] = {"workload": "C2XL: Z(16000, (11,13,17,19,23)) materialise u16 rows (canonical order)",
-                   "rows": total_rows, "bytes": bytes_, "ms": ms, "value": total_rows / (ms / 1e3), "unit": UNIT,
-                   "roofline": {"bound": "hbm", "achieved": gbs_all, "peak": peaks["hbm_gbs"] * world,
-                                "unit": "GB/s", "frac": gbs_all / (peaks["hbm_gbs"] * world),
-                                "peak_source": "MEASURED_PEAKS.json hbm_gbs (%s, copy r+w)" % peaks_kind,
-                                "per_gpu_gbs": gbs,
-                                "frac_of_write_microbench": (gbs / mb["hbm_write_gbs"]) if mb else None}}
-    del out
-    torch.cuda.empty_cache()
-    # C4 length histogram
-    inst = W.C4
-    p = api.Plan(inst.n, inst.gens, L.FS_CONSUMER_HIST, device=local, stream=stream.cuda_stream, rank=rank,
-                 world=world)
-    h = torch.zeros(api.hist_len(inst.n, inst.gens), dtype=torch.int64, device=dev)
-    p.hist_async(h)
-    ts = []
-    barrier()
-    for _ in range(2):
-        a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-        a.record(stream)
-        p.hist_async(h)
+    kw = dict(device=local, stream=stream.cuda_stream, rank=rank, world=world)
+
+    def allreduce(t, op=None):
         if world > 1:
-            dist.all_reduce(h, op=dist.ReduceOp.SUM)
-        b.record(stream)
-        torch.cuda.synchronize()
-        ts.append(a.elapsed_time(b))
-    ms = max_over_ranks(statistics.median(ts))
+            dist.all_reduce(t, op=op or dist.ReduceOp.SUM)
+
+    # ---- store: C2-XL rows, u16; canonical layout (M1) and warp-compacted layout (M2)
+    inst = W.C2XL
+    for order, key in ((L.FS_ORDER_CANONICAL, "store"), (L.FS_ORDER_ANY, "store_any")):
+        p = api.Plan(inst.n, inst.gens, L.FS_CONSUMER_ROWS, order=order, **kw)
+        info = p.info
+        rows = info["row_end"] - info["row_begin"]
+        out = torch.empty((rows, inst.d), dtype=torch.uint16, device=dev)
+        p.enumerate_async(16, out, rows)
+        ms = _time_ms(lambda: p.enumerate_async(16, out, rows), stream, 3, barrier, max_over_ranks)
+        total_rows = info["total_rows"]
+        bytes_ = total_rows * inst.d * 2
+        gbs_all = bytes_ / (ms / 1e3) / 1e9
+        peak = peaks["hbm_gbs"] * world
+        ex[key] = {"workload": "C2XL: Z(16000, (11,13,17,19,23)) materialise u16 rows, %s order"
+                               % ("canonical (exact offsets)" if order == 0 else "any (warp compaction)"),
+                   "rows": total_rows, "bytes": bytes_, "ms": ms, "value": total_rows / (ms / 1e3), "unit": UNIT,
+                   "roofline": {"bound": "hbm", "achieved": gbs_all, "peak": peak, "unit": "GB/s",
+                                "frac": gbs_all / peak,
+                                "peak_source": "MEASURED_PEAKS.json hbm_gbs x %d (%s, copy r+w)" % (world, peaks_kind),
+                                "frac_of_write_microbench": (gbs_all / world / mb["hbm_write_gbs"]) if mb else None}}
+        del out
+        torch.cuda.empty_cache()
+
+    # ---- C4 length histogram
+    inst = W.C4
+    p = api.Plan(inst.n, inst.gens, L.FS_CONSUMER_HIST, **kw)
+    h = torch.zeros(api.hist_len(inst.n, inst.gens), dtype=torch.int64, device=dev)
+
+    def hist_step():
+        p.hist_async(h)
+        allreduce(h)
+
+    ms = _time_ms(hist_step, stream, 2, barrier, max_over_ranks)
     total = int(h.sum().item())
     ex["hist"] = {"workload": "C4: Z(4275, C3 gens) length histogram (329 bins)", "rows": total, "ms": ms,
                   "value": total / (ms / 1e3), "unit": UNIT}
+
+    # ---- C3 count with the NEXT-1 closed-form tail
+    inst = W.C3
+    p = api.Plan(inst.n, inst.gens, L.FS_CONSUMER_COUNT, tail=L.FS_TAIL_CLOSED, **kw)
+    c = torch.zeros(1, dtype=torch.int64, device=dev)
+
+    def cc_step():
+        p.count_async(c)
+        allreduce(c)
+
+    ms = _time_ms(cc_step, stream, 3, barrier, max_over_ranks)
+    ex["count_closed_tail"] = {"workload": "C3 count, closed-form 2-D tail (NEXT-1)", "rows": int(c.item()),
+                               "ms": ms, "value": int(c.item()) / (ms / 1e3), "unit": UNIT}
+
+    # ---- C5: skewed/non-minimal generators: count and the any-predicates (early exit)
+    inst = W.C5
+    p = api.Plan(inst.n, inst.gens, L.FS_CONSUMER_COUNT, **kw)
+
+    def c5_step():
+        p.count_async(c)
+        allreduce(c)
+
+    ms = _time_ms(c5_step, stream, 1, barrier, max_over_ranks)
+    ex["c5_count"] = {"workload": "C5: Z(20000, (1,1,2,997,1000)) count", "rows": int(c.item()), "ms": ms,
+                      "value": int(c.item()) / (ms / 1e3), "unit": UNIT}
+    pa = api.Plan(inst.n, inst.gens, L.FS_CONSUMER_ANY, **kw)
+    f = torch.zeros(1, dtype=torch.int32, device=dev)
+    w = torch.zeros(inst.d, dtype=torch.int32, device=dev)
+    for name, pred, arg in (("P_late", L.FS_PRED_LEN_LE, 20), ("P_none", L.FS_PRED_LEN_LE, 19),
+                            ("P_first", L.FS_PRED_LEN_GE, 19995)):
+        def any_step():
+            pa.any_async(pred, arg, f, w)
+            allreduce(f, dist.ReduceOp.MAX if world > 1 else None)
+
+        ms = _time_ms(any_step, stream, 1, barrier, max_over_ranks)
+        ex["c5_any_" + name] = {"pred": [pred, arg], "found": bool(f.item()), "ms": ms}
     return ex
 
 
