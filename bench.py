@@ -328,7 +328,7 @@ def main():
                    "instance": inst.name, "n": inst.n, "gens": list(inst.gens), "consumer": "count",
                    "parallelism": "lex-slice dp%d" % world, "l2": "flushed between steps (256 MB write)",
                    "slice_units": info["slice_units"], "num_slices": info["num_slices"],
-                   "grid": info["grid"], "block": info["block"]},
+                   "grid": plan.info["grid"], "block": info["block"]},
         "roofline": {"bound": "alu", "achieved": achieved, "peak": peak_tops, "unit": "Tops/s (int32 lane-ops)",
                      "frac": achieved / peak_tops, "traffic": traffic,
                      "peak_source": ("measured: best INT32 microbenchmark (fs_micro.cu)" if measured_tops else

@@ -213,4 +213,4 @@ def sort_rows_desc(rows):
     for j in range(x.shape[1] - 1, -1, -1):
         order = torch.sort(x[idx, j], descending=True, stable=True).indices
         idx = idx[order]
-    return rows[idx]
+    return x[idx].to(rows.dtype)

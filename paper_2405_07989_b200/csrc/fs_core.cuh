@@ -21,12 +21,13 @@
 //   candidate: it visits every node the paper's stream visits, in the same order, and emits
 //   the same factorizations in the same order (Thm. 3.2/3.3).
 //
-// Units and slices: the stream is a sequence of units -- for each node in lex-descending
-// order, one ENTRY unit (alpha = 1; 0 for row-sliced plans) followed by one unit per ROW
-// (beta = 1).  The exact DP tables U[k][r] (units below a level-k node with residual r) let
-// a lane jump to any unit index (unrank) and run exactly `budget` units, so slices are
-// disjoint, gap-free and equal in work (a finer, exact form of the paper's bound splitting,
-// P:196-225, and of the "better work division" of P:316-317).
+// Units and slices: a slice is a range of units of the stream.  Count / histogram / any
+// plans use NODE units (alpha = 1, beta = 0): a slice owns whole nodes with all their rows.
+// Materialise plans use ROW units (alpha = 0, beta = 1): a slice owns exactly T rows, so it
+// writes them at exact canonical offsets.  The exact DP tables U[k][r] (units below a
+// level-k node with residual r) let a lane jump to any unit index (unrank) and run exactly
+// `budget` units, so slices are disjoint, gap-free and equal in work (a finer, exact form of
+// the paper's bound splitting, and of its "better work division").
 #pragma once
 
 #include <stdint.h>
@@ -228,20 +229,21 @@ FS_HD uint64_t unrank(Lane<D> &st, const Consts &c, const KT &kt, uint64_t u) {
   return u;
 }
 
-// After unrank(): consume the entry unit or skip to row j of the node.  Returns the units
-// consumed (0 or 1).
+// After unrank(): node-unit plans (alpha = 1) start at the node's entry, which is consumed
+// here (returns 1); row-unit plans (alpha = 0) skip to row `off` of the node (returns 0).
 template <int D, bool NEED_AD>
 FS_HD uint32_t position_in_node(Lane<D> &st, const Consts &c, uint64_t off) {
-  uint64_t j;
-  if (c.alpha) {
-    if (off == 0) return 1;
-    j = off - 1;
-  } else {
-    j = off;
-  }
-  st.cur -= (int32_t)((uint32_t)j * c.s);
-  if (NEED_AD) st.ad += (uint32_t)j * c.t;
+  if (c.alpha) return 1;  // off == 0: node units never split a node
+  st.cur -= (int32_t)((uint32_t)off * c.s);
+  if (NEED_AD) st.ad += (uint32_t)off * c.t;
   return 0;
+}
+
+// A lane needs a new slice when its budget is spent and -- for node-unit slices, whose last
+// node's rows all belong to the slice -- its current node has no rows left.
+template <int D, int ALPHA>
+FS_HD bool needs_refill(const Lane<D> &st, uint32_t budget) {
+  return ALPHA ? (budget == 0 && st.cur < 0) : (budget == 0);
 }
 
 // Slow step, for a lane whose node is exhausted and whose level-L coordinate is 0: Alg. 3.1
@@ -258,11 +260,12 @@ FS_HD void slow_step(Lane<D> &st, const Consts &c, const KT &kt, uint32_t &budge
   budget -= ALPHA;
 }
 
-// Branch-free fast step for SIMT lanes.  Every active lane does, under predicates:
+// Branch-free fast step for SIMT lanes.  Every lane does, under predicates:
 //   - a row lane (cur >= 0) emits its row and steps a_{d-1} -= s;
-//   - a lane whose node is exhausted and whose level-L coordinate a_L > 0 advances to the next
-//     node (a_L -= 1, residual += g_L, incremental floor/residue of R_L by g_{d-1}), solves the
-//     node's first valid row through k0 (ENTRY unit) and, budget permitting, emits it.
+//   - a lane with budget whose node is exhausted and whose level-L coordinate a_L > 0
+//     advances to the next node (a_L -= 1, residual += g_L, incremental floor/residue of R_L
+//     by g_{d-1}), solves the node's first valid row through k0 and emits it (row units:
+//     budget permitting).
 // Lanes that need the rare ascend (a_L = 0) or end of stream do nothing here and are left for
 // slow_step() (needs_slow()).
 template <int D, bool NEED_AD, int ALPHA, class KT, class Emit>
@@ -291,18 +294,20 @@ FS_HD void fast_step(Lane<D> &st, const Consts &c, const KT &kt, uint32_t &budge
     }
     if (ALPHA) budget -= fa ? 1u : 0u;
   }
-  const bool em = (has || fa) && st.cur >= 0 && budget != 0;
+  // node units: every row of an entered node belongs to the slice; row units: budget-limited
+  const bool em = ALPHA ? (st.cur >= 0) : (st.cur >= 0 && budget != 0);
   emit.cond(em, st);
   st.cur -= em ? (int32_t)c.s : 0;
   if (NEED_AD) st.ad += em ? c.t : 0u;
-  budget -= em ? 1u : 0u;
+  if (!ALPHA) budget -= em ? 1u : 0u;
+  (void)has;
 }
 
 // NEXT-1 of SURVEY Sec. 8(f) (the paper's "dynamic behavior" future work, in its
 // cheapest closed form): for the COUNT consumer a node's valid a_{d-1} form the progression
 // a*, a*-s, ..., so its rows are counted in O(1) as floor(a*/s) + 1 (one magic division)
-// instead of one step per row.  Same units and slice boundaries as fast_step: a slice that
-// ends inside a node takes exactly its remaining budget of that node's rows.
+// instead of one step per row.  Node-unit slices only (a slice owns whole nodes), so the
+// slice boundaries are those of fast_step.
 template <int D, class KT>
 FS_HD void fast_step_closed(Lane<D> &st, const Consts &c, const KT &kt, uint32_t &budget, uint32_t &cnt) {
   constexpr int L = D - 2;
@@ -324,13 +329,11 @@ FS_HD void fast_step_closed(Lane<D> &st, const Consts &c, const KT &kt, uint32_t
     st.cur = fa ? nc : st.cur;
     budget -= fa ? 1u : 0u;
   }
-  const bool em = (has || fa) && st.cur >= 0 && budget != 0;
-  const uint32_t rem = divq((uint32_t)(st.cur < 0 ? 0 : st.cur), c.dvS) + 1u;
-  uint32_t take = rem < budget ? rem : budget;
-  take = em ? take : 0u;
-  cnt += take;
-  budget -= take;
+  const bool em = st.cur >= 0;  // node units: the node's rows all belong to this slice
+  const uint32_t rows = divq((uint32_t)(em ? st.cur : 0), c.dvS) + 1u;
+  cnt += em ? rows : 0u;
   st.cur = em ? -1 : st.cur;
+  (void)has;
 }
 
 template <int D>

@@ -95,8 +95,9 @@ int fs_validate_and_build(fs_plan *p, uint64_t n, const uint32_t *gens, int d, i
     c.g[i] = gens[i];
     c.dv[i] = fs_make_div(gens[i]);
   }
+  // node units for count / hist / any; row units for materialise (exact offsets)
   c.alpha = (consumer == FS_CONSUMER_ROWS) ? 0u : 1u;
-  c.beta = 1;
+  c.beta = (consumer == FS_CONSUMER_ROWS) ? 1u : 0u;
 
   if (d == 1) {
     // Z(n,(g)) = {(n/g)} iff g | n: one row or none; no tables, no nodes.
@@ -131,9 +132,10 @@ int fs_validate_and_build(fs_plan *p, uint64_t n, const uint32_t *gens, int d, i
       // d = 2: the root is the only node; no tables are needed
       Consts cr = c;
       cr.alpha = 0;
+      cr.beta = 1;
       const uint64_t nr = fs::node_units_host((uint32_t)n, cr, p->ktab.empty() ? nullptr : p->ktab.data());
       p->total_rows = nr;
-      p->total_units = c.alpha + nr;
+      p->total_units = c.alpha + c.beta * nr;
       p->nodes_per_level[0] = 1;
     } else {
       if ((uint64_t)L * N1 * 8ull > FS_MAX_TABLE_BYTES) return FS_ERANGE;
@@ -143,9 +145,10 @@ int fs_validate_and_build(fs_plan *p, uint64_t n, const uint32_t *gens, int d, i
       for (uint64_t r = 0; r <= n; ++r) {
         Consts cr = c;
         cr.alpha = 0;
+        cr.beta = 1;
         const uint64_t nr = fs::node_units_host((uint32_t)r, cr, p->ktab.empty() ? nullptr : p->ktab.data());
         rows[r] = nr;
-        arr[r] = c.alpha + nr;
+        arr[r] = c.alpha + c.beta * nr;
       }
       p->U.assign((size_t)L * N1, 0);
       for (int k = L - 1; k >= 0; --k) {
@@ -304,14 +307,14 @@ void host_model_d(const fs_plan *p, const KT &ktab, HostSink &sink, uint64_t *sl
     // the kernels' schedule: branch-free fast steps, slow_step() for lanes needing an ascend
     if (ALPHA && p->consumer == FS_CONSUMER_COUNT && p->ex.tail == FS_TAIL_CLOSED) {
       uint32_t cnt = 0;
-      while (budget > 0) {
+      while (!fs::needs_refill<D, ALPHA>(st, budget)) {
         fs::fast_step_closed<D>(st, c, ktab, budget, cnt);
         if (fs::needs_slow<D>(st, budget)) fs::slow_step<D, true, ALPHA>(st, c, ktab, budget);
       }
       sink.count += cnt;
       sink.slice_rows = cnt;
     } else {
-      while (budget > 0) {
+      while (!fs::needs_refill<D, ALPHA>(st, budget)) {
         fs::fast_step<D, true, ALPHA>(st, c, ktab, budget, emit);
         if (fs::needs_slow<D>(st, budget)) fs::slow_step<D, true, ALPHA>(st, c, ktab, budget);
       }
@@ -388,10 +391,7 @@ int unrank_host(const fs_plan *p, uint64_t unit, uint32_t *prefix_out, int64_t *
   uint64_t off = p->ktab.empty() ? fs::unrank<D, true>(st, p->c, fs::KTabArith{}, unit)
                                  : fs::unrank<D, true>(st, p->c, fs::KTabPtr{p->ktab.data()}, unit);
   for (int j = 0; j < D - 2; ++j) prefix_out[j] = st.a[j];
-  if (p->c.alpha)
-    *row_out = off == 0 ? -1 : (int64_t)(off - 1);
-  else
-    *row_out = (int64_t)off;
+  *row_out = p->c.alpha ? -1 : (int64_t)off;
   return FS_OK;
 }
 }  // namespace

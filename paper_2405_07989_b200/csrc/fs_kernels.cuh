@@ -326,7 +326,7 @@ __global__ void __launch_bounds__(kBlock) fs_enum_kernel(const KParams P) {
   e_cmp.wrows = 0;
 
   for (;;) {
-    const bool need = alive && budget == 0;
+    const bool need = alive && needs_refill<D, ALPHA>(st, budget);
     const unsigned needm = __ballot_sync(kFull, need);
     if (needm) {
       if (need) {
@@ -379,6 +379,7 @@ __global__ void __launch_bounds__(kBlock) fs_enum_kernel(const KParams P) {
       if (f) {
         alive = false;
         budget = 0;
+        st.cur = -1;
       }
     }
     if (__ballot_sync(kFull, alive) == 0) break;
@@ -421,6 +422,7 @@ __global__ void __launch_bounds__(kBlock) fs_enum_kernel(const KParams P) {
       }
       if (CONS == FS_CONSUMER_ANY && e_any.hit) {
         budget = 0;
+        st.cur = -1;
         alive = false;
       }
     }

@@ -143,7 +143,7 @@ def test_dp_totals_and_nodes(oracle_mod):
             # nodes at level k = #(a_1..a_k) with sum <= n = sum_{r<=n} |Z(r, g_1..g_k)|
             for k, nk in enumerate(info["nodes_per_level"]):
                 assert nk == sum(gf.count_table(n, g[:k])) if k else nk == 1
-            assert info["total_units"] == info["nodes_per_level"][d - 2] + info["total_rows"]
+            assert info["total_units"] == info["nodes_per_level"][d - 2]  # node units
 
 
 def test_full_size_plans():
