@@ -271,36 +271,35 @@ FS_HD void slow_step(Lane<D> &st, const Consts &c, const KT &kt, uint32_t &budge
 template <int D, bool NEED_AD, int ALPHA, class KT, class Emit>
 FS_HD void fast_step(Lane<D> &st, const Consts &c, const KT &kt, uint32_t &budget, Emit &emit) {
   constexpr int L = D - 2;
-  const bool act = budget != 0;
-  const bool has = st.cur >= 0;
-  bool fa = false;
   if constexpr (L >= 1) {
     const uint32_t al = st.a[L - 1];
-    fa = act && !has && al != 0;
-    uint32_t r2 = st.rho + c.delta;
-    const uint32_t cy = r2 >= c.gA ? 1u : 0u;
-    r2 = cy ? r2 - c.gA : r2;
-    const uint32_t A2 = st.A + c.q + cy;
-    st.rho = fa ? r2 : st.rho;
-    st.A = fa ? A2 : st.A;
-    st.a[L - 1] = al - (fa ? 1u : 0u);
-    st.lsum -= fa ? 1u : 0u;
-    const uint32_t k = kt(st.rho, c);
-    const int32_t nc = (int32_t)st.A - (int32_t)k;
-    st.cur = fa ? nc : st.cur;
-    if (NEED_AD) {
-      const uint32_t ad2 = divq(st.rho + k * c.gA, c.dvB);
-      st.ad = fa ? ad2 : st.ad;
+    const bool fa = budget != 0 && st.cur < 0 && al != 0;
+    if (fa) {  // advance: a_L -= 1, R_L += g_L (predicated, no branch)
+      st.a[L - 1] = al - 1u;
+      st.R[L - 1] += c.g[L - 1];
+      if (ALPHA) budget -= 1u;
+      if (NEED_AD) st.lsum -= 1u;
     }
-    if (ALPHA) budget -= fa ? 1u : 0u;
+    // entry, computed for every lane (idle lanes hold a valid residual): A = R_L / g_{d-1}
+    // by magic division, rho = R_L mod g_{d-1}, a* = A - k0(rho)
+    const uint32_t R = st.R[L - 1];
+    const uint32_t A = divq(R, c.dvA);
+    const uint32_t rho = R - A * c.gA;
+    const uint32_t k = kt(rho, c);
+    const int32_t nc = (int32_t)A - (int32_t)k;
+    if (fa) {
+      st.cur = nc;
+      if (NEED_AD) st.ad = divq(rho + k * c.gA, c.dvB);
+    }
   }
   // node units: every row of an entered node belongs to the slice; row units: budget-limited
   const bool em = ALPHA ? (st.cur >= 0) : (st.cur >= 0 && budget != 0);
   emit.cond(em, st);
-  st.cur -= em ? (int32_t)c.s : 0;
-  if (NEED_AD) st.ad += em ? c.t : 0u;
-  if (!ALPHA) budget -= em ? 1u : 0u;
-  (void)has;
+  if (em) {
+    st.cur -= (int32_t)c.s;
+    if (NEED_AD) st.ad += c.t;
+    if (!ALPHA) budget -= 1u;
+  }
 }
 
 // NEXT-1 of SURVEY Sec. 8(f) (the paper's "dynamic behavior" future work, in its
@@ -311,29 +310,26 @@ FS_HD void fast_step(Lane<D> &st, const Consts &c, const KT &kt, uint32_t &budge
 template <int D, class KT>
 FS_HD void fast_step_closed(Lane<D> &st, const Consts &c, const KT &kt, uint32_t &budget, uint32_t &cnt) {
   constexpr int L = D - 2;
-  const bool act = budget != 0;
-  const bool has = st.cur >= 0;
-  bool fa = false;
   if constexpr (L >= 1) {
     const uint32_t al = st.a[L - 1];
-    fa = act && !has && al != 0;
-    uint32_t r2 = st.rho + c.delta;
-    const uint32_t cy = r2 >= c.gA ? 1u : 0u;
-    r2 = cy ? r2 - c.gA : r2;
-    const uint32_t A2 = st.A + c.q + cy;
-    st.rho = fa ? r2 : st.rho;
-    st.A = fa ? A2 : st.A;
-    st.a[L - 1] = al - (fa ? 1u : 0u);
-    const uint32_t k = kt(st.rho, c);
-    const int32_t nc = (int32_t)st.A - (int32_t)k;
-    st.cur = fa ? nc : st.cur;
-    budget -= fa ? 1u : 0u;
+    const bool fa = budget != 0 && st.cur < 0 && al != 0;
+    if (fa) {
+      st.a[L - 1] = al - 1u;
+      st.R[L - 1] += c.g[L - 1];
+      budget -= 1u;
+    }
+    const uint32_t R = st.R[L - 1];
+    const uint32_t A = divq(R, c.dvA);
+    const uint32_t k = kt(R - A * c.gA, c);
+    const int32_t nc = (int32_t)A - (int32_t)k;
+    if (fa) st.cur = nc;
   }
   const bool em = st.cur >= 0;  // node units: the node's rows all belong to this slice
   const uint32_t rows = divq((uint32_t)(em ? st.cur : 0), c.dvS) + 1u;
-  cnt += em ? rows : 0u;
-  st.cur = em ? -1 : st.cur;
-  (void)has;
+  if (em) {
+    cnt += rows;
+    st.cur = -1;
+  }
 }
 
 template <int D>

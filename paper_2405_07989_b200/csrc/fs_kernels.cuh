@@ -33,7 +33,7 @@ constexpr unsigned kFull = 0xffffffffu;
 
 template <int CONS>
 struct Inner {
-  static constexpr int value = (CONS == FS_CONSUMER_ROWS) ? 8 : 64;
+  static constexpr int value = 64;
 };
 
 // ---------------------------------------------------------------- consumers
@@ -117,9 +117,9 @@ struct EmitRows {
   uint64_t pend_goff;
   __device__ __forceinline__ void put(uint32_t p, int i, uint32_t v) {
     if (B == 16)
-      *reinterpret_cast<uint16_t *>(ring + ((p + 2 * i + rot) & 255u)) = (uint16_t)v;
+      *reinterpret_cast<uint16_t *>(ring + ((p + 2 * i + rot) & (kStageBytes - 1))) = (uint16_t)v;
     else
-      *reinterpret_cast<uint32_t *>(ring + ((p + 4 * i + rot) & 255u)) = v;
+      *reinterpret_cast<uint32_t *>(ring + ((p + 4 * i + rot) & (kStageBytes - 1))) = v;
   }
   __device__ __forceinline__ void cond(bool em, const Lane<D> &st) {
     if (!em) return;
@@ -130,10 +130,10 @@ struct EmitRows {
     put(p, D - 1, st.ad);
     const uint32_t np = p + kRB;
     wpos = np;
-    if ((p >> 7) != (np >> 7)) {
+    if ((p / kHalf) != (np / kHalf)) {
       pend = true;
-      pend_soff = p & 128u;
-      pend_goff = slice_goff + (uint64_t)(p & ~127u);
+      pend_soff = p & kHalf;
+      pend_goff = slice_goff + (uint64_t)(p & ~(kHalf - 1));
     }
   }
 };
@@ -208,17 +208,18 @@ struct EmitCompact {
   }
 };
 
-// Warp-cooperative copy of every lane's pending ring segment: 4 segments per round, 8 lanes
-// x 16 B each -> fully coalesced 128 B stores.  len is a multiple of 16.
+// Warp-cooperative copy of every lane's pending ring segment: 32/(kHalf/16) segments per
+// round, kHalf/16 lanes x 16 B each -> fully coalesced 16 B stores.  len is a multiple of 16.
 __device__ __forceinline__ void warp_flush(bool &pend, uint32_t soff, uint64_t goff, uint32_t len,
                                            const unsigned char *warp_stage, unsigned char *out) {
   unsigned pm = __ballot_sync(kFull, pend);
   if (!pm) return;
-  const int lane = threadIdx.x & 31, sub = lane >> 3, j = lane & 7;
+  constexpr int kLanesPerSeg = kHalf / 16, kSegs = 32 / kLanesPerSeg;
+  const int lane = threadIdx.x & 31, sub = lane / kLanesPerSeg, j = lane % kLanesPerSeg;
   while (pm) {
     unsigned m = pm;
 #pragma unroll
-    for (int x = 0; x < 3; ++x)
+    for (int x = 0; x < kSegs - 1; ++x)
       if (x < sub) m &= m - 1;
     const int src = m ? (__ffs(m) - 1) : -1;
     const int sl = src < 0 ? 0 : src;
@@ -229,14 +230,15 @@ __device__ __forceinline__ void warp_flush(bool &pend, uint32_t soff, uint64_t g
       const unsigned char *r = warp_stage + src * kStageBytes;
       const uint32_t base = s_soff + (uint32_t)j * 16u + 4u * (uint32_t)src;
       uint4 v;
-      v.x = *reinterpret_cast<const uint32_t *>(r + (base & 255u));
-      v.y = *reinterpret_cast<const uint32_t *>(r + ((base + 4u) & 255u));
-      v.z = *reinterpret_cast<const uint32_t *>(r + ((base + 8u) & 255u));
-      v.w = *reinterpret_cast<const uint32_t *>(r + ((base + 12u) & 255u));
+      constexpr uint32_t M = kStageBytes - 1;
+      v.x = *reinterpret_cast<const uint32_t *>(r + (base & M));
+      v.y = *reinterpret_cast<const uint32_t *>(r + ((base + 4u) & M));
+      v.z = *reinterpret_cast<const uint32_t *>(r + ((base + 8u) & M));
+      v.w = *reinterpret_cast<const uint32_t *>(r + ((base + 12u) & M));
       __stcs(reinterpret_cast<uint4 *>(out + s_goff + (uint64_t)j * 16u), v);
     }
 #pragma unroll
-    for (int x = 0; x < 4; ++x) pm &= pm ? pm - 1 : 0u;
+    for (int x = 0; x < kSegs; ++x) pm &= pm ? pm - 1 : 0u;
   }
   pend = false;
 }
@@ -247,14 +249,14 @@ template <int D, int B>
 __device__ __forceinline__ void rows_slice_done(const KParams &P, EmitRows<D, B> &er, bool &fin, uint32_t &fin_soff,
                                                 uint64_t &fin_goff, uint32_t &fin_len) {
   const uint32_t w = er.wpos;
-  const uint32_t hstart = w & ~127u;
+  const uint32_t hstart = w & ~(kHalf - 1);
   const uint32_t plen = w - hstart;
   const uint32_t alen = plen & ~15u;
   for (uint32_t b = alen; b < plen; ++b)
-    P.rows_out[er.slice_goff + hstart + b] = er.ring[(hstart + b + er.rot) & 255u];
+    P.rows_out[er.slice_goff + hstart + b] = er.ring[(hstart + b + er.rot) & (kStageBytes - 1)];
   if (alen) {
     fin = true;
-    fin_soff = hstart & 128u;
+    fin_soff = hstart & kHalf;
     fin_goff = er.slice_goff + hstart;
     fin_len = alen;
   }
@@ -269,7 +271,10 @@ __global__ void __launch_bounds__(kBlock) fs_enum_kernel(const KParams P) {
   constexpr bool NEED_AD = CONS != FS_CONSUMER_COUNT && CONS != kConsCountClosed;
   constexpr int ALPHA = (CONS == FS_CONSUMER_ROWS || CONS == kConsRowsAny) ? 0 : 1;
   constexpr int INNER = Inner<CONS>::value;
-  constexpr int UNROLL = CONS == FS_CONSUMER_ROWS ? 1 : 4;
+  // ROWS: a lane completes at most one ring half in kHalf / row_bytes steps, so the warp
+  // flushes pending halves once per that many steps.
+  constexpr int kRowsPerHalf = (int)(kHalf / (D * (B / 8))) > 0 ? (int)(kHalf / (D * (B / 8))) : 1;
+  constexpr int UNROLL = CONS == FS_CONSUMER_ROWS ? kRowsPerHalf : 4;
   extern __shared__ __align__(16) unsigned char smem[];
   __shared__ unsigned int hist_guard;
   const Consts &c = P.c;
@@ -405,9 +410,11 @@ __global__ void __launch_bounds__(kBlock) fs_enum_kernel(const KParams P) {
           const bool was = budget != 0;
           fast_step<D, NEED_AD, ALPHA>(st, c, kt, budget, e_rows);
           if (was && budget == 0) rows_slice_done(P, e_rows, fin, fin_soff, fin_goff, fin_len);
-          warp_flush(e_rows.pend, e_rows.pend_soff, e_rows.pend_goff, 128u, warp_stage, P.rows_out);
-          warp_flush(fin, fin_soff, fin_goff, fin_len, warp_stage, P.rows_out);
         }
+      }
+      if (CONS == FS_CONSUMER_ROWS) {
+        warp_flush(e_rows.pend, e_rows.pend_soff, e_rows.pend_goff, kHalf, warp_stage, P.rows_out);
+        warp_flush(fin, fin_soff, fin_goff, fin_len, warp_stage, P.rows_out);
       }
       const bool slow = needs_slow<D>(st, budget);
       if (__any_sync(kFull, slow)) {
@@ -416,7 +423,7 @@ __global__ void __launch_bounds__(kBlock) fs_enum_kernel(const KParams P) {
           if (CONS == FS_CONSUMER_ROWS && budget == 0) rows_slice_done(P, e_rows, fin, fin_soff, fin_goff, fin_len);
         }
         if (CONS == FS_CONSUMER_ROWS) {
-          warp_flush(e_rows.pend, e_rows.pend_soff, e_rows.pend_goff, 128u, warp_stage, P.rows_out);
+          warp_flush(e_rows.pend, e_rows.pend_soff, e_rows.pend_goff, kHalf, warp_stage, P.rows_out);
           warp_flush(fin, fin_soff, fin_goff, fin_len, warp_stage, P.rows_out);
         }
       }

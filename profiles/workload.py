@@ -1,0 +1,52 @@
+"""Run one hot-path kernel a few times for ncu captures (never a bench number).
+
+  python profiles/workload.py <name> [reps]
+  names: c3count c3closed c4hist c5count c5any_none c2xl_m1 c2xl_m2
+"""
+import os
+import sys
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+sys.path.insert(0, ROOT)
+
+import torch  # noqa: E402
+
+from paper_2405_07989_b200 import _lib as L  # noqa: E402
+from paper_2405_07989_b200 import api  # noqa: E402
+from paper_2405_07989_b200 import workloads as W  # noqa: E402
+
+
+def main():
+    name = sys.argv[1]
+    reps = int(sys.argv[2]) if len(sys.argv) > 2 else 2
+    if name in ("c3count", "c3closed", "c5count"):
+        inst = W.C5 if name == "c5count" else W.C3
+        p = api.Plan(inst.n, inst.gens, L.FS_CONSUMER_COUNT, tail=1 if name == "c3closed" else 0)
+        out = torch.zeros(1, dtype=torch.int64, device="cuda")
+        fn = lambda: p.count_async(out)
+    elif name == "c4hist":
+        inst = W.C4
+        p = api.Plan(inst.n, inst.gens, L.FS_CONSUMER_HIST)
+        out = torch.zeros(api.hist_len(inst.n, inst.gens), dtype=torch.int64, device="cuda")
+        fn = lambda: p.hist_async(out)
+    elif name == "c5any_none":
+        inst = W.C5
+        p = api.Plan(inst.n, inst.gens, L.FS_CONSUMER_ANY)
+        f = torch.zeros(1, dtype=torch.int32, device="cuda")
+        fn = lambda: p.any_async(L.FS_PRED_LEN_LE, 19, f)
+    elif name in ("c2xl_m1", "c2xl_m2"):
+        inst = W.C2XL
+        p = api.Plan(inst.n, inst.gens, L.FS_CONSUMER_ROWS, order=0 if name == "c2xl_m1" else 1)
+        rows = p.info["total_rows"]
+        out = torch.empty((rows, inst.d), dtype=torch.uint16, device="cuda")
+        fn = lambda: p.enumerate_async(16, out, rows)
+    else:
+        raise SystemExit("unknown workload " + name)
+    for _ in range(reps):
+        fn()
+    torch.cuda.synchronize()
+    print(name, "ok")
+
+
+if __name__ == "__main__":
+    main()
