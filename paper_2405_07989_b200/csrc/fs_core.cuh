@@ -96,8 +96,8 @@ struct Lane {
   uint32_t R[LA];  // R_1..R_L
   uint32_t A, rho; // floor(R_L / g_{d-1}), R_L mod g_{d-1}
   int32_t cur;     // current row's a_{d-1} (< 0: none left in this node)
-  uint32_t ad;     // current row's a_d
-  uint32_t lsum;   // a_1 + .. + a_L
+  uint32_t ad;     // unused placeholder (a_d is solved on demand by row_ad())
+  uint32_t lsum;   // a_1 + .. + a_L (tracked when the consumer needs lengths/coordinates)
 };
 
 // k0 lookups: the table of k0(rho) for rho in [0, g_{d-1}) (host vector, or a shared-memory
@@ -115,7 +115,20 @@ template <int D, bool NEED_AD, class KT>
 FS_HD void entry(Lane<D> &st, const Consts &c, const KT &kt) {
   const uint32_t k = kt(st.rho, c);
   st.cur = (int32_t)st.A - (int32_t)k;  // A <= n < 2^31 - 1, so kNone gives cur < 0
-  if (NEED_AD) st.ad = divq(st.rho + k * c.gA, c.dvB);  // only meaningful if cur >= 0
+  (void)NEED_AD;
+}
+
+// The last coordinate of the current row, solved by division (decrementAndSolve):
+// a_d = (R_L - a_{d-1} g_{d-1}) / g_d, exact for a valid row.
+template <int D>
+FS_HD uint32_t row_ad(const Lane<D> &st, const Consts &c) {
+  constexpr int L = D - 2;
+  uint32_t R;
+  if constexpr (L >= 1)
+    R = st.R[L - 1];
+  else
+    R = c.n;
+  return divq(R - (uint32_t)st.cur * c.gA, c.dvB);
 }
 
 // Deeper ascend of Alg. 3.1 steps 2-11: rightmost nonzero index i < L, a_i -= 1,
@@ -235,7 +248,6 @@ template <int D, bool NEED_AD>
 FS_HD uint32_t position_in_node(Lane<D> &st, const Consts &c, uint64_t off) {
   if (c.alpha) return 1;  // off == 0: node units never split a node
   st.cur -= (int32_t)((uint32_t)off * c.s);
-  if (NEED_AD) st.ad += (uint32_t)off * c.t;
   return 0;
 }
 
@@ -287,17 +299,13 @@ FS_HD void fast_step(Lane<D> &st, const Consts &c, const KT &kt, uint32_t &budge
     const uint32_t rho = R - A * c.gA;
     const uint32_t k = kt(rho, c);
     const int32_t nc = (int32_t)A - (int32_t)k;
-    if (fa) {
-      st.cur = nc;
-      if (NEED_AD) st.ad = divq(rho + k * c.gA, c.dvB);
-    }
+    if (fa) st.cur = nc;
   }
   // node units: every row of an entered node belongs to the slice; row units: budget-limited
   const bool em = ALPHA ? (st.cur >= 0) : (st.cur >= 0 && budget != 0);
-  emit.cond(em, st);
+  emit.cond(em, st, c);
   if (em) {
     st.cur -= (int32_t)c.s;
-    if (NEED_AD) st.ad += c.t;
     if (!ALPHA) budget -= 1u;
   }
 }

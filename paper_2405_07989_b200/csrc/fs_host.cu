@@ -280,13 +280,13 @@ struct HostSink {
 template <int D>
 struct HostEmit {
   HostSink *sink;
-  FS_HD void cond(bool em, const fs::Lane<D> &st) {
+  FS_HD void cond(bool em, const fs::Lane<D> &st, const fs::Consts &c) {
 #ifndef __CUDA_ARCH__
     if (!em) return;
     uint32_t v[FS_MAX_D];
     for (int j = 0; j < D - 2; ++j) v[j] = st.a[j];
     v[D - 2] = (uint32_t)st.cur;
-    v[D - 1] = st.ad;
+    v[D - 1] = fs::row_ad<D>(st, c);
     sink->put(v);
 #endif
   }

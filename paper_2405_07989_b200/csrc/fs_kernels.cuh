@@ -40,7 +40,7 @@ struct Inner {
 template <int D>
 struct EmitCount {
   uint32_t n;
-  __device__ __forceinline__ void cond(bool em, const Lane<D> &) { n += em ? 1u : 0u; }
+  __device__ __forceinline__ void cond(bool em, const Lane<D> &, const Consts &) { n += em ? 1u : 0u; }
 };
 
 template <int D>
@@ -49,9 +49,9 @@ struct EmitHist {
   unsigned long long *gbins;
   uint32_t smem;
   uint32_t n;
-  __device__ __forceinline__ void cond(bool em, const Lane<D> &st) {
+  __device__ __forceinline__ void cond(bool em, const Lane<D> &st, const Consts &c) {
     if (!em) return;
-    const uint32_t l = st.lsum + (uint32_t)st.cur + st.ad;  // length = sum_i a_i
+    const uint32_t l = st.lsum + (uint32_t)st.cur + row_ad<D>(st, c);  // length = sum_i a_i
     if (smem)
       atomicAdd(&bins[l], 1u);
     else
@@ -61,8 +61,8 @@ struct EmitHist {
 };
 
 template <int D>
-__device__ __forceinline__ uint32_t coord(const Lane<D> &st, uint32_t i) {
-  uint32_t v = st.ad;
+__device__ __forceinline__ uint32_t coord(const Lane<D> &st, uint32_t i, uint32_t ad) {
+  uint32_t v = ad;
   if (i == D - 2) v = (uint32_t)st.cur;
 #pragma unroll
   for (int j = 0; j < D - 2; ++j)
@@ -77,9 +77,10 @@ struct EmitAny {
   int *found;
   uint32_t *wit;
   bool hit;
-  __device__ __forceinline__ void cond(bool em, const Lane<D> &st) {
+  __device__ __forceinline__ void cond(bool em, const Lane<D> &st, const Consts &c) {
     if (!em) return;
-    const uint64_t len = (uint64_t)st.lsum + (uint32_t)st.cur + st.ad;
+    const uint32_t ad = row_ad<D>(st, c);
+    const uint64_t len = (uint64_t)st.lsum + (uint32_t)st.cur + ad;
     bool ok;
     switch (pred) {
       case FS_PRED_LEN_LE: ok = len <= arg; break;
@@ -87,7 +88,7 @@ struct EmitAny {
       case FS_PRED_LEN_EQ: ok = len == arg; break;
       default: {
         const uint32_t i = (uint32_t)(arg >> 32);
-        ok = i < (uint32_t)D && coord<D>(st, i) >= (uint32_t)(arg & 0xffffffffu);
+        ok = i < (uint32_t)D && coord<D>(st, i, ad) >= (uint32_t)(arg & 0xffffffffu);
       }
     }
     if (ok && !hit) {
@@ -96,7 +97,7 @@ struct EmitAny {
 #pragma unroll
         for (int j = 0; j < D - 2; ++j) wit[j] = st.a[j];
         wit[D - 2] = (uint32_t)st.cur;
-        wit[D - 1] = st.ad;
+        wit[D - 1] = ad;
       }
     }
   }
@@ -121,13 +122,13 @@ struct EmitRows {
     else
       *reinterpret_cast<uint32_t *>(ring + ((p + 4 * i + rot) & (kStageBytes - 1))) = v;
   }
-  __device__ __forceinline__ void cond(bool em, const Lane<D> &st) {
+  __device__ __forceinline__ void cond(bool em, const Lane<D> &st, const Consts &c) {
     if (!em) return;
     const uint32_t p = wpos;
 #pragma unroll
     for (int j = 0; j < D - 2; ++j) put(p, j, st.a[j]);
     put(p, D - 2, (uint32_t)st.cur);
-    put(p, D - 1, st.ad);
+    put(p, D - 1, row_ad<D>(st, c));
     const uint32_t np = p + kRB;
     wpos = np;
     if ((p / kHalf) != (np / kHalf)) {
@@ -160,14 +161,14 @@ struct EmitCompact {
     else
       *reinterpret_cast<uint32_t *>(q + 4 * i) = v;
   }
-  __device__ __forceinline__ void cond(bool em, const Lane<D> &st) {
+  __device__ __forceinline__ void cond(bool em, const Lane<D> &st, const Consts &c) {
     const unsigned m = __ballot_sync(kFull, em);
     if (em) {
       unsigned char *q = buf + (wrows + (uint32_t)__popc(m & lanemask_lt())) * kRB;
 #pragma unroll
       for (int j = 0; j < D - 2; ++j) put(q, j, st.a[j]);
       put(q, D - 2, (uint32_t)st.cur);
-      put(q, D - 1, st.ad);
+      put(q, D - 1, row_ad<D>(st, c));
     }
     wrows += (uint32_t)__popc(m);
   }
