@@ -238,10 +238,17 @@ def main():
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
+    # one process per GPU; FS_DIST_BACKEND=gloo lets the multi-rank path run on a 1-GPU box
+    # (ranks then share devices round-robin) for testing -- numbers from it are not scaling data
+    backend = os.environ.get("FS_DIST_BACKEND", "nccl")
+    local = local % max(1, torch.cuda.device_count())
     torch.cuda.set_device(local)
     dev = torch.device("cuda", local)
     if world > 1:
-        dist.init_process_group("nccl", device_id=dev)
+        if backend == "nccl":
+            dist.init_process_group("nccl", device_id=dev)
+        else:
+            dist.init_process_group(backend)
     stream = torch.cuda.current_stream()
     peaks, peaks_kind = load_peaks()
 
@@ -327,6 +334,7 @@ def main():
         "config": {"workload": "%s: Z(%d, %s) count, |Z| = %d" % (inst.name, inst.n, list(inst.gens), total),
                    "instance": inst.name, "n": inst.n, "gens": list(inst.gens), "consumer": "count",
                    "parallelism": "lex-slice dp%d" % world, "l2": "flushed between steps (256 MB write)",
+                   "dist_backend": backend if world > 1 else None,
                    "slice_units": info["slice_units"], "num_slices": info["num_slices"],
                    "grid": plan.info["grid"], "block": info["block"]},
         "roofline": {"bound": "alu", "achieved": achieved, "peak": peak_tops, "unit": "Tops/s (int32 lane-ops)",
