@@ -67,10 +67,15 @@ struct Consts {
   Div dvA, dvB, dvH, dvS;
   uint32_t delta, q;     // g_L mod gA, g_L / gA (L >= 1)
   uint32_t alpha, beta;  // units per node entry / per row
-  uint32_t ktab_len;     // 0: k0 by arithmetic; else table of gA entries
-  uint32_t _pad;
+  uint32_t ktab_len;     // 0: k0 by arithmetic; else words of the node tables (below)
+  uint32_t adv_off;      // word offset of the advance table inside ktab (8 B aligned)
   const uint64_t *U;     // DP tables, L rows of (n+1) entries
-  const uint32_t *ktab;  // k0 table (device or host)
+  // node tables (device or host), for rho in [0, g_{d-1}):
+  //   ktab[rho]                     = k0(rho)
+  //   ktab[adv_off + 2 rho]         = next(rho) | carry(rho) << 31, next = (rho + delta) mod g_{d-1}
+  //   ktab[adv_off + 2 rho + 1]     = k0(next(rho))
+  // i.e. one 8 B load performs a node advance's residue update and the new node's entry.
+  const uint32_t *ktab;
 };
 
 #ifdef __CUDA_ARCH__
@@ -100,14 +105,26 @@ struct Lane {
   uint32_t lsum;   // a_1 + .. + a_L (tracked when the consumer needs lengths/coordinates)
 };
 
-// k0 lookups: the table of k0(rho) for rho in [0, g_{d-1}) (host vector, or a shared-memory
-// copy on the device), or the arithmetic form when g_{d-1} is too large for a table.
+// Node-table lookups: k0(rho), and step(rho) = the advance transition (next residue, carry,
+// k0 of the next residue) -- from the tables (host vector, or a shared-memory copy on the
+// device), or by arithmetic when g_{d-1} is too large for a table.
+struct Adv {
+  uint32_t x, y;  // x = next | carry << 31, y = k0(next)
+};
 struct KTabPtr {
   const uint32_t *p;
+  uint32_t adv_off;
   FS_HD uint32_t operator()(uint32_t rho, const Consts &) const { return p[rho]; }
+  FS_HD Adv step(uint32_t rho, const Consts &) const { return Adv{p[adv_off + 2 * rho], p[adv_off + 2 * rho + 1]}; }
 };
 struct KTabArith {
   FS_HD uint32_t operator()(uint32_t rho, const Consts &c) const { return k0_arith(rho, c); }
+  FS_HD Adv step(uint32_t rho, const Consts &c) const {
+    uint32_t r2 = rho + c.delta;
+    const uint32_t cy = r2 >= c.gA ? 1u : 0u;
+    r2 -= cy ? c.gA : 0u;
+    return Adv{r2 | (cy << 31), k0_arith(r2, c)};
+  }
 };
 
 // Node entry: solve the first valid a_{d-1} of the node (modulo skip at run entry).
@@ -120,15 +137,10 @@ FS_HD void entry(Lane<D> &st, const Consts &c, const KT &kt) {
 
 // The last coordinate of the current row, solved by division (decrementAndSolve):
 // a_d = (R_L - a_{d-1} g_{d-1}) / g_d, exact for a valid row.
+// (R_L = A g_{d-1} + rho, so R_L - a_{d-1} g_{d-1} = (A - a_{d-1}) g_{d-1} + rho.)
 template <int D>
 FS_HD uint32_t row_ad(const Lane<D> &st, const Consts &c) {
-  constexpr int L = D - 2;
-  uint32_t R;
-  if constexpr (L >= 1)
-    R = st.R[L - 1];
-  else
-    R = c.n;
-  return divq(R - (uint32_t)st.cur * c.gA, c.dvB);
+  return divq((st.A - (uint32_t)st.cur) * c.gA + st.rho, c.dvB);
 }
 
 // Deeper ascend of Alg. 3.1 steps 2-11: rightmost nonzero index i < L, a_i -= 1,
@@ -286,20 +298,17 @@ FS_HD void fast_step(Lane<D> &st, const Consts &c, const KT &kt, uint32_t &budge
   if constexpr (L >= 1) {
     const uint32_t al = st.a[L - 1];
     const bool fa = budget != 0 && st.cur < 0 && al != 0;
-    if (fa) {  // advance: a_L -= 1, R_L += g_L (predicated, no branch)
+    // one table load: next residue of R_L + g_L mod g_{d-1}, the carry into floor(R_L/g_{d-1}),
+    // and k0 of the next residue (all lanes load; only advancing lanes commit)
+    const Adv w = kt.step(st.rho, c);
+    if (fa) {  // advance (a_L -= 1, R_L += g_L) and entry of the new node, predicated
       st.a[L - 1] = al - 1u;
-      st.R[L - 1] += c.g[L - 1];
+      st.rho = w.x & 0x7fffffffu;
+      st.A += c.q + (w.x >> 31);
+      st.cur = (int32_t)st.A - (int32_t)w.y;
       if (ALPHA) budget -= 1u;
       if (NEED_AD) st.lsum -= 1u;
     }
-    // entry, computed for every lane (idle lanes hold a valid residual): A = R_L / g_{d-1}
-    // by magic division, rho = R_L mod g_{d-1}, a* = A - k0(rho)
-    const uint32_t R = st.R[L - 1];
-    const uint32_t A = divq(R, c.dvA);
-    const uint32_t rho = R - A * c.gA;
-    const uint32_t k = kt(rho, c);
-    const int32_t nc = (int32_t)A - (int32_t)k;
-    if (fa) st.cur = nc;
   }
   // node units: every row of an entered node belongs to the slice; row units: budget-limited
   const bool em = ALPHA ? (st.cur >= 0) : (st.cur >= 0 && budget != 0);
@@ -321,16 +330,14 @@ FS_HD void fast_step_closed(Lane<D> &st, const Consts &c, const KT &kt, uint32_t
   if constexpr (L >= 1) {
     const uint32_t al = st.a[L - 1];
     const bool fa = budget != 0 && st.cur < 0 && al != 0;
+    const Adv w = kt.step(st.rho, c);
     if (fa) {
       st.a[L - 1] = al - 1u;
-      st.R[L - 1] += c.g[L - 1];
+      st.rho = w.x & 0x7fffffffu;
+      st.A += c.q + (w.x >> 31);
+      st.cur = (int32_t)st.A - (int32_t)w.y;
       budget -= 1u;
     }
-    const uint32_t R = st.R[L - 1];
-    const uint32_t A = divq(R, c.dvA);
-    const uint32_t k = kt(R - A * c.gA, c);
-    const int32_t nc = (int32_t)A - (int32_t)k;
-    if (fa) st.cur = nc;
   }
   const bool em = st.cur >= 0;  // node units: the node's rows all belong to this slice
   const uint32_t rows = divq((uint32_t)(em ? st.cur : 0), c.dvS) + 1u;

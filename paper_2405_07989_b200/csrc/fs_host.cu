@@ -120,11 +120,21 @@ int fs_validate_and_build(fs_plan *p, uint64_t n, const uint32_t *gens, int d, i
       c.delta = gens[L - 1] % c.gA;
       c.q = gens[L - 1] / c.gA;
     }
-    if (c.gA <= fs::kKtabMax) {
-      p->ktab.resize(c.gA);
-      c.ktab_len = 0;  // compute entries with the arithmetic form
-      for (uint32_t rho = 0; rho < c.gA; ++rho) p->ktab[rho] = fs::k0_arith(rho, c);
-      c.ktab_len = c.gA;
+    if (c.gA <= fs::kKtabMax && (c.s < (1u << 31))) {
+      // node tables: k0(rho), then the advance transitions (8 B aligned), computed with the
+      // same arithmetic the table-less kernels use
+      const uint32_t adv_off = (c.gA + 1u) & ~1u;
+      p->ktab.assign(adv_off + 2u * c.gA, 0u);
+      c.ktab_len = 0;
+      const fs::KTabArith ar{};
+      for (uint32_t rho = 0; rho < c.gA; ++rho) {
+        p->ktab[rho] = fs::k0_arith(rho, c);
+        const fs::Adv w = ar.step(rho, c);
+        p->ktab[adv_off + 2 * rho] = w.x;
+        p->ktab[adv_off + 2 * rho + 1] = w.y;
+      }
+      c.ktab_len = (uint32_t)p->ktab.size();
+      c.adv_off = adv_off;
       c.ktab = p->ktab.data();
     }
     const uint64_t N1 = n + 1;
@@ -337,7 +347,7 @@ void host_model_kt(const fs_plan *p, const KT &kt, HostSink &sink, uint64_t *sc,
 template <int D>
 void host_model_alpha(const fs_plan *p, HostSink &sink, uint64_t *sc, uint32_t *sf) {
   if (!p->ktab.empty())
-    host_model_kt<D>(p, fs::KTabPtr{p->ktab.data()}, sink, sc, sf);
+    host_model_kt<D>(p, fs::KTabPtr{p->ktab.data(), p->c.adv_off}, sink, sc, sf);
   else
     host_model_kt<D>(p, fs::KTabArith{}, sink, sc, sf);
 }
@@ -389,7 +399,7 @@ template <int D>
 int unrank_host(const fs_plan *p, uint64_t unit, uint32_t *prefix_out, int64_t *row_out) {
   fs::Lane<D> st;
   uint64_t off = p->ktab.empty() ? fs::unrank<D, true>(st, p->c, fs::KTabArith{}, unit)
-                                 : fs::unrank<D, true>(st, p->c, fs::KTabPtr{p->ktab.data()}, unit);
+                                 : fs::unrank<D, true>(st, p->c, fs::KTabPtr{p->ktab.data(), p->c.adv_off}, unit);
   for (int j = 0; j < D - 2; ++j) prefix_out[j] = st.a[j];
   *row_out = p->c.alpha ? -1 : (int64_t)off;
   return FS_OK;

@@ -15,7 +15,7 @@ namespace fs {
 constexpr int kBlock = 256;          // threads per persistent CTA
 constexpr int kStageBytes = 128;     // per-lane staging ring for materialise (2 halves)
 constexpr uint32_t kHalf = kStageBytes / 2;  // flush granule: one completed half (64 B)
-constexpr uint32_t kKtabMax = 8192;  // k0 table in shared memory if g_{d-1} <= this
+constexpr uint32_t kKtabMax = 2048;  // node tables in shared memory if g_{d-1} <= this (<= 24 KB)
 constexpr uint32_t kHistSmemMax = 24576;  // u32 histogram bins kept in shared memory
 constexpr int kConsRowsAny = 4;           // internal consumer: materialise, order = any (M2)
 constexpr uint32_t kWarpBuf = 4096;       // M2 per-warp compaction buffer (bytes)

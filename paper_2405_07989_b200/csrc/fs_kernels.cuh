@@ -19,13 +19,19 @@
 
 namespace fs {
 
-// k0 table in shared memory (copied once per CTA)
+// node tables in shared memory (copied once per CTA)
 struct KTabSmem {
-  uint32_t base;  // shared-window address of the table
+  uint32_t base;  // shared-window address of the k0 table
+  uint32_t adv;   // shared-window address of the advance table (8 B aligned)
   __device__ __forceinline__ uint32_t operator()(uint32_t rho, const Consts &) const {
     uint32_t v;
     asm("ld.shared.u32 %0, [%1];" : "=r"(v) : "r"(base + rho * 4u));
     return v;
+  }
+  __device__ __forceinline__ Adv step(uint32_t rho, const Consts &) const {
+    Adv w;
+    asm("ld.shared.v2.u32 {%0, %1}, [%2];" : "=r"(w.x), "=r"(w.y) : "r"(adv + rho * 8u));
+    return w;
   }
 };
 
@@ -295,7 +301,10 @@ __global__ void __launch_bounds__(kBlock) fs_enum_kernel(const KParams P) {
 
   using KT = typename std::conditional<KTAB, KTabSmem, KTabArith>::type;
   KT kt;
-  if constexpr (KTAB) kt.base = (uint32_t)__cvta_generic_to_shared(ktab_s);
+  if constexpr (KTAB) {
+    kt.base = (uint32_t)__cvta_generic_to_shared(ktab_s);
+    kt.adv = kt.base + 4u * c.adv_off;
+  }
   const int lane = threadIdx.x & 31;
   Lane<D> st;
 #pragma unroll
