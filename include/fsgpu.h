@@ -93,7 +93,14 @@ enum {
  *   tail        count consumer only: FS_TAIL_ROWS (0, default) steps through every valid
  *               factorization of a node (one modulo-skip step per row); FS_TAIL_CLOSED (1)
  *               counts a node's rows in O(1) as floor(a* / s) + 1 (the
- *               closed form of the paper's suffix-set idea).  Same result. */
+ *               closed form of the paper's suffix-set idea).  Same result.
+ *   gen_order   FS_GENORDER_GIVEN (0, default) runs the stream over the generators in the
+ *               caller's order; FS_GENORDER_AUTO (1) lets count / hist / any and order=any
+ *               materialise run it over a permutation that minimises the number of nodes
+ *               (largest generators first; "regardless of
+ *               order").  Results are reported in the caller's coordinates (witnesses,
+ *               COORD_GE predicates, row coordinates); canonical-order materialise always
+ *               uses the given order. */
 typedef struct {
     int device;
     void *cuda_stream;
@@ -103,11 +110,13 @@ typedef struct {
     int ctas_per_sm;
     int order;
     int tail;
-    int reserved[6];
+    int gen_order;
+    int reserved[5];
 } fs_exec_t;
 
 enum { FS_ORDER_CANONICAL = 0, FS_ORDER_ANY = 1 };
 enum { FS_TAIL_ROWS = 0, FS_TAIL_CLOSED = 1 };
+enum { FS_GENORDER_GIVEN = 0, FS_GENORDER_AUTO = 1 };
 
 /* ---------------------------------------------------------------------------------
  * north_star entry points: current CUDA device, default stream, whole instance.

@@ -17,6 +17,7 @@ FS_CONSUMER_COUNT, FS_CONSUMER_HIST, FS_CONSUMER_ANY, FS_CONSUMER_ROWS = 0, 1, 2
 FS_MAX_D = 16
 FS_ORDER_CANONICAL, FS_ORDER_ANY = 0, 1
 FS_TAIL_ROWS, FS_TAIL_CLOSED = 0, 1
+FS_GENORDER_GIVEN, FS_GENORDER_AUTO = 0, 1
 
 u64 = ctypes.c_uint64
 i64 = ctypes.c_int64
@@ -35,7 +36,8 @@ class ExecT(ctypes.Structure):
         ("ctas_per_sm", ctypes.c_int),
         ("order", ctypes.c_int),
         ("tail", ctypes.c_int),
-        ("reserved", ctypes.c_int * 6),
+        ("gen_order", ctypes.c_int),
+        ("reserved", ctypes.c_int * 5),
     ]
 
 

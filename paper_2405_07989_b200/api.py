@@ -19,7 +19,8 @@ def _torch():
 
 
 def _exec(device: Optional[int] = None, stream=None, rank: int = 0, world: int = 1,
-          slice_units: int = 0, ctas_per_sm: int = 0, order: int = 0, tail: int = 0) -> L.ExecT:
+          slice_units: int = 0, ctas_per_sm: int = 0, order: int = 0, tail: int = 0,
+          gen_order: int = 0) -> L.ExecT:
     ex = L.ExecT()
     ex.device = -1 if device is None else int(device)
     ex.cuda_stream = None if stream is None else ctypes.c_void_p(int(stream))
@@ -29,6 +30,7 @@ def _exec(device: Optional[int] = None, stream=None, rank: int = 0, world: int =
     ex.ctas_per_sm = int(ctas_per_sm)
     ex.order = int(order)
     ex.tail = int(tail)
+    ex.gen_order = int(gen_order)
     return ex
 
 
@@ -92,19 +94,19 @@ def fs_enumerate(n: int, gens: Sequence[int], B: int = 16, cap: Optional[int] = 
 
 # ------------------------------------------------------------------ _ex variants
 def fs_count_ex(n, gens, *, device=None, stream=None, rank=0, world=1, slice_units=0, ctas_per_sm=0,
-                tail=L.FS_TAIL_ROWS) -> int:
+                tail=L.FS_TAIL_ROWS, gen_order=L.FS_GENORDER_GIVEN) -> int:
     g, d = L.gens_array(gens)
-    ex = _exec(device, _stream_handle(stream), rank, world, slice_units, ctas_per_sm, 0, tail)
+    ex = _exec(device, _stream_handle(stream), rank, world, slice_units, ctas_per_sm, 0, tail, gen_order)
     out = ctypes.c_uint64(0)
     L.check(L.lib().fs_count_ex(int(n), g, d, ctypes.byref(ex), ctypes.byref(out)), "fs_count_ex")
     return int(out.value)
 
 
 def fs_length_set_ex(n, gens, hist=None, *, device=None, stream=None, rank=0, world=1, slice_units=0,
-                     ctas_per_sm=0):
+                     ctas_per_sm=0, gen_order=L.FS_GENORDER_GIVEN):
     torch = _torch()
     g, d = L.gens_array(gens)
-    ex = _exec(device, _stream_handle(stream), rank, world, slice_units, ctas_per_sm)
+    ex = _exec(device, _stream_handle(stream), rank, world, slice_units, ctas_per_sm, 0, 0, gen_order)
     if hist is None:
         hist = torch.empty(hist_len(n, gens), dtype=torch.int64,
                            device="cuda" if device is None else "cuda:%d" % device)
@@ -114,9 +116,9 @@ def fs_length_set_ex(n, gens, hist=None, *, device=None, stream=None, rank=0, wo
 
 
 def fs_any_ex(n, gens, pred, pred_arg, *, device=None, stream=None, rank=0, world=1, slice_units=0,
-              ctas_per_sm=0):
+              ctas_per_sm=0, gen_order=L.FS_GENORDER_GIVEN):
     g, d = L.gens_array(gens)
-    ex = _exec(device, _stream_handle(stream), rank, world, slice_units, ctas_per_sm)
+    ex = _exec(device, _stream_handle(stream), rank, world, slice_units, ctas_per_sm, 0, 0, gen_order)
     found = ctypes.c_int(0)
     wit = (ctypes.c_uint32 * max(1, d))()
     L.check(L.lib().fs_any_ex(int(n), g, d, ctypes.byref(ex), int(pred), int(pred_arg), ctypes.byref(found),
@@ -125,12 +127,12 @@ def fs_any_ex(n, gens, pred, pred_arg, *, device=None, stream=None, rank=0, worl
 
 
 def fs_enumerate_ex(n, gens, B=16, cap=None, out=None, *, device=None, stream=None, rank=0, world=1,
-                    slice_units=0, ctas_per_sm=0, order=L.FS_ORDER_CANONICAL):
+                    slice_units=0, ctas_per_sm=0, order=L.FS_ORDER_CANONICAL, gen_order=L.FS_GENORDER_GIVEN):
     """This rank's block of rows.  Returns (rank_rows, global_row_offset, rows_tensor).
     order=FS_ORDER_ANY: warp-compacted (M2) layout, same multiset of rows, arbitrary order."""
     torch = _torch()
     g, d = L.gens_array(gens)
-    ex = _exec(device, _stream_handle(stream), rank, world, slice_units, ctas_per_sm, order)
+    ex = _exec(device, _stream_handle(stream), rank, world, slice_units, ctas_per_sm, order, 0, gen_order)
     if cap is None:
         info = Plan(n, gens, L.FS_CONSUMER_ROWS, rank=rank, world=world).info
         cap = info["row_end"] - info["row_begin"]
@@ -151,13 +153,14 @@ class Plan:
 
     def __init__(self, n: int, gens: Sequence[int], consumer: int = L.FS_CONSUMER_COUNT, *,
                  device: Optional[int] = None, stream=None, rank: int = 0, world: int = 1,
-                 slice_units: int = 0, ctas_per_sm: int = 0, order: int = 0, tail: int = 0):
+                 slice_units: int = 0, ctas_per_sm: int = 0, order: int = 0, tail: int = 0,
+                 gen_order: int = 0):
         self.n = int(n)
         self.gens = tuple(int(x) for x in gens)
         self.consumer = consumer
         g, d = L.gens_array(gens)
         self._stream = stream
-        ex = _exec(device, _stream_handle(stream), rank, world, slice_units, ctas_per_sm, order, tail)
+        ex = _exec(device, _stream_handle(stream), rank, world, slice_units, ctas_per_sm, order, tail, gen_order)
         h = ctypes.c_void_p()
         L.check(L.lib().fs_plan_create(self.n, g, d, int(consumer), ctypes.byref(ex), ctypes.byref(h)),
                 "fs_plan_create")

@@ -168,6 +168,10 @@ int fs_plan_any_async(fs_plan *p, int pred, uint64_t pred_arg, int *found_dev, u
   fs::KParams kp = base_params(p);
   kp.pred = pred;
   kp.pred_arg = pred_arg;
+  if (pred == FS_PRED_COORD_GE) {  // caller's coordinate index -> the stream's index
+    const uint64_t i = pred_arg >> 32;
+    if (i < (uint64_t)p->d) kp.pred_arg = ((uint64_t)p->iperm[i] << 32) | (pred_arg & 0xffffffffull);
+  }
   kp.found = found_dev;
   kp.witness = witness_dev;
   // bit-reversed claim order: every region of the lex order is sampled early (early exit)

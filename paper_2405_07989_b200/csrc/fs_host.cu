@@ -87,6 +87,38 @@ int fs_validate_and_build(fs_plan *p, uint64_t n, const uint32_t *gens, int d, i
   p->g.assign(gens, gens + d);
   p->hist_len = n / gmin + 1;
 
+  // Generator order of the stream.  Z(n, pi g) = pi Z(n, g), so count,
+  // histogram, any and unordered materialise may run over any permutation; the number of
+  // level-L nodes depends only on the multiset of the first L generators and is smallest
+  // with the largest first.  Canonical-order materialise keeps the caller's order.
+  std::vector<int> perm(d);
+  for (int i = 0; i < d; ++i) perm[i] = i;
+  const bool may_permute = e.gen_order == FS_GENORDER_AUTO &&
+                           (consumer != FS_CONSUMER_ROWS || e.order == FS_ORDER_ANY) && d >= 3;
+  if (may_permute) {
+    std::vector<int> desc(perm);
+    std::stable_sort(desc.begin(), desc.end(), [&](int a, int b) { return gens[a] > gens[b]; });
+    auto nodes_L = [&](const std::vector<int> &pm) {
+      std::vector<uint64_t> F(n + 1, 0);
+      F[0] = 1;
+      for (int k = 0; k < d - 2; ++k) {
+        const uint64_t gk = gens[pm[k]];
+        for (uint64_t r = gk; r <= n; ++r) F[r] = std::min<uint64_t>(F[r] + F[r - gk], 1ull << 62);
+      }
+      u128 s = 0;
+      for (uint64_t r = 0; r <= n; ++r) s += F[r];
+      return s;
+    };
+    if (nodes_L(desc) < nodes_L(perm)) perm = desc;
+  }
+  p->gi.resize(d);
+  std::vector<uint32_t> &gi = p->gi;
+  for (int j = 0; j < d; ++j) {
+    gi[j] = gens[perm[j]];
+    p->iperm[perm[j]] = (uint8_t)j;
+  }
+  gens = gi.data();
+
   Consts &c = p->c;
   memset(&c, 0, sizeof(c));
   c.n = (uint32_t)n;
@@ -94,6 +126,7 @@ int fs_validate_and_build(fs_plan *p, uint64_t n, const uint32_t *gens, int d, i
   for (int i = 0; i < d; ++i) {
     c.g[i] = gens[i];
     c.dv[i] = fs_make_div(gens[i]);
+    c.perm[i] = (uint8_t)perm[i];
   }
   // node units for count / hist / any; row units for materialise (exact offsets)
   c.alpha = (consumer == FS_CONSUMER_ROWS) ? 0u : 1u;
@@ -259,6 +292,7 @@ namespace {
 
 struct HostSink {
   int d = 0;
+  const uint8_t *perm = nullptr;  // internal coordinate j -> caller coordinate perm[j]
   uint64_t count = 0;
   uint64_t *hist = nullptr;
   uint64_t hist_cap = 0;
@@ -268,7 +302,9 @@ struct HostSink {
   uint64_t slice_rows = 0;
   uint32_t first[FS_MAX_D];
   bool have_first = false;
-  void put(const uint32_t *v) {
+  void put(const uint32_t *vi) {
+    uint32_t v[FS_MAX_D];
+    for (int j = 0; j < d; ++j) v[perm ? perm[j] : j] = vi[j];
     uint64_t len = 0;
     for (int i = 0; i < d; ++i) len += v[i];
     if (hist && len < hist_cap) hist[len]++;
@@ -361,6 +397,7 @@ extern "C" int fsdbg_host_model(const fs_plan *p, uint64_t *count_out, uint64_t 
   if (rows && B != 16 && B != 32) return FS_EINVAL;
   HostSink sink;
   sink.d = p->d;
+  sink.perm = p->c.perm;
   sink.hist = hist;
   sink.hist_cap = hist_cap;
   sink.B = B;

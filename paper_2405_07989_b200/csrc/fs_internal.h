@@ -56,7 +56,9 @@ struct fs_plan {
   int d = 0;
   int consumer = 0;
   fs_exec_t ex{};
-  std::vector<uint32_t> g;
+  std::vector<uint32_t> g;        // generators as given by the caller
+  std::vector<uint32_t> gi;       // generators in the internal (stream) order
+  uint8_t iperm[FS_MAX_D] = {0};  // caller coordinate i is internal coordinate iperm[i]
   fs::Consts c{};                 // host copy (U/ktab point at host vectors)
   std::vector<uint64_t> U;        // L * (n+1)
   std::vector<uint32_t> ktab;     // g_{d-1} entries or empty

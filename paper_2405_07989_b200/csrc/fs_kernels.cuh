@@ -99,11 +99,11 @@ struct EmitAny {
     }
     if (ok && !hit) {
       hit = true;
-      if (atomicCAS(found, 0, 1) == 0 && wit) {
+      if (atomicCAS(found, 0, 1) == 0 && wit) {  // caller's coordinate order
 #pragma unroll
-        for (int j = 0; j < D - 2; ++j) wit[j] = st.a[j];
-        wit[D - 2] = (uint32_t)st.cur;
-        wit[D - 1] = ad;
+        for (int j = 0; j < D - 2; ++j) wit[c.perm[j]] = st.a[j];
+        wit[c.perm[D - 2]] = (uint32_t)st.cur;
+        wit[c.perm[D - 1]] = ad;
       }
     }
   }
@@ -169,12 +169,12 @@ struct EmitCompact {
   }
   __device__ __forceinline__ void cond(bool em, const Lane<D> &st, const Consts &c) {
     const unsigned m = __ballot_sync(kFull, em);
-    if (em) {
+    if (em) {  // coordinates written at the caller's positions (generator order may differ)
       unsigned char *q = buf + (wrows + (uint32_t)__popc(m & lanemask_lt())) * kRB;
 #pragma unroll
-      for (int j = 0; j < D - 2; ++j) put(q, j, st.a[j]);
-      put(q, D - 2, (uint32_t)st.cur);
-      put(q, D - 1, row_ad<D>(st, c));
+      for (int j = 0; j < D - 2; ++j) put(q, c.perm[j], st.a[j]);
+      put(q, c.perm[D - 2], (uint32_t)st.cur);
+      put(q, c.perm[D - 1], row_ad<D>(st, c));
     }
     wrows += (uint32_t)__popc(m);
   }

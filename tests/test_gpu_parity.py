@@ -96,6 +96,42 @@ def test_count_closed_tail(oracle_mod, inst):
         assert api.fs_count_ex(n, g, slice_units=T, tail=L.FS_TAIL_CLOSED) == want
 
 
+@pytest.mark.parametrize("inst", ALL, ids=ids)
+def test_generator_order_auto(oracle_mod, inst):
+    """NEXT-2 (stream over the largest generators first): same count / histogram / any, rows in
+    the caller's coordinates (M2 layout), witnesses and COORD_GE indices in caller order."""
+    n, g = inst.n, inst.gens
+    AUTO = L.FS_GENORDER_AUTO
+    want = oracle.run(n, g, hist_len=oracle.hist_len_for(n, g))
+    assert api.fs_count_ex(n, g, gen_order=AUTO) == want["count"]
+    assert api.fs_count_ex(n, g, gen_order=AUTO, tail=L.FS_TAIL_CLOSED) == want["count"]
+    h = api.fs_length_set_ex(n, g, gen_order=AUTO)
+    assert hist_list(h, len(want["hist"])) == want["hist"]
+    rows = oracle.rows_as_tuples(oracle.rows(n, g, B=32), len(g), 32)
+    for pred, arg in [(L.FS_PRED_COORD_GE, ((len(g) - 1) << 32) | 2), (L.FS_PRED_COORD_GE, 1),
+                      (L.FS_PRED_LEN_EQ, sum(rows[len(rows) // 2]) if rows else 1)]:
+        found, wit = api.fs_any_ex(n, g, pred, arg, gen_order=AUTO)
+        assert found == any(oracle.pred_holds(r, pred, arg) for r in rows)
+        if found:
+            assert tuple(wit) in set(rows) and oracle.pred_holds(wit, pred, arg)
+    B = 32
+    nr, off, t = api.fs_enumerate_ex(n, g, B=B, order=L.FS_ORDER_ANY, gen_order=AUTO)
+    assert nr == len(rows)
+    assert rows_bytes(api.sort_rows_desc(t)) == oracle.rows(n, g, B=B)
+
+
+def test_c5_auto_order_full():
+    g = gold("C5")
+    AUTO = L.FS_GENORDER_AUTO
+    assert api.fs_count_ex(W.C5.n, W.C5.gens, gen_order=AUTO) == g["count"]
+    assert api.fs_count_ex(W.C5.n, W.C5.gens, gen_order=AUTO, tail=L.FS_TAIL_CLOSED) == g["count"]
+    h = api.fs_length_set_ex(W.C5.n, W.C5.gens, gen_order=AUTO)
+    assert hist_list(h, 20001) == g["hist"]
+    found, wit = api.fs_any_ex(W.C5.n, W.C5.gens, L.FS_PRED_LEN_LE, 20, gen_order=AUTO)
+    assert found and wit == [0, 0, 0, 0, 20]
+    assert not api.fs_any_ex(W.C5.n, W.C5.gens, L.FS_PRED_LEN_LE, 19, gen_order=AUTO)[0]
+
+
 @pytest.mark.parametrize("inst", ALL[:40], ids=ids)
 def test_any(oracle_mod, inst):
     n, g = inst.n, inst.gens

@@ -77,6 +77,35 @@ def test_closed_tail_count(oracle_mod, inst):
         assert a["slice_counts"] == b["slice_counts"]
 
 
+@pytest.mark.parametrize("inst", INSTANCES, ids=lambda i: "%s" % i.name)
+def test_generator_order_auto(oracle_mod, inst):
+    """NEXT-2: the stream over a permutation of the generators gives the same count and
+    histogram, and the same multiset of rows in the caller's coordinates."""
+    n, g = inst.n, inst.gens
+    want = oracle.run(n, g, hist_len=oracle.hist_len_for(n, g))
+    for tail in (0, 1):
+        r = host_model(n, g, L.FS_CONSUMER_COUNT, gen_order=L.FS_GENORDER_AUTO, tail=tail, slice_units=3,
+                       want_hist=(tail == 0))
+        assert r["count"] == want["count"]
+        if tail == 0:
+            assert r["hist"] == want["hist"]
+    r = host_model(n, g, L.FS_CONSUMER_COUNT, gen_order=L.FS_GENORDER_AUTO, want_rows=True, B=32)
+    got = sorted(oracle.rows_as_tuples(r["rows"], len(g), 32), reverse=True)
+    assert got == oracle.rows_as_tuples(oracle.rows(n, g, B=32), len(g), 32)
+
+
+def test_generator_order_choice():
+    # C5: largest generators first collapses 6.7e11 nodes to 7.7e5
+    p = Plan(W.C5.n, W.C5.gens, gen_order=L.FS_GENORDER_AUTO)
+    assert p.info["nodes_per_level"][-1] < 10 ** 6
+    assert p.info["total_rows"] == 4055053706
+    q = Plan(W.C3.n, W.C3.gens, gen_order=L.FS_GENORDER_AUTO)
+    assert q.info["nodes_per_level"][-1] < Plan(W.C3.n, W.C3.gens).info["nodes_per_level"][-1]
+    # canonical materialise never permutes
+    r = Plan(W.C5.n, W.C5.gens, L.FS_CONSUMER_ROWS, gen_order=L.FS_GENORDER_AUTO)
+    assert r.info["nodes_per_level"][-1] > 10 ** 11
+
+
 @pytest.mark.parametrize("inst", INSTANCES[:30], ids=lambda i: "%s" % i.name)
 def test_slices_exact_and_gap_free(oracle_mod, inst):
     """Per-slice row counts equal the oracle's rows in that lex range: no gaps, no overlap."""
