@@ -416,8 +416,9 @@ def extras(args, world, rank, local, dev, stream, peaks, peaks_kind, barrier, ma
 
     # ---- store: C2-XL rows, u16; canonical layout (M1) and warp-compacted layout (M2)
     inst = W.C2XL
-    for order, key in ((L.FS_ORDER_CANONICAL, "store"), (L.FS_ORDER_ANY, "store_any")):
-        p = api.Plan(inst.n, inst.gens, L.FS_CONSUMER_ROWS, order=order, **kw)
+    for order, key, go in ((L.FS_ORDER_CANONICAL, "store", 0), (L.FS_ORDER_ANY, "store_any", 0),
+                           (L.FS_ORDER_ANY, "store_any_auto_order", L.FS_GENORDER_AUTO)):
+        p = api.Plan(inst.n, inst.gens, L.FS_CONSUMER_ROWS, order=order, gen_order=go, **kw)
         info = p.info
         rows = info["row_end"] - info["row_begin"]
         out = torch.empty((rows, inst.d), dtype=torch.uint16, device=dev)
@@ -427,8 +428,9 @@ def extras(args, world, rank, local, dev, stream, peaks, peaks_kind, barrier, ma
         bytes_ = total_rows * inst.d * 2
         gbs_all = bytes_ / (ms / 1e3) / 1e9
         peak = peaks["hbm_gbs"] * world
-        ex[key] = {"workload": "C2XL: Z(16000, (11,13,17,19,23)) materialise u16 rows, %s order"
-                               % ("canonical (exact offsets)" if order == 0 else "any (warp compaction)"),
+        ex[key] = {"workload": "C2XL: Z(16000, (11,13,17,19,23)) materialise u16 rows, %s order%s"
+                               % ("canonical (exact offsets)" if order == 0 else "any (warp compaction)",
+                                  ", NEXT-2 generator order" if go else ""),
                    "rows": total_rows, "bytes": bytes_, "ms": ms, "value": total_rows / (ms / 1e3), "unit": UNIT,
                    "roofline": {"bound": "hbm", "achieved": gbs_all, "peak": peak, "unit": "GB/s",
                                 "frac": gbs_all / peak,
@@ -437,55 +439,51 @@ def extras(args, world, rank, local, dev, stream, peaks, peaks_kind, barrier, ma
         del out
         torch.cuda.empty_cache()
 
-    # ---- C4 length histogram
-    inst = W.C4
-    p = api.Plan(inst.n, inst.gens, L.FS_CONSUMER_HIST, **kw)
-    h = torch.zeros(api.hist_len(inst.n, inst.gens), dtype=torch.int64, device=dev)
-
-    def hist_step():
-        p.hist_async(h)
-        allreduce(h)
-
-    ms = _time_ms(hist_step, stream, 2, barrier, max_over_ranks)
-    total = int(h.sum().item())
-    ex["hist"] = {"workload": "C4: Z(4275, C3 gens) length histogram (329 bins)", "rows": total, "ms": ms,
-                  "value": total / (ms / 1e3), "unit": UNIT}
-
-    # ---- C3 count with the NEXT-1 closed-form tail
-    inst = W.C3
-    p = api.Plan(inst.n, inst.gens, L.FS_CONSUMER_COUNT, tail=L.FS_TAIL_CLOSED, **kw)
+    # ---- count / hist / any on their configs; NEXT-1 (closed tail) and NEXT-2 (generator
+    # order) variants of SURVEY 8(f) are labelled and reported beside the literal path
     c = torch.zeros(1, dtype=torch.int64, device=dev)
-
-    def cc_step():
-        p.count_async(c)
-        allreduce(c)
-
-    ms = _time_ms(cc_step, stream, 3, barrier, max_over_ranks)
-    ex["count_closed_tail"] = {"workload": "C3 count, closed-form 2-D tail (NEXT-1)", "rows": int(c.item()),
-                               "ms": ms, "value": int(c.item()) / (ms / 1e3), "unit": UNIT}
-
-    # ---- C5: skewed/non-minimal generators: count and the any-predicates (early exit)
-    inst = W.C5
-    p = api.Plan(inst.n, inst.gens, L.FS_CONSUMER_COUNT, **kw)
-
-    def c5_step():
-        p.count_async(c)
-        allreduce(c)
-
-    ms = _time_ms(c5_step, stream, 1, barrier, max_over_ranks)
-    ex["c5_count"] = {"workload": "C5: Z(20000, (1,1,2,997,1000)) count", "rows": int(c.item()), "ms": ms,
-                      "value": int(c.item()) / (ms / 1e3), "unit": UNIT}
-    pa = api.Plan(inst.n, inst.gens, L.FS_CONSUMER_ANY, **kw)
     f = torch.zeros(1, dtype=torch.int32, device=dev)
-    w = torch.zeros(inst.d, dtype=torch.int32, device=dev)
-    for name, pred, arg in (("P_late", L.FS_PRED_LEN_LE, 20), ("P_none", L.FS_PRED_LEN_LE, 19),
-                            ("P_first", L.FS_PRED_LEN_GE, 19995)):
-        def any_step():
-            pa.any_async(pred, arg, f, w)
-            allreduce(f, dist.ReduceOp.MAX if world > 1 else None)
+    w = torch.zeros(16, dtype=torch.int32, device=dev)
+    AUTO = L.FS_GENORDER_AUTO
+    runs = [
+        ("hist", W.C4, L.FS_CONSUMER_HIST, {}, "C4 length histogram (329 bins), given order", 2),
+        ("hist_auto_order", W.C4, L.FS_CONSUMER_HIST, {"gen_order": AUTO}, "C4 histogram, NEXT-2 order", 2),
+        ("count_closed_tail", W.C3, L.FS_CONSUMER_COUNT, {"tail": 1}, "C3 count, NEXT-1 closed tail", 3),
+        ("count_auto_order", W.C3, L.FS_CONSUMER_COUNT, {"gen_order": AUTO}, "C3 count, NEXT-2 order", 3),
+        ("count_auto_order_closed", W.C3, L.FS_CONSUMER_COUNT, {"gen_order": AUTO, "tail": 1},
+         "C3 count, NEXT-1 + NEXT-2", 3),
+        ("c5_count", W.C5, L.FS_CONSUMER_COUNT, {}, "C5 count, given order", 1),
+        ("c5_count_auto_order", W.C5, L.FS_CONSUMER_COUNT, {"gen_order": AUTO}, "C5 count, NEXT-2 order", 3),
+    ]
+    for key, inst, cons, pk, label, reps in runs:
+        p = api.Plan(inst.n, inst.gens, cons, **pk, **kw)
+        if cons == L.FS_CONSUMER_HIST:
+            h = torch.zeros(api.hist_len(inst.n, inst.gens), dtype=torch.int64, device=dev)
 
-        ms = _time_ms(any_step, stream, 1, barrier, max_over_ranks)
-        ex["c5_any_" + name] = {"pred": [pred, arg], "found": bool(f.item()), "ms": ms}
+            def fn():
+                p.hist_async(h)
+                allreduce(h)
+        else:
+            def fn():
+                p.count_async(c)
+                allreduce(c)
+        fn()
+        ms = _time_ms(fn, stream, reps, barrier, max_over_ranks)
+        total = int(h.sum().item()) if cons == L.FS_CONSUMER_HIST else int(c.item())
+        assert total == p.info["total_rows"], (key, total)
+        ex[key] = {"workload": "%s: Z(%d, %s)" % (label, inst.n, list(inst.gens)), "rows": total, "ms": ms,
+                   "value": total / (ms / 1e3), "unit": UNIT,
+                   "nodes": p.info["nodes_per_level"][-1]}
+    for order_name, pk in (("", {}), ("_auto_order", {"gen_order": AUTO})):
+        pa = api.Plan(W.C5.n, W.C5.gens, L.FS_CONSUMER_ANY, **pk, **kw)
+        for name, pred, arg in (("P_late", L.FS_PRED_LEN_LE, 20), ("P_none", L.FS_PRED_LEN_LE, 19),
+                                ("P_first", L.FS_PRED_LEN_GE, 19995)):
+            def any_step():
+                pa.any_async(pred, arg, f, w)
+                allreduce(f, dist.ReduceOp.MAX if world > 1 else None)
+
+            ms = _time_ms(any_step, stream, 1, barrier, max_over_ranks)
+            ex["c5_any_%s%s" % (name, order_name)] = {"pred": [pred, arg], "found": bool(f.item()), "ms": ms}
     return ex
 
 
