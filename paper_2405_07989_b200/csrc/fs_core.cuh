@@ -70,6 +70,7 @@ struct Consts {
   uint32_t ktab_len;     // 0: k0 by arithmetic; else words of the node tables (below)
   uint32_t adv_off;      // word offset of the advance table inside ktab (8 B aligned)
   uint8_t perm[FS_MAX_D];  // internal coordinate j is the caller's coordinate perm[j]
+  uint32_t permuted;       // perm is not the identity
   const uint64_t *U;     // DP tables, L rows of (n+1) entries
   // node tables (device or host), for rho in [0, g_{d-1}):
   //   ktab[rho]                     = k0(rho)

@@ -109,38 +109,59 @@ struct EmitAny {
   }
 };
 
-// Rows are appended to a per-lane 256 B ring in shared memory (lane-rotated by 4 B so that
-// lanes at equal positions hit distinct banks).  When a 128 B half completes it becomes
-// "pending" and the warp copies it to its exact canonical byte offset.
+// M1 (canonical order).  Rows are appended LINEARLY to the lane's staging buffer at byte w
+// (w < 2 kHalf before a write, so a row never wraps and every coordinate is one STS with an
+// immediate offset).  When w crosses kHalf, half 0 is complete; when it crosses 2 kHalf,
+// half 1 is complete and the bytes that spilled past it are moved to the front (half 0 was
+// flushed one group earlier).  Completed halves are copied by the warp to their exact
+// canonical byte offsets.
 template <int D, int B>
 struct EmitRows {
   static constexpr uint32_t kRB = D * (B / 8);
-  unsigned char *ring;
-  uint32_t rot;
-  uint32_t wpos;        // bytes of the current slice written so far
+  unsigned char *buf;
+  uint32_t w;           // write position in buf
+  uint64_t gpos;        // canonical byte offset of buf[0] in the output
   uint64_t slice_goff;  // byte offset of the slice in the output
   bool pend;
-  uint32_t pend_soff;
+  uint32_t pend_soff, pend_len;
   uint64_t pend_goff;
-  __device__ __forceinline__ void put(uint32_t p, int i, uint32_t v) {
+  __device__ __forceinline__ void put(unsigned char *q, int i, uint32_t v) {
     if (B == 16)
-      *reinterpret_cast<uint16_t *>(ring + ((p + 2 * i + rot) & (kStageBytes - 1))) = (uint16_t)v;
+      *reinterpret_cast<uint16_t *>(q + 2 * i) = (uint16_t)v;
     else
-      *reinterpret_cast<uint32_t *>(ring + ((p + 4 * i + rot) & (kStageBytes - 1))) = v;
+      *reinterpret_cast<uint32_t *>(q + 4 * i) = v;
+  }
+  __device__ __forceinline__ void start(uint64_t goff) {
+    slice_goff = goff;
+    gpos = goff;
+    w = 0;
   }
   __device__ __forceinline__ void cond(bool em, const Lane<D> &st, const Consts &c) {
     if (!em) return;
-    const uint32_t p = wpos;
+    unsigned char *q = buf + w;
 #pragma unroll
-    for (int j = 0; j < D - 2; ++j) put(p, j, st.a[j]);
-    put(p, D - 2, (uint32_t)st.cur);
-    put(p, D - 1, row_ad<D>(st, c));
-    const uint32_t np = p + kRB;
-    wpos = np;
-    if ((p / kHalf) != (np / kHalf)) {
+    for (int j = 0; j < D - 2; ++j) put(q, j, st.a[j]);
+    put(q, D - 2, (uint32_t)st.cur);
+    put(q, D - 1, row_ad<D>(st, c));
+    const uint32_t nw = w + kRB;
+    const bool c0 = w < kHalf && nw >= kHalf;          // half 0 complete
+    const bool c1 = w < 2 * kHalf && nw >= 2 * kHalf;  // half 1 complete (both, for rows > kHalf)
+    if (c0 || c1) {
       pend = true;
-      pend_soff = p & kHalf;
-      pend_goff = slice_goff + (uint64_t)(p & ~(kHalf - 1));
+      pend_soff = c0 ? 0u : kHalf;
+      pend_len = (c0 && c1) ? 2 * kHalf : kHalf;
+      pend_goff = gpos + pend_soff;
+    }
+    w = nw;
+  }
+  // after the group's flush: move the bytes that spilled past the two halves to the front
+  // (a group writes at most max(kHalf, one row) bytes, so w < 2 kHalf + 64 here)
+  __device__ __forceinline__ void rebase() {
+    if (w >= 2 * kHalf) {
+      for (uint32_t i = 2 * kHalf; i < w; i += 2)
+        *reinterpret_cast<uint16_t *>(buf + (i - 2 * kHalf)) = *reinterpret_cast<const uint16_t *>(buf + i);
+      gpos += 2 * kHalf;
+      w -= 2 * kHalf;
     }
   }
 };
@@ -171,10 +192,18 @@ struct EmitCompact {
     const unsigned m = __ballot_sync(kFull, em);
     if (em) {  // coordinates written at the caller's positions (generator order may differ)
       unsigned char *q = buf + (wrows + (uint32_t)__popc(m & lanemask_lt())) * kRB;
+      const uint32_t ad = row_ad<D>(st, c);
+      if (c.permuted) {
 #pragma unroll
-      for (int j = 0; j < D - 2; ++j) put(q, c.perm[j], st.a[j]);
-      put(q, c.perm[D - 2], (uint32_t)st.cur);
-      put(q, c.perm[D - 1], row_ad<D>(st, c));
+        for (int j = 0; j < D - 2; ++j) put(q, c.perm[j], st.a[j]);
+        put(q, c.perm[D - 2], (uint32_t)st.cur);
+        put(q, c.perm[D - 1], ad);
+      } else {
+#pragma unroll
+        for (int j = 0; j < D - 2; ++j) put(q, j, st.a[j]);
+        put(q, D - 2, (uint32_t)st.cur);
+        put(q, D - 1, ad);
+      }
     }
     wrows += (uint32_t)__popc(m);
   }
@@ -215,34 +244,32 @@ struct EmitCompact {
   }
 };
 
-// Warp-cooperative copy of every lane's pending ring segment: 32/(kHalf/16) segments per
-// round, kHalf/16 lanes x 16 B each -> fully coalesced 16 B stores.  len is a multiple of 16.
+// Warp-cooperative copy of every lane's pending staging segment (a multiple of 16 B, at most
+// 2 kHalf): 16 segments per round, 2 lanes per segment, 16 B per lane per iteration.
 __device__ __forceinline__ void warp_flush(bool &pend, uint32_t soff, uint64_t goff, uint32_t len,
                                            const unsigned char *warp_stage, unsigned char *out) {
   unsigned pm = __ballot_sync(kFull, pend);
   if (!pm) return;
-  constexpr int kLanesPerSeg = kHalf / 16, kSegs = 32 / kLanesPerSeg;
+  constexpr int kLanesPerSeg = 2, kSegs = 32 / kLanesPerSeg;
   const int lane = threadIdx.x & 31, sub = lane / kLanesPerSeg, j = lane % kLanesPerSeg;
   while (pm) {
     unsigned m = pm;
-#pragma unroll
-    for (int x = 0; x < kSegs - 1; ++x)
-      if (x < sub) m &= m - 1;
+    for (int x = 0; x < sub && m; ++x) m &= m - 1;
     const int src = m ? (__ffs(m) - 1) : -1;
     const int sl = src < 0 ? 0 : src;
     const uint32_t s_soff = __shfl_sync(kFull, soff, sl);
     const uint32_t s_len = __shfl_sync(kFull, len, sl);
     const uint64_t s_goff = __shfl_sync(kFull, goff, sl);
-    if (src >= 0 && (uint32_t)j * 16u < s_len) {
-      const unsigned char *r = warp_stage + src * kStageBytes;
-      const uint32_t base = s_soff + (uint32_t)j * 16u + 4u * (uint32_t)src;
-      uint4 v;
-      constexpr uint32_t M = kStageBytes - 1;
-      v.x = *reinterpret_cast<const uint32_t *>(r + (base & M));
-      v.y = *reinterpret_cast<const uint32_t *>(r + ((base + 4u) & M));
-      v.z = *reinterpret_cast<const uint32_t *>(r + ((base + 8u) & M));
-      v.w = *reinterpret_cast<const uint32_t *>(r + ((base + 12u) & M));
-      __stcs(reinterpret_cast<uint4 *>(out + s_goff + (uint64_t)j * 16u), v);
+    if (src >= 0) {
+      for (uint32_t o = (uint32_t)j * 16u; o < s_len; o += 16u * kLanesPerSeg) {
+        const uint32_t *r = reinterpret_cast<const uint32_t *>(warp_stage + src * kLaneStride + s_soff + o);
+        uint4 v;
+        v.x = r[0];
+        v.y = r[1];
+        v.z = r[2];
+        v.w = r[3];
+        __stcs(reinterpret_cast<uint4 *>(out + s_goff + o), v);
+      }
     }
 #pragma unroll
     for (int x = 0; x < kSegs; ++x) pm &= pm ? pm - 1 : 0u;
@@ -250,21 +277,21 @@ __device__ __forceinline__ void warp_flush(bool &pend, uint32_t soff, uint64_t g
   pend = false;
 }
 
-// ROWS: the lane's slice is complete -- copy the ragged tail of its last half byte by byte
-// (only at the end of the rank's block) and mark the 16 B-aligned part for the warp flush.
+// ROWS: the lane's slice is complete -- the bytes [w & ~(kHalf-1), w) of its last half: the
+// 16 B-aligned part goes to the warp flush, a ragged tail (only at the very end of the
+// rank's block) is stored byte by byte.
 template <int D, int B>
 __device__ __forceinline__ void rows_slice_done(const KParams &P, EmitRows<D, B> &er, bool &fin, uint32_t &fin_soff,
                                                 uint64_t &fin_goff, uint32_t &fin_len) {
-  const uint32_t w = er.wpos;
+  const uint32_t w = er.w;
   const uint32_t hstart = w & ~(kHalf - 1);
   const uint32_t plen = w - hstart;
   const uint32_t alen = plen & ~15u;
-  for (uint32_t b = alen; b < plen; ++b)
-    P.rows_out[er.slice_goff + hstart + b] = er.ring[(hstart + b + er.rot) & (kStageBytes - 1)];
+  for (uint32_t b = alen; b < plen; ++b) P.rows_out[er.gpos + hstart + b] = er.buf[hstart + b];
   if (alen) {
     fin = true;
-    fin_soff = hstart & kHalf;
-    fin_goff = er.slice_goff + hstart;
+    fin_soff = hstart;
+    fin_goff = er.gpos + hstart;
     fin_len = alen;
   }
 }
@@ -325,17 +352,16 @@ __global__ void __launch_bounds__(kBlock) fs_enum_kernel(const KParams P) {
   EmitHist<D> e_hist{hist_s, P.hist_out, P.hist_smem, 0};
   EmitAny<D> e_any{P.pred, P.pred_arg, P.found, P.witness, false};
   EmitRows<D, B> e_rows;
-  e_rows.ring = stage + threadIdx.x * kStageBytes;
-  e_rows.rot = 4u * (uint32_t)lane;
-  e_rows.wpos = 0;
-  e_rows.slice_goff = 0;
+  e_rows.buf = stage + threadIdx.x * kLaneStride;
+  e_rows.start(0);
+  e_rows.pend_len = kHalf;
   e_rows.pend = false;
   e_rows.pend_soff = 0;
   e_rows.pend_goff = 0;
   bool fin = false;
   uint32_t fin_soff = 0, fin_len = 0;
   uint64_t fin_goff = 0;
-  const unsigned char *warp_stage = stage + (threadIdx.x & ~31) * kStageBytes;
+  const unsigned char *warp_stage = stage + (threadIdx.x & ~31) * kLaneStride;
   EmitCompact<D, B> e_cmp;
   e_cmp.buf = stage + (threadIdx.x >> 5) * kWarpBuf;
   e_cmp.wrows = 0;
@@ -379,10 +405,7 @@ __global__ void __launch_bounds__(kBlock) fs_enum_kernel(const KParams P) {
             budget = (uint32_t)(e - u);
             const uint64_t off = unrank<D, NEED_AD>(st, c, kt, u);
             budget -= position_in_node<D, NEED_AD>(st, c, off);
-            if (CONS == FS_CONSUMER_ROWS) {
-              e_rows.slice_goff = (u - P.unit0) * (uint64_t)EmitRows<D, B>::kRB;
-              e_rows.wpos = 0;
-            }
+            if (CONS == FS_CONSUMER_ROWS) e_rows.start((u - P.unit0) * (uint64_t)EmitRows<D, B>::kRB);
           }
         }
       }
@@ -401,6 +424,7 @@ __global__ void __launch_bounds__(kBlock) fs_enum_kernel(const KParams P) {
 
 #pragma unroll 1
     for (int it = 0; it < INNER; it += UNROLL) {
+      const bool had = budget != 0;
       // UNROLL branch-free fast steps, then one (warp-uniform) check for lanes parked on an
       // ascend; the rare slow lanes run the generic successor step together.
 #pragma unroll
@@ -417,14 +441,14 @@ __global__ void __launch_bounds__(kBlock) fs_enum_kernel(const KParams P) {
           fast_step<D, NEED_AD, ALPHA>(st, c, kt, budget, e_cmp);
           e_cmp.flush(P, false);
         } else {
-          const bool was = budget != 0;
           fast_step<D, NEED_AD, ALPHA>(st, c, kt, budget, e_rows);
-          if (was && budget == 0) rows_slice_done(P, e_rows, fin, fin_soff, fin_goff, fin_len);
         }
       }
       if (CONS == FS_CONSUMER_ROWS) {
-        warp_flush(e_rows.pend, e_rows.pend_soff, e_rows.pend_goff, kHalf, warp_stage, P.rows_out);
+        if (had && budget == 0) rows_slice_done(P, e_rows, fin, fin_soff, fin_goff, fin_len);
+        warp_flush(e_rows.pend, e_rows.pend_soff, e_rows.pend_goff, e_rows.pend_len, warp_stage, P.rows_out);
         warp_flush(fin, fin_soff, fin_goff, fin_len, warp_stage, P.rows_out);
+        e_rows.rebase();
       }
       const bool slow = needs_slow<D>(st, budget);
       if (__any_sync(kFull, slow)) {
@@ -433,7 +457,7 @@ __global__ void __launch_bounds__(kBlock) fs_enum_kernel(const KParams P) {
           if (CONS == FS_CONSUMER_ROWS && budget == 0) rows_slice_done(P, e_rows, fin, fin_soff, fin_goff, fin_len);
         }
         if (CONS == FS_CONSUMER_ROWS) {
-          warp_flush(e_rows.pend, e_rows.pend_soff, e_rows.pend_goff, kHalf, warp_stage, P.rows_out);
+          warp_flush(e_rows.pend, e_rows.pend_soff, e_rows.pend_goff, e_rows.pend_len, warp_stage, P.rows_out);
           warp_flush(fin, fin_soff, fin_goff, fin_len, warp_stage, P.rows_out);
         }
       }
@@ -492,7 +516,7 @@ __global__ void fs_d1_kernel(const KParams P) {
 static size_t smem_bytes(const KParams &kp, int consumer) {
   size_t b = (size_t)((kp.c.ktab_len + 3u) & ~3u) * 4;
   if (consumer == FS_CONSUMER_HIST && kp.hist_smem) b += (size_t)((kp.hist_len + 3u) & ~3u) * 4;
-  if (consumer == FS_CONSUMER_ROWS) b += (size_t)kBlock * kStageBytes;
+  if (consumer == FS_CONSUMER_ROWS) b += (size_t)kBlock * kLaneStride;
   if (consumer == kConsRowsAny) b += (size_t)(kBlock / 32) * kWarpBuf;
   return b;
 }
