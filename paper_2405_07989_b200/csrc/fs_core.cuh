@@ -105,7 +105,48 @@ struct Lane {
   int32_t cur;     // current row's a_{d-1} (< 0: none left in this node)
   uint32_t ad;     // unused placeholder (a_d is solved on demand by row_ad())
   uint32_t lsum;   // a_1 + .. + a_L (tracked when the consumer needs lengths/coordinates)
+  // Lazy counters of the fast path: k = node advances still allowed before a sync (at most
+  // min(budget, a_L)); kb = its value at the last sync.  Between syncs, a_L, lsum and (node
+  // units) the budget are behind by (kb - k); see sync_k / cur_aL / cur_lsum.
+  uint32_t k, kb;
 };
+
+template <int D>
+FS_HD uint32_t cur_aL(const Lane<D> &st) {  // a_L as of now
+  if constexpr (D >= 3)
+    return st.a[D - 3] - (st.kb - st.k);
+  else
+    return 0;
+}
+template <int D>
+FS_HD uint32_t cur_lsum(const Lane<D> &st) {
+  return st.lsum - (st.kb - st.k);
+}
+// row coordinate j < L as of now
+template <int D>
+FS_HD uint32_t cur_coord(const Lane<D> &st, int j) {
+  if constexpr (D >= 3)
+    return j == D - 3 ? cur_aL<D>(st) : st.a[j];
+  else
+    return 0;
+}
+
+// Apply the fast path's pending advances to a_L, lsum and the budget, and re-arm k.
+template <int D, int ALPHA>
+FS_HD void sync_k(Lane<D> &st, uint32_t &budget) {
+  constexpr int L = D - 2;
+  if constexpr (L >= 1) {
+    const uint32_t used = st.kb - st.k;
+    st.a[L - 1] -= used;
+    st.lsum -= used;
+    if (ALPHA) budget -= used;
+    const uint32_t al = st.a[L - 1];
+    st.k = ALPHA ? (budget < al ? budget : al) : al;
+    st.kb = st.k;
+  } else {
+    st.k = st.kb = 0;
+  }
+}
 
 // Node-table lookups: k0(rho), and step(rho) = the advance transition (next residue, carry,
 // k0 of the next residue) -- from the tables (host vector, or a shared-memory copy on the
@@ -252,6 +293,7 @@ FS_HD uint64_t unrank(Lane<D> &st, const Consts &c, const KT &kt, uint64_t u) {
   st.A = A;
   st.rho = R - A * c.gA;
   st.lsum = lsum;
+  st.k = st.kb = 0;
   entry<D, NEED_AD>(st, c, kt);
   return u;
 }
@@ -298,18 +340,16 @@ template <int D, bool NEED_AD, int ALPHA, class KT, class Emit>
 FS_HD void fast_step(Lane<D> &st, const Consts &c, const KT &kt, uint32_t &budget, Emit &emit) {
   constexpr int L = D - 2;
   if constexpr (L >= 1) {
-    const uint32_t al = st.a[L - 1];
-    const bool fa = budget != 0 && st.cur < 0 && al != 0;
+    // k > 0 <=> a_L > 0 and (node units) budget left, as of the last sync
+    const bool fa = st.cur < 0 && st.k != 0;
     // one table load: next residue of R_L + g_L mod g_{d-1}, the carry into floor(R_L/g_{d-1}),
     // and k0 of the next residue (all lanes load; only advancing lanes commit)
     const Adv w = kt.step(st.rho, c);
-    if (fa) {  // advance (a_L -= 1, R_L += g_L) and entry of the new node, predicated
-      st.a[L - 1] = al - 1u;
+    if (fa) {  // advance (a_L -= 1, R_L += g_L, lazily via k) and entry of the new node
+      st.k -= 1u;
       st.rho = w.x & 0x7fffffffu;
       st.A += c.q + (w.x >> 31);
       st.cur = (int32_t)st.A - (int32_t)w.y;
-      if (ALPHA) budget -= 1u;
-      if (NEED_AD) st.lsum -= 1u;
     }
   }
   // node units: every row of an entered node belongs to the slice; row units: budget-limited
@@ -330,15 +370,13 @@ template <int D, class KT>
 FS_HD void fast_step_closed(Lane<D> &st, const Consts &c, const KT &kt, uint32_t &budget, uint32_t &cnt) {
   constexpr int L = D - 2;
   if constexpr (L >= 1) {
-    const uint32_t al = st.a[L - 1];
-    const bool fa = budget != 0 && st.cur < 0 && al != 0;
+    const bool fa = st.cur < 0 && st.k != 0;
     const Adv w = kt.step(st.rho, c);
     if (fa) {
-      st.a[L - 1] = al - 1u;
+      st.k -= 1u;
       st.rho = w.x & 0x7fffffffu;
       st.A += c.q + (w.x >> 31);
       st.cur = (int32_t)st.A - (int32_t)w.y;
-      budget -= 1u;
     }
   }
   const bool em = st.cur >= 0;  // node units: the node's rows all belong to this slice
@@ -349,6 +387,7 @@ FS_HD void fast_step_closed(Lane<D> &st, const Consts &c, const KT &kt, uint32_t
   }
 }
 
+// (called after sync_k)
 template <int D>
 FS_HD bool needs_slow(const Lane<D> &st, uint32_t budget) {
   constexpr int L = D - 2;

@@ -331,7 +331,7 @@ struct HostEmit {
 #ifndef __CUDA_ARCH__
     if (!em) return;
     uint32_t v[FS_MAX_D];
-    for (int j = 0; j < D - 2; ++j) v[j] = st.a[j];
+    for (int j = 0; j < D - 2; ++j) v[j] = fs::cur_coord<D>(st, j);
     v[D - 2] = (uint32_t)st.cur;
     v[D - 1] = fs::row_ad<D>(st, c);
     sink->put(v);
@@ -348,6 +348,7 @@ void host_model_d(const fs_plan *p, const KT &ktab, HostSink &sink, uint64_t *sl
     fs::Lane<D> st;
     uint64_t off = fs::unrank<D, true>(st, c, ktab, u);
     budget -= fs::position_in_node<D, true>(st, c, off);
+    fs::sync_k<D, ALPHA>(st, budget);
     sink.slice_rows = 0;
     sink.have_first = false;
     HostEmit<D> emit{&sink};
@@ -356,14 +357,22 @@ void host_model_d(const fs_plan *p, const KT &ktab, HostSink &sink, uint64_t *sl
       uint32_t cnt = 0;
       while (!fs::needs_refill<D, ALPHA>(st, budget)) {
         fs::fast_step_closed<D>(st, c, ktab, budget, cnt);
-        if (fs::needs_slow<D>(st, budget)) fs::slow_step<D, true, ALPHA>(st, c, ktab, budget);
+        fs::sync_k<D, ALPHA>(st, budget);
+        if (fs::needs_slow<D>(st, budget)) {
+          fs::slow_step<D, true, ALPHA>(st, c, ktab, budget);
+          fs::sync_k<D, ALPHA>(st, budget);
+        }
       }
       sink.count += cnt;
       sink.slice_rows = cnt;
     } else {
       while (!fs::needs_refill<D, ALPHA>(st, budget)) {
         fs::fast_step<D, true, ALPHA>(st, c, ktab, budget, emit);
-        if (fs::needs_slow<D>(st, budget)) fs::slow_step<D, true, ALPHA>(st, c, ktab, budget);
+        fs::sync_k<D, ALPHA>(st, budget);
+        if (fs::needs_slow<D>(st, budget)) {
+          fs::slow_step<D, true, ALPHA>(st, c, ktab, budget);
+          fs::sync_k<D, ALPHA>(st, budget);
+        }
       }
     }
     if (slice_counts) slice_counts[sl] = sink.slice_rows;

@@ -57,7 +57,7 @@ struct EmitHist {
   uint32_t n;
   __device__ __forceinline__ void cond(bool em, const Lane<D> &st, const Consts &c) {
     if (!em) return;
-    const uint32_t l = st.lsum + (uint32_t)st.cur + row_ad<D>(st, c);  // length = sum_i a_i
+    const uint32_t l = cur_lsum<D>(st) + (uint32_t)st.cur + row_ad<D>(st, c);  // length = sum_i a_i
     if (smem)
       atomicAdd(&bins[l], 1u);
     else
@@ -72,7 +72,7 @@ __device__ __forceinline__ uint32_t coord(const Lane<D> &st, uint32_t i, uint32_
   if (i == D - 2) v = (uint32_t)st.cur;
 #pragma unroll
   for (int j = 0; j < D - 2; ++j)
-    if (i == (uint32_t)j) v = st.a[j];
+    if (i == (uint32_t)j) v = cur_coord<D>(st, j);
   return v;
 }
 
@@ -86,7 +86,7 @@ struct EmitAny {
   __device__ __forceinline__ void cond(bool em, const Lane<D> &st, const Consts &c) {
     if (!em) return;
     const uint32_t ad = row_ad<D>(st, c);
-    const uint64_t len = (uint64_t)st.lsum + (uint32_t)st.cur + ad;
+    const uint64_t len = (uint64_t)cur_lsum<D>(st) + (uint32_t)st.cur + ad;
     bool ok;
     switch (pred) {
       case FS_PRED_LEN_LE: ok = len <= arg; break;
@@ -101,7 +101,7 @@ struct EmitAny {
       hit = true;
       if (atomicCAS(found, 0, 1) == 0 && wit) {  // caller's coordinate order
 #pragma unroll
-        for (int j = 0; j < D - 2; ++j) wit[c.perm[j]] = st.a[j];
+        for (int j = 0; j < D - 2; ++j) wit[c.perm[j]] = cur_coord<D>(st, j);
         wit[c.perm[D - 2]] = (uint32_t)st.cur;
         wit[c.perm[D - 1]] = ad;
       }
@@ -140,7 +140,7 @@ struct EmitRows {
     if (!em) return;
     unsigned char *q = buf + w;
 #pragma unroll
-    for (int j = 0; j < D - 2; ++j) put(q, j, st.a[j]);
+    for (int j = 0; j < D - 2; ++j) put(q, j, cur_coord<D>(st, j));
     put(q, D - 2, (uint32_t)st.cur);
     put(q, D - 1, row_ad<D>(st, c));
     const uint32_t nw = w + kRB;
@@ -195,12 +195,12 @@ struct EmitCompact {
       const uint32_t ad = row_ad<D>(st, c);
       if (c.permuted) {
 #pragma unroll
-        for (int j = 0; j < D - 2; ++j) put(q, c.perm[j], st.a[j]);
+        for (int j = 0; j < D - 2; ++j) put(q, c.perm[j], cur_coord<D>(st, j));
         put(q, c.perm[D - 2], (uint32_t)st.cur);
         put(q, c.perm[D - 1], ad);
       } else {
 #pragma unroll
-        for (int j = 0; j < D - 2; ++j) put(q, j, st.a[j]);
+        for (int j = 0; j < D - 2; ++j) put(q, j, cur_coord<D>(st, j));
         put(q, D - 2, (uint32_t)st.cur);
         put(q, D - 1, ad);
       }
@@ -344,6 +344,7 @@ __global__ void __launch_bounds__(kBlock) fs_enum_kernel(const KParams P) {
   st.cur = -1;
   st.ad = 0;
   st.lsum = 0;
+  st.k = st.kb = 0;
   uint32_t budget = 0;
   bool alive = true;
   uint64_t acc = 0;
@@ -405,6 +406,7 @@ __global__ void __launch_bounds__(kBlock) fs_enum_kernel(const KParams P) {
             budget = (uint32_t)(e - u);
             const uint64_t off = unrank<D, NEED_AD>(st, c, kt, u);
             budget -= position_in_node<D, NEED_AD>(st, c, off);
+            sync_k<D, ALPHA>(st, budget);
             if (CONS == FS_CONSUMER_ROWS) e_rows.start((u - P.unit0) * (uint64_t)EmitRows<D, B>::kRB);
           }
         }
@@ -418,6 +420,7 @@ __global__ void __launch_bounds__(kBlock) fs_enum_kernel(const KParams P) {
         alive = false;
         budget = 0;
         st.cur = -1;
+        st.k = st.kb = 0;
       }
     }
     if (__ballot_sync(kFull, alive) == 0) break;
@@ -450,10 +453,12 @@ __global__ void __launch_bounds__(kBlock) fs_enum_kernel(const KParams P) {
         warp_flush(fin, fin_soff, fin_goff, fin_len, warp_stage, P.rows_out);
         e_rows.rebase();
       }
+      sync_k<D, ALPHA>(st, budget);
       const bool slow = needs_slow<D>(st, budget);
       if (__any_sync(kFull, slow)) {
         if (slow) {
           slow_step<D, NEED_AD, ALPHA>(st, c, kt, budget);
+          sync_k<D, ALPHA>(st, budget);
           if (CONS == FS_CONSUMER_ROWS && budget == 0) rows_slice_done(P, e_rows, fin, fin_soff, fin_goff, fin_len);
         }
         if (CONS == FS_CONSUMER_ROWS) {
@@ -464,6 +469,7 @@ __global__ void __launch_bounds__(kBlock) fs_enum_kernel(const KParams P) {
       if (CONS == FS_CONSUMER_ANY && e_any.hit) {
         budget = 0;
         st.cur = -1;
+        st.k = st.kb = 0;
         alive = false;
       }
     }
