@@ -84,7 +84,7 @@ enum {
  *               order (contiguous, equal DP weight; PAPER.md:196-200 bounds, 230-231
  *               distributed workers).  world = 0 is treated as 1.
  *   slice_units target units per slice (0 = automatic); rows per slice for ROWS plans
- *               (rounded up to a multiple of 32).  Tests force tiny slices with it.
+ *               (rounded up to a multiple of 64).  Tests force tiny slices with it.
  *   ctas_per_sm persistent CTAs per SM (0 = occupancy maximum).
  *   order       materialise layout: FS_ORDER_CANONICAL (0, default) writes every row at its
  *               exact canonical offset; FS_ORDER_ANY (1) compacts rows per warp with

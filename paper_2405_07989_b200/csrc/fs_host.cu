@@ -235,7 +235,7 @@ int fs_validate_and_build(fs_plan *p, uint64_t n, const uint32_t *gens, int d, i
   uint64_t T = e.slice_units;
   if (T == 0) T = std::max<uint64_t>(1, ceil_div_u64(span, kTargetLanes * kSlicesPerLane));
   T = std::min<uint64_t>(T, 1ull << 24);
-  if (consumer == FS_CONSUMER_ROWS) T = (T + 31) & ~31ull;  // slices start 64 B aligned
+  if (consumer == FS_CONSUMER_ROWS) T = (T + 63) & ~63ull;  // slices start 128 B aligned
   p->T = T;
   p->num_slices = span ? ceil_div_u64(span, T) : 0;
   return FS_OK;

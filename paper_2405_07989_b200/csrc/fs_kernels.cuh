@@ -181,7 +181,18 @@ struct EmitCompact {
   static constexpr uint32_t kRB = D * (B / 8);
   static constexpr uint32_t kCap = kWarpBuf / kRB;
   unsigned char *buf;
-  uint32_t wrows;  // warp-uniform
+  uint32_t wrows;           // warp-uniform
+  uint32_t poff[D];         // byte offset of internal coordinate j in the caller's row
+  __device__ __forceinline__ void init(const Consts &c) {
+#pragma unroll
+    for (int j = 0; j < D; ++j) poff[j] = (uint32_t)c.perm[j] * (B / 8);
+  }
+  __device__ __forceinline__ void putb(unsigned char *q, uint32_t off, uint32_t v) {
+    if (B == 16)
+      *reinterpret_cast<uint16_t *>(q + off) = (uint16_t)v;
+    else
+      *reinterpret_cast<uint32_t *>(q + off) = v;
+  }
   __device__ __forceinline__ void put(unsigned char *q, int i, uint32_t v) {
     if (B == 16)
       *reinterpret_cast<uint16_t *>(q + 2 * i) = (uint16_t)v;
@@ -195,9 +206,9 @@ struct EmitCompact {
       const uint32_t ad = row_ad<D>(st, c);
       if (c.permuted) {
 #pragma unroll
-        for (int j = 0; j < D - 2; ++j) put(q, c.perm[j], cur_coord<D>(st, j));
-        put(q, c.perm[D - 2], (uint32_t)st.cur);
-        put(q, c.perm[D - 1], ad);
+        for (int j = 0; j < D - 2; ++j) putb(q, poff[j], cur_coord<D>(st, j));
+        putb(q, poff[D - 2], (uint32_t)st.cur);
+        putb(q, poff[D - 1], ad);
       } else {
 #pragma unroll
         for (int j = 0; j < D - 2; ++j) put(q, j, cur_coord<D>(st, j));
@@ -245,12 +256,12 @@ struct EmitCompact {
 };
 
 // Warp-cooperative copy of every lane's pending staging segment (a multiple of 16 B, at most
-// 2 kHalf): 16 segments per round, 2 lanes per segment, 16 B per lane per iteration.
+// 2 kHalf): 8 segments per round, 4 lanes per segment, 16 B per lane per iteration.
 __device__ __forceinline__ void warp_flush(bool &pend, uint32_t soff, uint64_t goff, uint32_t len,
                                            const unsigned char *warp_stage, unsigned char *out) {
   unsigned pm = __ballot_sync(kFull, pend);
   if (!pm) return;
-  constexpr int kLanesPerSeg = 2, kSegs = 32 / kLanesPerSeg;
+  constexpr int kLanesPerSeg = 4, kSegs = 32 / kLanesPerSeg;
   const int lane = threadIdx.x & 31, sub = lane / kLanesPerSeg, j = lane % kLanesPerSeg;
   while (pm) {
     unsigned m = pm;
@@ -366,6 +377,7 @@ __global__ void __launch_bounds__(kBlock) fs_enum_kernel(const KParams P) {
   EmitCompact<D, B> e_cmp;
   e_cmp.buf = stage + (threadIdx.x >> 5) * kWarpBuf;
   e_cmp.wrows = 0;
+  if (CONS == kConsRowsAny) e_cmp.init(c);
 
   for (;;) {
     const bool need = alive && needs_refill<D, ALPHA>(st, budget);

@@ -121,7 +121,7 @@ def test_slices_exact_and_gap_free(oracle_mod, inst):
     # row-sliced plans: every slice holds exactly T rows except the last
     rr = host_model(n, g, L.FS_CONSUMER_ROWS, slice_units=8, want_slices=True)
     sc, T = rr["slice_counts"], rr["info"]["slice_units"]
-    assert T % 32 == 0
+    assert T % 64 == 0
     assert all(c == T for c in sc[:-1]) and (not sc or 1 <= sc[-1] <= T)
 
 
