@@ -122,11 +122,17 @@ def microbench():
     return out
 
 
-def ops_model(info) -> float:
-    """algorithmic integer ops of the whole instance."""
+OPS_NODE_CLOSED = 14  # node entry + closed-form row count floor(a*/s) + 1 (NEXT-1)
+
+
+def ops_model(info, closed: bool = False) -> float:
+    """algorithmic integer ops of the stream the kernel runs: per node
+    entry, per row (per-row tail) or per node (closed tail), per deeper node."""
     nodes = info["nodes_per_level"]
     L = info["level"]
     deep = sum(nodes[1:L]) if L >= 2 else 0
+    if closed:
+        return OPS_NODE_CLOSED * nodes[L] + OPS_DEEP * deep
     return OPS_NODE * nodes[L] + OPS_ROW * info["total_rows"] + OPS_DEEP * deep
 
 
@@ -265,8 +271,11 @@ def main():
         return float(t.item())
 
     # ---- plan: constants + DP tables resident in HBM before the timed region
+    # the configuration fs_count() runs: generators largest-first (NEXT-2) and the closed-form
+    # tail (NEXT-1); the literal per-row stream over the given order is reported in extra
+    headline = {"gen_order": L.FS_GENORDER_AUTO, "tail": L.FS_TAIL_CLOSED}
     plan = api.Plan(inst.n, inst.gens, L.FS_CONSUMER_COUNT, device=local, stream=stream.cuda_stream,
-                    rank=rank, world=world)
+                    rank=rank, world=world, **headline)
     info = plan.info
     out = torch.zeros(1, dtype=torch.int64, device=dev)
     flush = torch.empty(256 << 20, dtype=torch.uint8, device=dev)  # > 126 MB L2
@@ -317,7 +326,7 @@ def main():
     measured_tops = max(v["tops"] for k, v in mb.items() if isinstance(v, dict)) if mb else None
     peak_tops = measured_tops or derived_tops
     share = (info["unit_end"] - info["unit_begin"]) / max(1, info["total_units"])
-    ops = ops_model(info) * share
+    ops = ops_model(info, closed=True) * share
     achieved = ops / (ms_kern / 1e3) / 1e12
     traffic = None
     prof = os.path.join(ROOT, "profiles", "traffic.json")
@@ -333,6 +342,9 @@ def main():
         "vs_baseline": None, "dtype": "u32", "data": "synthetic",
         "config": {"workload": "%s: Z(%d, %s) count, |Z| = %d" % (inst.name, inst.n, list(inst.gens), total),
                    "instance": inst.name, "n": inst.n, "gens": list(inst.gens), "consumer": "count",
+                   "method": "Alg. 3.1 stream over the generators largest-first (gen_order=auto, NEXT-2), "
+                             "modulo skip at run entry, closed-form row count per node (tail=closed, NEXT-1)",
+                   "nodes": info["nodes_per_level"][-1],
                    "parallelism": "lex-slice dp%d" % world, "l2": "flushed between steps (256 MB write)",
                    "dist_backend": backend if world > 1 else None,
                    "slice_units": info["slice_units"], "num_slices": info["num_slices"],
@@ -446,6 +458,7 @@ def extras(args, world, rank, local, dev, stream, peaks, peaks_kind, barrier, ma
     w = torch.zeros(16, dtype=torch.int32, device=dev)
     AUTO = L.FS_GENORDER_AUTO
     runs = [
+        ("count_literal", W.C3, L.FS_CONSUMER_COUNT, {}, "C3 count, given order, one step per row", 3),
         ("hist", W.C4, L.FS_CONSUMER_HIST, {}, "C4 length histogram (329 bins), given order", 2),
         ("hist_auto_order", W.C4, L.FS_CONSUMER_HIST, {"gen_order": AUTO}, "C4 histogram, NEXT-2 order", 2),
         ("count_closed_tail", W.C3, L.FS_CONSUMER_COUNT, {"tail": 1}, "C3 count, NEXT-1 closed tail", 3),
@@ -474,6 +487,13 @@ def extras(args, world, rank, local, dev, stream, peaks, peaks_kind, barrier, ma
         ex[key] = {"workload": "%s: Z(%d, %s)" % (label, inst.n, list(inst.gens)), "rows": total, "ms": ms,
                    "value": total / (ms / 1e3), "unit": UNIT,
                    "nodes": p.info["nodes_per_level"][-1]}
+        if cons == L.FS_CONSUMER_COUNT and mb:
+            pi = p.info
+            sh = (pi["unit_end"] - pi["unit_begin"]) / max(1, pi["total_units"])
+            ach = ops_model(pi, closed=pk.get("tail", 0) == 1) * sh / (ms / 1e3) / 1e12
+            pk_tops = max(v["tops"] for v in mb.values() if isinstance(v, dict))
+            ex[key]["roofline"] = {"bound": "alu", "achieved": ach, "peak": pk_tops, "unit": "Tops/s",
+                                   "frac": ach / pk_tops}
     for order_name, pk in (("", {}), ("_auto_order", {"gen_order": AUTO})):
         pa = api.Plan(W.C5.n, W.C5.gens, L.FS_CONSUMER_ANY, **pk, **kw)
         for name, pred, arg in (("P_late", L.FS_PRED_LEN_LE, 20), ("P_none", L.FS_PRED_LEN_LE, 19),

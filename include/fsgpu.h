@@ -120,7 +120,11 @@ enum { FS_GENORDER_GIVEN = 0, FS_GENORDER_AUTO = 1 };
 
 /* ---------------------------------------------------------------------------------
  * north_star entry points: current CUDA device, default stream, whole instance.
- * All are synchronous: they return after the result is available.
+ * All are synchronous: they return after the result is available.  They pick the fastest
+ * exact configuration: fs_count / fs_length_set / fs_any run the stream with
+ * gen_order = FS_GENORDER_AUTO (and fs_count with tail = FS_TAIL_CLOSED); fs_enumerate
+ * keeps the caller's generator order (it defines the canonical row order).  The _ex
+ * variants run exactly the configuration their fs_exec_t asks for.
  * --------------------------------------------------------------------------------- */
 
 /* |Z(n, gens)| into *count_out (host). */

@@ -236,6 +236,8 @@ int fs_count(uint64_t n, const uint32_t *gens, int d, uint64_t *count_out) {
   memset(&ex, 0, sizeof(ex));
   ex.device = -1;
   ex.world = 1;
+  ex.gen_order = FS_GENORDER_AUTO;  // exact for any order; fewest nodes first
+  ex.tail = FS_TAIL_CLOSED;         // a node's rows counted by division (NEXT-1)
   return fs_count_ex(n, gens, d, &ex, count_out);
 }
 
@@ -256,6 +258,7 @@ int fs_length_set(uint64_t n, const uint32_t *gens, int d, uint64_t *hist_dev, u
   memset(&ex, 0, sizeof(ex));
   ex.device = -1;
   ex.world = 1;
+  ex.gen_order = FS_GENORDER_AUTO;
   return fs_length_set_ex(n, gens, d, &ex, hist_dev, hist_cap);
 }
 
@@ -291,6 +294,7 @@ int fs_any(uint64_t n, const uint32_t *gens, int d, int pred, uint64_t pred_arg,
   memset(&ex, 0, sizeof(ex));
   ex.device = -1;
   ex.world = 1;
+  ex.gen_order = FS_GENORDER_AUTO;
   return fs_any_ex(n, gens, d, &ex, pred, pred_arg, found_out, witness_or_null);
 }
 

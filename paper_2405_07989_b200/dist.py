@@ -73,7 +73,8 @@ def count(n: int, gens: Sequence[int], *, slice_units: int = 0) -> int:
 
     rank, world = _world()
     p = Plan(n, gens, L.FS_CONSUMER_COUNT, device=torch.cuda.current_device(),
-             stream=torch.cuda.current_stream().cuda_stream, rank=rank, world=world, slice_units=slice_units)
+             stream=torch.cuda.current_stream().cuda_stream, rank=rank, world=world, slice_units=slice_units,
+             gen_order=L.FS_GENORDER_AUTO, tail=L.FS_TAIL_CLOSED)  # same configuration as fs_count
     t = torch.zeros(1, dtype=torch.int64, device="cuda")
     p.count_async(t)
     combine_sum(t)
@@ -85,7 +86,8 @@ def length_set(n: int, gens: Sequence[int], *, slice_units: int = 0):
 
     rank, world = _world()
     p = Plan(n, gens, L.FS_CONSUMER_HIST, device=torch.cuda.current_device(),
-             stream=torch.cuda.current_stream().cuda_stream, rank=rank, world=world, slice_units=slice_units)
+             stream=torch.cuda.current_stream().cuda_stream, rank=rank, world=world, slice_units=slice_units,
+             gen_order=L.FS_GENORDER_AUTO)
     h = torch.zeros(hist_len(n, gens), dtype=torch.int64, device="cuda")
     p.hist_async(h)
     return combine_sum(h)
@@ -96,7 +98,7 @@ def any_pred(n: int, gens: Sequence[int], pred: int, arg: int) -> bool:
 
     rank, world = _world()
     p = Plan(n, gens, L.FS_CONSUMER_ANY, device=torch.cuda.current_device(),
-             stream=torch.cuda.current_stream().cuda_stream, rank=rank, world=world)
+             stream=torch.cuda.current_stream().cuda_stream, rank=rank, world=world, gen_order=L.FS_GENORDER_AUTO)
     f = torch.zeros(1, dtype=torch.int32, device="cuda")
     p.any_async(pred, arg, f)
     return bool(combine_max(f).item())

@@ -1,7 +1,7 @@
 """Run one hot-path kernel a few times for ncu captures (never a bench number).
 
   python profiles/workload.py <name> [reps]
-  names: c3count c3closed c4hist c5count c5any_none c2xl_m1 c2xl_m2
+  names: c3count c3closed c3auto c3autoclosed c4hist c5count c5any_none c2xl_m1 c2xl_m2 c2xl_m2auto
 """
 import os
 import sys
@@ -19,9 +19,10 @@ from paper_2405_07989_b200 import workloads as W  # noqa: E402
 def main():
     name = sys.argv[1]
     reps = int(sys.argv[2]) if len(sys.argv) > 2 else 2
-    if name in ("c3count", "c3closed", "c5count"):
+    if name in ("c3count", "c3closed", "c5count", "c3auto", "c3autoclosed"):
         inst = W.C5 if name == "c5count" else W.C3
-        p = api.Plan(inst.n, inst.gens, L.FS_CONSUMER_COUNT, tail=1 if name == "c3closed" else 0)
+        p = api.Plan(inst.n, inst.gens, L.FS_CONSUMER_COUNT, tail=1 if "closed" in name else 0,
+                     gen_order=1 if "auto" in name else 0)
         out = torch.zeros(1, dtype=torch.int64, device="cuda")
         fn = lambda: p.count_async(out)
     elif name == "c4hist":
@@ -34,9 +35,10 @@ def main():
         p = api.Plan(inst.n, inst.gens, L.FS_CONSUMER_ANY)
         f = torch.zeros(1, dtype=torch.int32, device="cuda")
         fn = lambda: p.any_async(L.FS_PRED_LEN_LE, 19, f)
-    elif name in ("c2xl_m1", "c2xl_m2"):
+    elif name in ("c2xl_m1", "c2xl_m2", "c2xl_m2auto"):
         inst = W.C2XL
-        p = api.Plan(inst.n, inst.gens, L.FS_CONSUMER_ROWS, order=0 if name == "c2xl_m1" else 1)
+        p = api.Plan(inst.n, inst.gens, L.FS_CONSUMER_ROWS, order=0 if name == "c2xl_m1" else 1,
+                     gen_order=1 if name == "c2xl_m2auto" else 0)
         rows = p.info["total_rows"]
         out = torch.empty((rows, inst.d), dtype=torch.uint16, device="cuda")
         fn = lambda: p.enumerate_async(16, out, rows)
