@@ -461,6 +461,8 @@ def extras(args, world, rank, local, dev, stream, peaks, peaks_kind, barrier, ma
         ("count_literal", W.C3, L.FS_CONSUMER_COUNT, {}, "C3 count, given order, one step per row", 3),
         ("hist", W.C4, L.FS_CONSUMER_HIST, {}, "C4 length histogram (329 bins), given order", 2),
         ("hist_auto_order", W.C4, L.FS_CONSUMER_HIST, {"gen_order": AUTO}, "C4 histogram, NEXT-2 order", 2),
+        ("hist_auto_order_closed", W.C4, L.FS_CONSUMER_HIST, {"gen_order": AUTO, "tail": 1},
+         "C4 histogram, NEXT-1 + NEXT-2 (fs_length_set default)", 3),
         ("count_closed_tail", W.C3, L.FS_CONSUMER_COUNT, {"tail": 1}, "C3 count, NEXT-1 closed tail", 3),
         ("count_auto_order", W.C3, L.FS_CONSUMER_COUNT, {"gen_order": AUTO}, "C3 count, NEXT-2 order", 3),
         ("count_auto_order_closed", W.C3, L.FS_CONSUMER_COUNT, {"gen_order": AUTO, "tail": 1},

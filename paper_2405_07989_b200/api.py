@@ -103,10 +103,10 @@ def fs_count_ex(n, gens, *, device=None, stream=None, rank=0, world=1, slice_uni
 
 
 def fs_length_set_ex(n, gens, hist=None, *, device=None, stream=None, rank=0, world=1, slice_units=0,
-                     ctas_per_sm=0, gen_order=L.FS_GENORDER_GIVEN):
+                     ctas_per_sm=0, gen_order=L.FS_GENORDER_GIVEN, tail=L.FS_TAIL_ROWS):
     torch = _torch()
     g, d = L.gens_array(gens)
-    ex = _exec(device, _stream_handle(stream), rank, world, slice_units, ctas_per_sm, 0, 0, gen_order)
+    ex = _exec(device, _stream_handle(stream), rank, world, slice_units, ctas_per_sm, 0, tail, gen_order)
     if hist is None:
         hist = torch.empty(hist_len(n, gens), dtype=torch.int64,
                            device="cuda" if device is None else "cuda:%d" % device)

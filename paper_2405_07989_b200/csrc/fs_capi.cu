@@ -155,6 +155,19 @@ int fs_plan_hist_async(fs_plan *p, uint64_t *hist_dev, uint64_t hist_cap) {
   if (cudaMemsetAsync(hist_dev, 0, hist_cap * 8, p->stream) != cudaSuccess) return FS_ECUDA;
   fs::KParams kp = base_params(p);
   kp.hist_out = reinterpret_cast<unsigned long long *>(hist_dev);
+  if (p->ex.tail == FS_TAIL_CLOSED && p->d >= 2) {
+    // closed tail: strided difference array + finalize (two launches)
+    kp.diff_len = (uint32_t)(p->hist_len + p->c.dstride);
+    kp.hist_smem = kp.diff_len <= fs::kHistSmemMax ? 1u : 0u;
+    if (!p->diff_dev && cudaMalloc(&p->diff_dev, (size_t)kp.diff_len * 8) != cudaSuccess) return FS_ENOMEM;
+    if (cudaMemsetAsync(p->diff_dev, 0, (size_t)kp.diff_len * 8, p->stream) != cudaSuccess) return FS_ECUDA;
+    kp.diff_out = p->diff_dev;
+    rc = fs_launch(p, fs::kConsHistClosed, 16, kp, p->stream);
+    if (rc != FS_OK) return rc;
+    rc = fs_launch_hist_finalize(kp, p->stream);
+    if (rc == FS_OK) p->last_launches = 2;
+    return rc;
+  }
   return finish(p, fs_launch(p, FS_CONSUMER_HIST, 16, kp, p->stream));
 }
 
@@ -259,6 +272,7 @@ int fs_length_set(uint64_t n, const uint32_t *gens, int d, uint64_t *hist_dev, u
   ex.device = -1;
   ex.world = 1;
   ex.gen_order = FS_GENORDER_AUTO;
+  ex.tail = FS_TAIL_CLOSED;
   return fs_length_set_ex(n, gens, d, &ex, hist_dev, hist_cap);
 }
 

@@ -69,6 +69,8 @@ struct Consts {
   uint32_t alpha, beta;  // units per node entry / per row
   uint32_t ktab_len;     // 0: k0 by arithmetic; else words of the node tables (below)
   uint32_t adv_off;      // word offset of the advance table inside ktab (8 B aligned)
+  int32_t dl;            // t - s: change of a row's length from one valid a_{d-1} to the next
+  uint32_t dstride;      // stride of the closed-tail length-difference array (|dl|, or 1 if 0)
   uint8_t perm[FS_MAX_D];  // internal coordinate j is the caller's coordinate perm[j]
   uint32_t permuted;       // perm is not the identity
   const uint64_t *U;     // DP tables, L rows of (n+1) entries
@@ -366,8 +368,12 @@ FS_HD void fast_step(Lane<D> &st, const Consts &c, const KT &kt, uint32_t &budge
 // a*, a*-s, ..., so its rows are counted in O(1) as floor(a*/s) + 1 (one magic division)
 // instead of one step per row.  Node-unit slices only (a slice owns whole nodes), so the
 // slice boundaries are those of fast_step.
-template <int D, class KT>
-FS_HD void fast_step_closed(Lane<D> &st, const Consts &c, const KT &kt, uint32_t &budget, uint32_t &cnt) {
+//
+// Node consumers (NodeEmit::node(em, st, c, rows) receives the whole progression at once):
+// the count adds `rows`; the length histogram adds the progression's lengths
+// l_j = l_0 + j (t - s), j < rows, as two updates of a strided difference array.
+template <int D, class KT, class NodeEmit>
+FS_HD void fast_step_closed(Lane<D> &st, const Consts &c, const KT &kt, uint32_t &budget, NodeEmit &ne) {
   constexpr int L = D - 2;
   if constexpr (L >= 1) {
     const bool fa = st.cur < 0 && st.k != 0;
@@ -381,9 +387,32 @@ FS_HD void fast_step_closed(Lane<D> &st, const Consts &c, const KT &kt, uint32_t
   }
   const bool em = st.cur >= 0;  // node units: the node's rows all belong to this slice
   const uint32_t rows = divq((uint32_t)(em ? st.cur : 0), c.dvS) + 1u;
-  if (em) {
-    cnt += rows;
-    st.cur = -1;
+  ne.node(em, st, c, rows);
+  if (em) st.cur = -1;
+}
+
+struct NodeCount {
+  uint32_t n;
+  template <int D>
+  FS_HD void node(bool em, const Lane<D> &, const Consts &, uint32_t rows) {
+    n += em ? rows : 0u;
+  }
+};
+
+// The two difference-array updates of a node's length progression: +v at lo, -v at hi
+// (hi = lo + rows * dstride).  dl == 0: all rows share one length (v = rows, stride 1).
+template <int D>
+FS_HD void hist_diff_updates(const Lane<D> &st, const Consts &c, uint32_t rows, uint32_t &lo, uint32_t &hi,
+                             uint32_t &v) {
+  const uint32_t l0 = cur_lsum<D>(st) + (uint32_t)st.cur + row_ad<D>(st, c);
+  if (c.dl == 0) {
+    lo = l0;
+    hi = l0 + 1u;
+    v = rows;
+  } else {
+    lo = c.dl > 0 ? l0 : l0 - (rows - 1u) * (uint32_t)(-c.dl);
+    hi = lo + rows * c.dstride;
+    v = 1u;
   }
 }
 

@@ -150,6 +150,8 @@ int fs_validate_and_build(fs_plan *p, uint64_t n, const uint32_t *gens, int d, i
     c.dvB = fs_make_div(c.gB);
     c.dvH = fs_make_div(c.h);
     c.dvS = fs_make_div(c.s);
+    c.dl = (int32_t)c.t - (int32_t)c.s;
+    c.dstride = c.dl == 0 ? 1u : (uint32_t)(c.dl > 0 ? c.dl : -c.dl);
     if (L >= 1) {
       c.delta = gens[L - 1] % c.gA;
       c.q = gens[L - 1] / c.gA;
@@ -249,6 +251,8 @@ void fs_plan_free_device(fs_plan *p) {
   if (p->U_dev) cudaFree(p->U_dev);
   if (p->ktab_dev) cudaFree(p->ktab_dev);
   if (p->scratch_dev) cudaFree(p->scratch_dev);
+  if (p->diff_dev) cudaFree(p->diff_dev);
+  p->diff_dev = nullptr;
   p->U_dev = nullptr;
   p->ktab_dev = nullptr;
   p->scratch_dev = nullptr;
@@ -301,6 +305,8 @@ struct HostSink {
   unsigned char *rows = nullptr;
   uint64_t cap = 0;
   uint64_t slice_rows = 0;
+  std::vector<int64_t> diffv;
+  int64_t *diff = nullptr;
   uint32_t first[FS_MAX_D];
   bool have_first = false;
   void put(const uint32_t *vi) {
@@ -339,6 +345,25 @@ struct HostEmit {
   }
 };
 
+// closed-tail node consumer of the host model: the count, and the length histogram through
+// the same strided difference array the kernels use (resolved by host_finish_diff)
+struct HostNodeSink {
+  const fs_plan *p;
+  HostSink *sink;
+  uint64_t n;
+  template <int D>
+  void node(bool em, const fs::Lane<D> &st, const fs::Consts &c, uint32_t rows) {
+    if (!em) return;
+    n += rows;
+    if (sink->diff) {
+      uint32_t lo, hi, v;
+      fs::hist_diff_updates<D>(st, c, rows, lo, hi, v);
+      sink->diff[lo] += (int64_t)v;
+      sink->diff[hi] -= (int64_t)v;
+    }
+  }
+};
+
 template <int D, int ALPHA, class KT>
 void host_model_d(const fs_plan *p, const KT &ktab, HostSink &sink, uint64_t *slice_counts, uint32_t *slice_first) {
   const Consts &c = p->c;
@@ -353,18 +378,19 @@ void host_model_d(const fs_plan *p, const KT &ktab, HostSink &sink, uint64_t *sl
     sink.have_first = false;
     HostEmit<D> emit{&sink};
     // the kernels' schedule: branch-free fast steps, slow_step() for lanes needing an ascend
-    if (ALPHA && p->consumer == FS_CONSUMER_COUNT && p->ex.tail == FS_TAIL_CLOSED) {
-      uint32_t cnt = 0;
+    if (ALPHA && (p->consumer == FS_CONSUMER_COUNT || p->consumer == FS_CONSUMER_HIST) &&
+        p->ex.tail == FS_TAIL_CLOSED) {
+      HostNodeSink ns{p, &sink, 0};
       while (!fs::needs_refill<D, ALPHA>(st, budget)) {
-        fs::fast_step_closed<D>(st, c, ktab, budget, cnt);
+        fs::fast_step_closed<D>(st, c, ktab, budget, ns);
         fs::sync_k<D, ALPHA>(st, budget);
         if (fs::needs_slow<D>(st, budget)) {
           fs::slow_step<D, true, ALPHA>(st, c, ktab, budget);
           fs::sync_k<D, ALPHA>(st, budget);
         }
       }
-      sink.count += cnt;
-      sink.slice_rows = cnt;
+      sink.count += ns.n;
+      sink.slice_rows = ns.n;
     } else {
       while (!fs::needs_refill<D, ALPHA>(st, budget)) {
         fs::fast_step<D, true, ALPHA>(st, c, ktab, budget, emit);
@@ -414,6 +440,11 @@ extern "C" int fsdbg_host_model(const fs_plan *p, uint64_t *count_out, uint64_t 
   sink.rows = (unsigned char *)rows;
   sink.cap = cap;
   if (hist) memset(hist, 0, hist_cap * 8);
+  const bool closed_hist = hist && p->consumer == FS_CONSUMER_HIST && p->ex.tail == FS_TAIL_CLOSED && p->d >= 2;
+  if (closed_hist) {
+    sink.diffv.assign(p->hist_len + p->c.dstride + 1, 0);
+    sink.diff = sink.diffv.data();
+  }
   if (p->d == 1) {
     // one slice, one unit at most
     for (uint64_t sl = 0; sl < p->num_slices; ++sl) {
@@ -435,6 +466,16 @@ extern "C" int fsdbg_host_model(const fs_plan *p, uint64_t *count_out, uint64_t 
 #undef FS_CASE
       default:
         return FS_EINVAL;
+    }
+  }
+  if (closed_hist) {  // strided prefix sums of the difference array
+    const uint64_t L = p->hist_len, S = p->c.dstride;
+    for (uint64_t r = 0; r < S && r < L; ++r) {
+      int64_t acc = 0;
+      for (uint64_t l = r; l < L; l += S) {
+        acc += sink.diff[l];
+        if (l < hist_cap) hist[l] = (uint64_t)acc;
+      }
     }
   }
   if (count_out) *count_out = sink.count;

@@ -24,6 +24,7 @@ constexpr uint32_t kHistSmemMax = 24576;  // u32 histogram bins kept in shared m
 constexpr int kConsRowsAny = 4;           // internal consumer: materialise, order = any (M2)
 constexpr uint32_t kWarpBuf = 4096;       // M2 per-warp compaction buffer (bytes)
 constexpr int kConsCountClosed = 5;       // internal consumer: count with the closed-form tail
+constexpr int kConsHistClosed = 6;        // internal consumer: histogram with the closed-form tail
 
 // Everything a kernel needs, by value (fits the 4 KB parameter space comfortably).
 struct KParams {
@@ -51,6 +52,10 @@ struct KParams {
   unsigned long long *front;
   unsigned long long *back;
   uint64_t rank_rows;
+  // closed-tail histogram: strided difference array (hist_len + dstride entries, signed
+  // values stored as two's-complement u64), resolved by the finalize kernel
+  unsigned long long *diff_out;
+  uint32_t diff_len;
 };
 
 }  // namespace fs
@@ -78,6 +83,7 @@ struct fs_plan {
   uint64_t *U_dev = nullptr;
   uint32_t *ktab_dev = nullptr;
   unsigned long long *scratch_dev = nullptr;  // [0] queue head, [1..] spare
+  unsigned long long *diff_dev = nullptr;     // closed-tail histogram difference array
   bool uploaded = false;
   uint32_t grid = 0, block = fs::kBlock;
   int last_launches = 0;
@@ -93,4 +99,5 @@ fs::Div fs_make_div(uint32_t g);
 // kernel launchers (fs_kernels.cu); return FS_OK or an error
 int fs_launch(fs_plan *p, int consumer, int B, const fs::KParams &kp_template, cudaStream_t stream);
 int fs_occupancy_grid(fs_plan *p, int consumer, int B, uint32_t *grid_out);
+int fs_launch_hist_finalize(const fs::KParams &kp, cudaStream_t stream);
 extern unsigned long long g_fs_total_launches;

@@ -47,6 +47,32 @@ template <int D>
 struct EmitCount {
   uint32_t n;
   __device__ __forceinline__ void cond(bool em, const Lane<D> &, const Consts &) { n += em ? 1u : 0u; }
+  __device__ __forceinline__ void node(bool em, const Lane<D> &, const Consts &, uint32_t rows) {
+    n += em ? rows : 0u;
+  }
+};
+
+// Closed-tail histogram: a node's lengths form l_0 + j (t - s); two atomics on a strided
+// difference array (shared-memory u32 with wrap-around, or global u64) replace one per row.
+template <int D>
+struct EmitHistClosed {
+  uint32_t *diff;
+  unsigned long long *gdiff;
+  uint32_t smem;
+  uint32_t n;
+  __device__ __forceinline__ void node(bool em, const Lane<D> &st, const Consts &c, uint32_t rows) {
+    if (!em) return;
+    uint32_t lo, hi, v;
+    hist_diff_updates<D>(st, c, rows, lo, hi, v);
+    if (smem) {
+      atomicAdd(&diff[lo], v);
+      atomicAdd(&diff[hi], 0u - v);
+    } else {
+      atomicAdd(&gdiff[lo], (unsigned long long)v);
+      atomicAdd(&gdiff[hi], 0ull - (unsigned long long)v);
+    }
+    n += rows;
+  }
 };
 
 template <int D>
@@ -314,6 +340,7 @@ __device__ __forceinline__ uint64_t bitrev_bits(uint64_t x, uint32_t bits) {
 template <int D, int CONS, int B, bool KTAB>
 __global__ void __launch_bounds__(kBlock) fs_enum_kernel(const KParams P) {
   constexpr bool NEED_AD = CONS != FS_CONSUMER_COUNT && CONS != kConsCountClosed;
+  constexpr bool HISTLIKE = CONS == FS_CONSUMER_HIST || CONS == kConsHistClosed;
   constexpr int ALPHA = (CONS == FS_CONSUMER_ROWS || CONS == kConsRowsAny) ? 0 : 1;
   constexpr int INNER = Inner<CONS>::value;
   // ROWS: a lane completes at most one ring half in kHalf / row_bytes steps, so the warp
@@ -327,11 +354,13 @@ __global__ void __launch_bounds__(kBlock) fs_enum_kernel(const KParams P) {
   uint32_t *ktab_s = reinterpret_cast<uint32_t *>(smem);
   const uint32_t kt_words = (c.ktab_len + 3u) & ~3u;
   uint32_t *hist_s = ktab_s + kt_words;
-  const uint32_t hist_words = (CONS == FS_CONSUMER_HIST && P.hist_smem) ? ((P.hist_len + 3u) & ~3u) : 0u;
+  const uint32_t hist_words =
+      !(HISTLIKE && P.hist_smem) ? 0u
+      : ((CONS == kConsHistClosed ? P.diff_len : P.hist_len) + 3u) & ~3u;
   unsigned char *stage = reinterpret_cast<unsigned char *>(hist_s + hist_words);
 
   for (uint32_t i = threadIdx.x; i < c.ktab_len; i += blockDim.x) ktab_s[i] = c.ktab[i];
-  if (CONS == FS_CONSUMER_HIST) {
+  if (HISTLIKE) {
     for (uint32_t i = threadIdx.x; i < hist_words; i += blockDim.x) hist_s[i] = 0u;
     if (threadIdx.x == 0) hist_guard = 0u;
   }
@@ -362,6 +391,7 @@ __global__ void __launch_bounds__(kBlock) fs_enum_kernel(const KParams P) {
 
   EmitCount<D> e_count{0};
   EmitHist<D> e_hist{hist_s, P.hist_out, P.hist_smem, 0};
+  EmitHistClosed<D> e_hcl{hist_s, P.diff_out, P.hist_smem, 0};
   EmitAny<D> e_any{P.pred, P.pred_arg, P.found, P.witness, false};
   EmitRows<D, B> e_rows;
   e_rows.buf = stage + threadIdx.x * kLaneStride;
@@ -387,16 +417,25 @@ __global__ void __launch_bounds__(kBlock) fs_enum_kernel(const KParams P) {
         if (CONS == FS_CONSUMER_COUNT || CONS == kConsCountClosed) {
           acc += e_count.n;
           e_count.n = 0;
-        } else if (CONS == FS_CONSUMER_HIST) {
-          const uint32_t rows = e_hist.n;
+        } else if (HISTLIKE) {
+          const uint32_t rows = CONS == kConsHistClosed ? e_hcl.n : e_hist.n;
           e_hist.n = 0;
+          e_hcl.n = 0;
           if (P.hist_smem && rows) {
-            // overflow guard: every 2^30 rows added to this CTA, drain the u32 bins
+            // overflow guard: every 2^30 rows added to this CTA, drain the u32 bins (or the
+            // difference array, as sign-extended values) to global memory
             const uint32_t old = atomicAdd(&hist_guard, rows);
             if ((old >> 30) != ((old + rows) >> 30)) {
-              for (uint32_t i = 0; i < P.hist_len; ++i) {
-                const uint32_t v = atomicExch(&hist_s[i], 0u);
-                if (v) atomicAdd(&P.hist_out[i], (unsigned long long)v);
+              if (CONS == kConsHistClosed) {
+                for (uint32_t i = 0; i < P.diff_len; ++i) {
+                  const int32_t v = (int32_t)atomicExch(&hist_s[i], 0u);
+                  if (v) atomicAdd(&P.diff_out[i], (unsigned long long)(long long)v);
+                }
+              } else {
+                for (uint32_t i = 0; i < P.hist_len; ++i) {
+                  const uint32_t v = atomicExch(&hist_s[i], 0u);
+                  if (v) atomicAdd(&P.hist_out[i], (unsigned long long)v);
+                }
               }
             }
           }
@@ -447,7 +486,9 @@ __global__ void __launch_bounds__(kBlock) fs_enum_kernel(const KParams P) {
         if (CONS == FS_CONSUMER_COUNT) {
           fast_step<D, NEED_AD, ALPHA>(st, c, kt, budget, e_count);
         } else if (CONS == kConsCountClosed) {
-          fast_step_closed<D>(st, c, kt, budget, e_count.n);
+          fast_step_closed<D>(st, c, kt, budget, e_count);
+        } else if (CONS == kConsHistClosed) {
+          fast_step_closed<D>(st, c, kt, budget, e_hcl);
         } else if (CONS == FS_CONSUMER_HIST) {
           fast_step<D, NEED_AD, ALPHA>(st, c, kt, budget, e_hist);
         } else if (CONS == FS_CONSUMER_ANY) {
@@ -502,6 +543,13 @@ __global__ void __launch_bounds__(kBlock) fs_enum_kernel(const KParams P) {
       if (v) atomicAdd(&P.hist_out[i], (unsigned long long)v);
     }
   }
+  if (CONS == kConsHistClosed && P.hist_smem) {
+    __syncthreads();
+    for (uint32_t i = threadIdx.x; i < P.diff_len; i += blockDim.x) {
+      const int32_t v = (int32_t)hist_s[i];
+      if (v) atomicAdd(&P.diff_out[i], (unsigned long long)(long long)v);
+    }
+  }
 }
 
 // d = 1: Z(n,(g)) = {(n/g)} iff g | n.  One thread; the rank owning unit 0 emits it.
@@ -511,7 +559,7 @@ __global__ void fs_d1_kernel(const KParams P) {
   if (!(P.unit0 == 0 && P.unit1 > 0)) return;
   const uint32_t x = P.c.n / P.c.g[0];
   if (CONS == FS_CONSUMER_COUNT || CONS == kConsCountClosed) atomicAdd(P.count_out, 1ull);
-  if (CONS == FS_CONSUMER_HIST) atomicAdd(&P.hist_out[x], 1ull);
+  if (CONS == FS_CONSUMER_HIST || CONS == kConsHistClosed) atomicAdd(&P.hist_out[x], 1ull);
   if (CONS == FS_CONSUMER_ANY) {
     bool ok;
     switch (P.pred) {
@@ -531,9 +579,22 @@ __global__ void fs_d1_kernel(const KParams P) {
   }
 }
 
+// Closed-tail histogram: hist[l] = sum of diff[k] over k <= l, k = l mod dstride.
+static __global__ void fs_hist_finalize_kernel(const unsigned long long *diff, unsigned long long *hist, uint32_t hist_len,
+                                        uint32_t dstride) {
+  for (uint32_t r = blockIdx.x * blockDim.x + threadIdx.x; r < dstride && r < hist_len; r += gridDim.x * blockDim.x) {
+    unsigned long long acc = 0;
+    for (uint32_t l = r; l < hist_len; l += dstride) {
+      acc += diff[l];
+      hist[l] = acc;
+    }
+  }
+}
+
 static size_t smem_bytes(const KParams &kp, int consumer) {
   size_t b = (size_t)((kp.c.ktab_len + 3u) & ~3u) * 4;
   if (consumer == FS_CONSUMER_HIST && kp.hist_smem) b += (size_t)((kp.hist_len + 3u) & ~3u) * 4;
+  if (consumer == kConsHistClosed && kp.hist_smem) b += (size_t)((kp.diff_len + 3u) & ~3u) * 4;
   if (consumer == FS_CONSUMER_ROWS) b += (size_t)kBlock * kLaneStride;
   if (consumer == kConsRowsAny) b += (size_t)(kBlock / 32) * kWarpBuf;
   return b;

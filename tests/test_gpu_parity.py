@@ -97,6 +97,19 @@ def test_count_closed_tail(oracle_mod, inst):
 
 
 @pytest.mark.parametrize("inst", ALL, ids=ids)
+def test_hist_closed_tail(oracle_mod, inst):
+    n, g = inst.n, inst.gens
+    want = oracle.hist(n, g)
+    for go in (L.FS_GENORDER_GIVEN, L.FS_GENORDER_AUTO):
+        for T in (0, 1, 5):
+            h = api.fs_length_set_ex(n, g, slice_units=T, gen_order=go, tail=L.FS_TAIL_CLOSED)
+            assert hist_list(h, len(want)) == want
+    hs = [api.fs_length_set_ex(n, g, rank=r, world=3, tail=L.FS_TAIL_CLOSED, gen_order=L.FS_GENORDER_AUTO)
+          for r in range(3)]
+    assert hist_list(sum(hs), len(want)) == want
+
+
+@pytest.mark.parametrize("inst", ALL, ids=ids)
 def test_generator_order_auto(oracle_mod, inst):
     """NEXT-2 (stream over the largest generators first): same count / histogram / any, rows in
     the caller's coordinates (M2 layout), witnesses and COORD_GE indices in caller order."""
@@ -225,8 +238,12 @@ def test_c3_count_full():
 
 
 def test_c4_hist_full():
-    h = api.fs_length_set(W.C4.n, W.C4.gens)
+    h = api.fs_length_set(W.C4.n, W.C4.gens)  # default: generator order auto, closed tail
     assert hist_list(h, 329) == gold("C3")["hist"]
+    for go in (0, 1):
+        for tail in (0, 1):
+            h = api.fs_length_set_ex(W.C4.n, W.C4.gens, gen_order=go, tail=tail)
+            assert hist_list(h, 329) == gold("C3")["hist"], (go, tail)
 
 
 @pytest.mark.parametrize("world", [2, 8])

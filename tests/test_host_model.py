@@ -78,6 +78,18 @@ def test_closed_tail_count(oracle_mod, inst):
 
 
 @pytest.mark.parametrize("inst", INSTANCES, ids=lambda i: "%s" % i.name)
+def test_closed_tail_hist(oracle_mod, inst):
+    """Closed-tail histogram: strided difference array of each node's length progression."""
+    n, g = inst.n, inst.gens
+    want = oracle.hist(n, g)
+    for go in (0, 1):
+        for T in (0, 1, 5):
+            r = host_model(n, g, L.FS_CONSUMER_HIST, slice_units=T, want_hist=True, tail=L.FS_TAIL_CLOSED,
+                           gen_order=go)
+            assert r["hist"] == want
+
+
+@pytest.mark.parametrize("inst", INSTANCES, ids=lambda i: "%s" % i.name)
 def test_generator_order_auto(oracle_mod, inst):
     """NEXT-2: the stream over a permutation of the generators gives the same count and
     histogram, and the same multiset of rows in the caller's coordinates."""
