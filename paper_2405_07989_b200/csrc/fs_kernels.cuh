@@ -282,17 +282,22 @@ struct EmitCompact {
 };
 
 // Warp-cooperative copy of every lane's pending staging segment (a multiple of 16 B, at most
-// 2 kHalf): 8 segments per round, 4 lanes per segment, 16 B per lane per iteration.
+// 2 kHalf): 8 segments per round, 4 lanes per segment, 16 B per lane per iteration.  Pending
+// lanes publish their lane id at their rank in a per-warp slot table, so consumer lanes find
+// the segment they copy with one shared-memory load.
 __device__ __forceinline__ void warp_flush(bool &pend, uint32_t soff, uint64_t goff, uint32_t len,
-                                           const unsigned char *warp_stage, unsigned char *out) {
-  unsigned pm = __ballot_sync(kFull, pend);
+                                           const unsigned char *warp_stage, unsigned char *out,
+                                           unsigned char *slot) {
+  const unsigned pm = __ballot_sync(kFull, pend);
   if (!pm) return;
   constexpr int kLanesPerSeg = 4, kSegs = 32 / kLanesPerSeg;
   const int lane = threadIdx.x & 31, sub = lane / kLanesPerSeg, j = lane % kLanesPerSeg;
-  while (pm) {
-    unsigned m = pm;
-    for (int x = 0; x < sub && m; ++x) m &= m - 1;
-    const int src = m ? (__ffs(m) - 1) : -1;
+  if (pend) slot[__popc(pm & lanemask_lt())] = (unsigned char)lane;
+  __syncwarp();
+  const int npend = __popc(pm);
+  for (int base = 0; base < npend; base += kSegs) {
+    const int seg = base + sub;
+    const int src = seg < npend ? (int)slot[seg] : -1;
     const int sl = src < 0 ? 0 : src;
     const uint32_t s_soff = __shfl_sync(kFull, soff, sl);
     const uint32_t s_len = __shfl_sync(kFull, len, sl);
@@ -308,9 +313,8 @@ __device__ __forceinline__ void warp_flush(bool &pend, uint32_t soff, uint64_t g
         __stcs(reinterpret_cast<uint4 *>(out + s_goff + o), v);
       }
     }
-#pragma unroll
-    for (int x = 0; x < kSegs; ++x) pm &= pm ? pm - 1 : 0u;
   }
+  __syncwarp();
   pend = false;
 }
 
@@ -404,6 +408,8 @@ __global__ void __launch_bounds__(kBlock) fs_enum_kernel(const KParams P) {
   uint32_t fin_soff = 0, fin_len = 0;
   uint64_t fin_goff = 0;
   const unsigned char *warp_stage = stage + (threadIdx.x & ~31) * kLaneStride;
+  // per-warp slot table of the M1 flush, after the staging buffers
+  unsigned char *wslot = stage + kBlock * kLaneStride + (threadIdx.x >> 5) * 32;
   EmitCompact<D, B> e_cmp;
   e_cmp.buf = stage + (threadIdx.x >> 5) * kWarpBuf;
   e_cmp.wrows = 0;
@@ -502,8 +508,8 @@ __global__ void __launch_bounds__(kBlock) fs_enum_kernel(const KParams P) {
       }
       if (CONS == FS_CONSUMER_ROWS) {
         if (had && budget == 0) rows_slice_done(P, e_rows, fin, fin_soff, fin_goff, fin_len);
-        warp_flush(e_rows.pend, e_rows.pend_soff, e_rows.pend_goff, e_rows.pend_len, warp_stage, P.rows_out);
-        warp_flush(fin, fin_soff, fin_goff, fin_len, warp_stage, P.rows_out);
+        warp_flush(e_rows.pend, e_rows.pend_soff, e_rows.pend_goff, e_rows.pend_len, warp_stage, P.rows_out, wslot);
+        warp_flush(fin, fin_soff, fin_goff, fin_len, warp_stage, P.rows_out, wslot);
         e_rows.rebase();
       }
       sync_k<D, ALPHA>(st, budget);
@@ -515,8 +521,8 @@ __global__ void __launch_bounds__(kBlock) fs_enum_kernel(const KParams P) {
           if (CONS == FS_CONSUMER_ROWS && budget == 0) rows_slice_done(P, e_rows, fin, fin_soff, fin_goff, fin_len);
         }
         if (CONS == FS_CONSUMER_ROWS) {
-          warp_flush(e_rows.pend, e_rows.pend_soff, e_rows.pend_goff, e_rows.pend_len, warp_stage, P.rows_out);
-          warp_flush(fin, fin_soff, fin_goff, fin_len, warp_stage, P.rows_out);
+          warp_flush(e_rows.pend, e_rows.pend_soff, e_rows.pend_goff, e_rows.pend_len, warp_stage, P.rows_out, wslot);
+          warp_flush(fin, fin_soff, fin_goff, fin_len, warp_stage, P.rows_out, wslot);
         }
       }
       if (CONS == FS_CONSUMER_ANY && e_any.hit) {
@@ -595,7 +601,7 @@ static size_t smem_bytes(const KParams &kp, int consumer) {
   size_t b = (size_t)((kp.c.ktab_len + 3u) & ~3u) * 4;
   if (consumer == FS_CONSUMER_HIST && kp.hist_smem) b += (size_t)((kp.hist_len + 3u) & ~3u) * 4;
   if (consumer == kConsHistClosed && kp.hist_smem) b += (size_t)((kp.diff_len + 3u) & ~3u) * 4;
-  if (consumer == FS_CONSUMER_ROWS) b += (size_t)kBlock * kLaneStride;
+  if (consumer == FS_CONSUMER_ROWS) b += (size_t)kBlock * kLaneStride + (kBlock / 32) * 32;
   if (consumer == kConsRowsAny) b += (size_t)(kBlock / 32) * kWarpBuf;
   return b;
 }
