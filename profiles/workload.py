@@ -25,9 +25,10 @@ def main():
                      gen_order=1 if "auto" in name else 0)
         out = torch.zeros(1, dtype=torch.int64, device="cuda")
         fn = lambda: p.count_async(out)
-    elif name == "c4hist":
+    elif name in ("c4hist", "c4histclosed"):
         inst = W.C4
-        p = api.Plan(inst.n, inst.gens, L.FS_CONSUMER_HIST)
+        p = api.Plan(inst.n, inst.gens, L.FS_CONSUMER_HIST, tail=1 if "closed" in name else 0,
+                     gen_order=1 if "closed" in name else 0)
         out = torch.zeros(api.hist_len(inst.n, inst.gens), dtype=torch.int64, device="cuda")
         fn = lambda: p.hist_async(out)
     elif name == "c5any_none":
