@@ -74,11 +74,13 @@ struct Consts {
   uint8_t perm[FS_MAX_D];  // internal coordinate j is the caller's coordinate perm[j]
   uint32_t permuted;       // perm is not the identity
   const uint64_t *U;     // DP tables, L rows of (n+1) entries
-  // node tables (device or host), for rho in [0, g_{d-1}):
+  // node tables (device or host), for rho in [0, g_{d-1}) (g_{d-1} <= 2048):
   //   ktab[rho]                     = k0(rho)
-  //   ktab[adv_off + 2 rho]         = next(rho) | carry(rho) << 31, next = (rho + delta) mod g_{d-1}
+  //   ktab[adv_off + 2 rho]         = next(rho) | (q + carry(rho)) << 11,
+  //                                   next = (rho + delta) mod g_{d-1}
   //   ktab[adv_off + 2 rho + 1]     = k0(next(rho))
-  // i.e. one 8 B load performs a node advance's residue update and the new node's entry.
+  // i.e. one 8 B load performs a node advance's residue and quotient update and the new
+  // node's entry.
   const uint32_t *ktab;
 };
 
@@ -154,13 +156,20 @@ FS_HD void sync_k(Lane<D> &st, uint32_t &budget) {
 // k0 of the next residue) -- from the tables (host vector, or a shared-memory copy on the
 // device), or by arithmetic when g_{d-1} is too large for a table.
 struct Adv {
-  uint32_t x, y;  // x = next | carry << 31, y = k0(next)
+  uint32_t next, k0, inc;  // next residue, k0(next), increment of floor(R_L / g_{d-1})
 };
+constexpr uint32_t kAdvBits = 11;  // next < 2^11 in the packed table word
+FS_HD uint32_t adv_pack(uint32_t next, uint32_t inc) { return next | (inc << kAdvBits); }
+FS_HD Adv adv_unpack(uint32_t w0, uint32_t w1) {
+  return Adv{w0 & ((1u << kAdvBits) - 1u), w1, w0 >> kAdvBits};
+}
 struct KTabPtr {
   const uint32_t *p;
   uint32_t adv_off;
   FS_HD uint32_t operator()(uint32_t rho, const Consts &) const { return p[rho]; }
-  FS_HD Adv step(uint32_t rho, const Consts &) const { return Adv{p[adv_off + 2 * rho], p[adv_off + 2 * rho + 1]}; }
+  FS_HD Adv step(uint32_t rho, const Consts &) const {
+    return adv_unpack(p[adv_off + 2 * rho], p[adv_off + 2 * rho + 1]);
+  }
 };
 struct KTabArith {
   FS_HD uint32_t operator()(uint32_t rho, const Consts &c) const { return k0_arith(rho, c); }
@@ -168,7 +177,7 @@ struct KTabArith {
     uint32_t r2 = rho + c.delta;
     const uint32_t cy = r2 >= c.gA ? 1u : 0u;
     r2 -= cy ? c.gA : 0u;
-    return Adv{r2 | (cy << 31), k0_arith(r2, c)};
+    return Adv{r2, k0_arith(r2, c), c.q + cy};
   }
 };
 
@@ -349,9 +358,9 @@ FS_HD void fast_step(Lane<D> &st, const Consts &c, const KT &kt, uint32_t &budge
     const Adv w = kt.step(st.rho, c);
     if (fa) {  // advance (a_L -= 1, R_L += g_L, lazily via k) and entry of the new node
       st.k -= 1u;
-      st.rho = w.x & 0x7fffffffu;
-      st.A += c.q + (w.x >> 31);
-      st.cur = (int32_t)st.A - (int32_t)w.y;
+      st.rho = w.next;
+      st.A += w.inc;
+      st.cur = (int32_t)st.A - (int32_t)w.k0;
     }
   }
   // node units: every row of an entered node belongs to the slice; row units: budget-limited
@@ -380,9 +389,9 @@ FS_HD void fast_step_closed(Lane<D> &st, const Consts &c, const KT &kt, uint32_t
     const Adv w = kt.step(st.rho, c);
     if (fa) {
       st.k -= 1u;
-      st.rho = w.x & 0x7fffffffu;
-      st.A += c.q + (w.x >> 31);
-      st.cur = (int32_t)st.A - (int32_t)w.y;
+      st.rho = w.next;
+      st.A += w.inc;
+      st.cur = (int32_t)st.A - (int32_t)w.k0;
     }
   }
   const bool em = st.cur >= 0;  // node units: the node's rows all belong to this slice

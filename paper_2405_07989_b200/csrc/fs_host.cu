@@ -156,7 +156,7 @@ int fs_validate_and_build(fs_plan *p, uint64_t n, const uint32_t *gens, int d, i
       c.delta = gens[L - 1] % c.gA;
       c.q = gens[L - 1] / c.gA;
     }
-    if (c.gA <= fs::kKtabMax && (c.s < (1u << 31))) {
+    if (c.gA <= fs::kKtabMax && (c.s < (1u << 31)) && c.q + 1u < (1u << (32 - fs::kAdvBits))) {
       // node tables: k0(rho), then the advance transitions (8 B aligned), computed with the
       // same arithmetic the table-less kernels use
       const uint32_t adv_off = (c.gA + 1u) & ~1u;
@@ -166,8 +166,8 @@ int fs_validate_and_build(fs_plan *p, uint64_t n, const uint32_t *gens, int d, i
       for (uint32_t rho = 0; rho < c.gA; ++rho) {
         p->ktab[rho] = fs::k0_arith(rho, c);
         const fs::Adv w = ar.step(rho, c);
-        p->ktab[adv_off + 2 * rho] = w.x;
-        p->ktab[adv_off + 2 * rho + 1] = w.y;
+        p->ktab[adv_off + 2 * rho] = fs::adv_pack(w.next, w.inc);
+        p->ktab[adv_off + 2 * rho + 1] = w.k0;
       }
       c.ktab_len = (uint32_t)p->ktab.size();
       c.adv_off = adv_off;

@@ -29,9 +29,9 @@ struct KTabSmem {
     return v;
   }
   __device__ __forceinline__ Adv step(uint32_t rho, const Consts &) const {
-    Adv w;
-    asm("ld.shared.v2.u32 {%0, %1}, [%2];" : "=r"(w.x), "=r"(w.y) : "r"(adv + rho * 8u));
-    return w;
+    uint32_t w0, w1;
+    asm("ld.shared.v2.u32 {%0, %1}, [%2];" : "=r"(w0), "=r"(w1) : "r"(adv + rho * 8u));
+    return adv_unpack(w0, w1);
   }
 };
 
@@ -350,7 +350,7 @@ __global__ void __launch_bounds__(kBlock) fs_enum_kernel(const KParams P) {
   // ROWS: a lane completes at most one ring half in kHalf / row_bytes steps, so the warp
   // flushes pending halves once per that many steps.
   constexpr int kRowsPerHalf = (int)(kHalf / (D * (B / 8))) > 0 ? (int)(kHalf / (D * (B / 8))) : 1;
-  constexpr int UNROLL = CONS == FS_CONSUMER_ROWS ? kRowsPerHalf : 4;
+  constexpr int UNROLL = CONS == FS_CONSUMER_ROWS ? kRowsPerHalf : (CONS == kConsCountClosed ? 8 : 4);
   extern __shared__ __align__(16) unsigned char smem[];
   __shared__ unsigned int hist_guard;
   const Consts &c = P.c;
