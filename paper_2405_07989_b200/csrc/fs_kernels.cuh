@@ -244,9 +244,9 @@ struct EmitCompact {
     }
     wrows += (uint32_t)__popc(m);
   }
-  // converged; flush 8k rows when the buffer cannot take another full warp of rows
-  __device__ __forceinline__ void flush(const KParams &P, bool final) {
-    if (!final && wrows + 32 <= kCap) return;
+  // converged; flush 8k rows when the buffer cannot take `room` more rows
+  __device__ __forceinline__ void flush(const KParams &P, bool final, uint32_t room = 32) {
+    if (!final && wrows + room <= kCap) return;
     const uint32_t k = wrows & ~7u;
     if (k == 0) return;
     __syncwarp();
@@ -501,11 +501,13 @@ __global__ void __launch_bounds__(kBlock) fs_enum_kernel(const KParams P) {
           fast_step<D, NEED_AD, ALPHA>(st, c, kt, budget, e_any);
         } else if (CONS == kConsRowsAny) {
           fast_step<D, NEED_AD, ALPHA>(st, c, kt, budget, e_cmp);
-          e_cmp.flush(P, false);
+          // per-step check only when the warp buffer cannot hold a whole group of rows
+          if (EmitCompact<D, B>::kCap < 32u * UNROLL + 8u) e_cmp.flush(P, false);
         } else {
           fast_step<D, NEED_AD, ALPHA>(st, c, kt, budget, e_rows);
         }
       }
+      if (CONS == kConsRowsAny && EmitCompact<D, B>::kCap >= 32u * UNROLL + 8u) e_cmp.flush(P, false, 32u * UNROLL);
       if (CONS == FS_CONSUMER_ROWS) {
         if (had && budget == 0) rows_slice_done(P, e_rows, fin, fin_soff, fin_goff, fin_len);
         warp_flush(e_rows.pend, e_rows.pend_soff, e_rows.pend_goff, e_rows.pend_len, warp_stage, P.rows_out, wslot);
