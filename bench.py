@@ -188,6 +188,12 @@ def oracle_sample(inst, seconds: float, seed: int = 0):
     return (num / den if den else 0.0), rows_tot, secs_tot, boxes
 
 
+def base_config(inst, total: int) -> dict:
+    """The workload keys both arms report (fsgpu and --impl reference)."""
+    return {"workload": "%s: Z(%d, %s) count, |Z| = %d" % (inst.name, inst.n, list(inst.gens), total),
+            "instance": inst.name, "n": inst.n, "gens": list(inst.gens), "consumer": "count"}
+
+
 def run_reference(args, inst):
     rank = int(os.environ.get("RANK", "0"))
     if rank != 0:
@@ -207,7 +213,7 @@ def run_reference(args, inst):
         "impl": "reference", "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": args.gpus,
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1000.0 * tot_s / args.steps,
         "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "u64",
-        "data": "synthetic", "config": {"workload": args.workload, "n": inst.n, "gens": list(inst.gens)},
+        "data": "synthetic", "config": base_config(inst, __import__("oracle").gf.count(inst.n, inst.gens)),
         "cpu_baseline": {"value": value, "unit": UNIT, "cores": 1, "kind": "oracle",
                          "sample": "work-weighted prefix boxes of %s, seeds 100..%d, %.0f s per step, "
                                    "%d rows total, ratio estimator" % (inst.name, 99 + args.steps, per_step,
@@ -340,8 +346,7 @@ def main():
         "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
         "warmup": args.warmup, "ms_per_step": ms_step, "higher_is_better": True, "scaling": "strong",
         "vs_baseline": None, "dtype": "u32", "data": "synthetic",
-        "config": {"workload": "%s: Z(%d, %s) count, |Z| = %d" % (inst.name, inst.n, list(inst.gens), total),
-                   "instance": inst.name, "n": inst.n, "gens": list(inst.gens), "consumer": "count",
+        "config": {**base_config(inst, total),
                    "method": "Alg. 3.1 stream over the generators largest-first (gen_order=auto, NEXT-2), "
                              "modulo skip at run entry, closed-form row count per node (tail=closed, NEXT-1)",
                    "nodes": info["nodes_per_level"][-1],
