@@ -94,6 +94,9 @@ enum {
  *               factorization of a node (one modulo-skip step per row); FS_TAIL_CLOSED (1)
  *               counts a node's rows in O(1) as floor(a* / s) + 1 (the
  *               closed form of the paper's suffix-set idea).  Same result.
+ *               Count-only ablations of PAPER.md Alg. 3.1's index-(d-1) loop (SURVEY 8(a)
+ *               A6, E2): FS_TAIL_SKIP_OFF (2) visits every candidate a_{d-1} and tests it;
+ *               FS_TAIL_SKIP_PAPER (3) adds the paper's modulo jump after a valid candidate.
  *   gen_order   FS_GENORDER_GIVEN (0, default) runs the stream over the generators in the
  *               caller's order; FS_GENORDER_AUTO (1) lets count / hist / any and order=any
  *               materialise run it over a permutation that minimises the number of nodes
@@ -115,7 +118,7 @@ typedef struct {
 } fs_exec_t;
 
 enum { FS_ORDER_CANONICAL = 0, FS_ORDER_ANY = 1 };
-enum { FS_TAIL_ROWS = 0, FS_TAIL_CLOSED = 1 };
+enum { FS_TAIL_ROWS = 0, FS_TAIL_CLOSED = 1, FS_TAIL_SKIP_OFF = 2, FS_TAIL_SKIP_PAPER = 3 };
 enum { FS_GENORDER_GIVEN = 0, FS_GENORDER_AUTO = 1 };
 
 /* ---------------------------------------------------------------------------------

@@ -143,7 +143,10 @@ int fs_plan_count_async(fs_plan *p, uint64_t *count_dev) {
   if (cudaMemsetAsync(count_dev, 0, 8, p->stream) != cudaSuccess) return FS_ECUDA;
   fs::KParams kp = base_params(p);
   kp.count_out = reinterpret_cast<unsigned long long *>(count_dev);
-  const int cons = p->ex.tail == FS_TAIL_CLOSED ? fs::kConsCountClosed : FS_CONSUMER_COUNT;
+  const int cons = p->ex.tail == FS_TAIL_CLOSED       ? fs::kConsCountClosed
+                   : p->ex.tail == FS_TAIL_SKIP_OFF   ? fs::kConsCountSkipOff
+                   : p->ex.tail == FS_TAIL_SKIP_PAPER ? fs::kConsCountSkipPaper
+                                                      : FS_CONSUMER_COUNT;
   return finish(p, fs_launch(p, cons, 16, kp, p->stream));
 }
 

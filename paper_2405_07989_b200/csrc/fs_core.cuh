@@ -66,6 +66,7 @@ struct Consts {
   uint32_t h, s, t, inv; // h = gcd(gA,gB), s = gB/h, t = gA/h, inv = t^{-1} mod s
   Div dvA, dvB, dvH, dvS;
   uint32_t delta, q;     // g_L mod gA, g_L / gA (L >= 1)
+  uint32_t cB;           // gA mod gB (skip ablation: residue step of one a_{d-1} decrement)
   uint32_t alpha, beta;  // units per node entry / per row
   uint32_t ktab_len;     // 0: k0 by arithmetic; else words of the node tables (below)
   uint32_t adv_off;      // word offset of the advance table inside ktab (8 B aligned)
@@ -113,6 +114,7 @@ struct Lane {
   // min(budget, a_L)); kb = its value at the last sync.  Between syncs, a_L, lsum and (node
   // units) the budget are behind by (kb - k); see sync_k / cur_aL / cur_lsum.
   uint32_t k, kb;
+  uint32_t e;      // skip ablation only: (R_L - a_{d-1} g_{d-1}) mod g_d of the current candidate
 };
 
 template <int D>
@@ -423,6 +425,45 @@ FS_HD void hist_diff_updates(const Lane<D> &st, const Consts &c, uint32_t rows, 
     hi = lo + rows * c.dstride;
     v = 1u;
   }
+}
+
+// Skip ablation: the paper's literal index-(d-1) loop.  A node's
+// candidates a_{d-1} = A, A-1, ..., 0 are visited one per step and tested by the residue
+// e = (R_L - a_{d-1} g_{d-1}) mod g_d (Skip=off); with PAPER, a valid candidate is followed
+// by a jump of s (the paper's modulo optimisation; single steps once a_{d-1} < s,
+// SURVEY 8c #9).  Count consumer, node units; same slices and result as the other tails.
+template <int D>
+FS_HD void enter_candidates(Lane<D> &st, const Consts &c) {
+  st.cur = (int32_t)st.A;
+  st.e = st.rho - divq(st.rho, c.dvB) * c.gB;
+}
+
+template <int D, bool PAPER, class KT>
+FS_HD void fast_step_cand(Lane<D> &st, const Consts &c, const KT &kt, uint32_t &budget, uint32_t &cnt) {
+  constexpr int L = D - 2;
+  if constexpr (L >= 1) {
+    const bool fa = st.cur < 0 && st.k != 0;
+    const Adv w = kt.step(st.rho, c);
+    if (fa) {
+      st.k -= 1u;
+      st.rho = w.next;
+      st.A += w.inc;
+      st.cur = (int32_t)st.A;
+      st.e = w.next - divq(w.next, c.dvB) * c.gB;
+    }
+  }
+  if (st.cur >= 0) {
+    const bool valid = st.e == 0;
+    cnt += valid ? 1u : 0u;
+    if (PAPER && valid && st.cur >= (int32_t)c.s) {
+      st.cur -= (int32_t)c.s;  // the next candidate is valid again
+    } else {
+      st.cur -= 1;
+      const uint32_t e2 = st.e + c.cB;
+      st.e = e2 >= c.gB ? e2 - c.gB : e2;
+    }
+  }
+  (void)budget;
 }
 
 // (called after sync_k)

@@ -150,6 +150,7 @@ int fs_validate_and_build(fs_plan *p, uint64_t n, const uint32_t *gens, int d, i
     c.dvB = fs_make_div(c.gB);
     c.dvH = fs_make_div(c.h);
     c.dvS = fs_make_div(c.s);
+    c.cB = c.gA % c.gB;
     c.dl = (int32_t)c.t - (int32_t)c.s;
     c.dstride = c.dl == 0 ? 1u : (uint32_t)(c.dl > 0 ? c.dl : -c.dl);
     if (L >= 1) {
@@ -378,8 +379,27 @@ void host_model_d(const fs_plan *p, const KT &ktab, HostSink &sink, uint64_t *sl
     sink.have_first = false;
     HostEmit<D> emit{&sink};
     // the kernels' schedule: branch-free fast steps, slow_step() for lanes needing an ascend
-    if (ALPHA && (p->consumer == FS_CONSUMER_COUNT || p->consumer == FS_CONSUMER_HIST) &&
-        p->ex.tail == FS_TAIL_CLOSED) {
+    if (ALPHA && p->consumer == FS_CONSUMER_COUNT &&
+        (p->ex.tail == FS_TAIL_SKIP_OFF || p->ex.tail == FS_TAIL_SKIP_PAPER)) {
+      const bool paper = p->ex.tail == FS_TAIL_SKIP_PAPER;
+      uint32_t cnt = 0;
+      fs::enter_candidates<D>(st, c);
+      while (!fs::needs_refill<D, ALPHA>(st, budget)) {
+        if (paper)
+          fs::fast_step_cand<D, true>(st, c, ktab, budget, cnt);
+        else
+          fs::fast_step_cand<D, false>(st, c, ktab, budget, cnt);
+        fs::sync_k<D, ALPHA>(st, budget);
+        if (fs::needs_slow<D>(st, budget)) {
+          fs::slow_step<D, true, ALPHA>(st, c, ktab, budget);
+          fs::enter_candidates<D>(st, c);
+          fs::sync_k<D, ALPHA>(st, budget);
+        }
+      }
+      sink.count += cnt;
+      sink.slice_rows = cnt;
+    } else if (ALPHA && (p->consumer == FS_CONSUMER_COUNT || p->consumer == FS_CONSUMER_HIST) &&
+               p->ex.tail == FS_TAIL_CLOSED) {
       HostNodeSink ns{p, &sink, 0};
       while (!fs::needs_refill<D, ALPHA>(st, budget)) {
         fs::fast_step_closed<D>(st, c, ktab, budget, ns);

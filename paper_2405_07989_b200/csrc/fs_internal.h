@@ -25,6 +25,8 @@ constexpr int kConsRowsAny = 4;           // internal consumer: materialise, ord
 constexpr uint32_t kWarpBuf = 4096;       // M2 per-warp compaction buffer (bytes)
 constexpr int kConsCountClosed = 5;       // internal consumer: count with the closed-form tail
 constexpr int kConsHistClosed = 6;        // internal consumer: histogram with the closed-form tail
+constexpr int kConsCountSkipOff = 7;      // internal consumer: count, Skip=off ablation
+constexpr int kConsCountSkipPaper = 8;    // internal consumer: count, Skip=paper ablation
 
 // Everything a kernel needs, by value (fits the 4 KB parameter space comfortably).
 struct KParams {

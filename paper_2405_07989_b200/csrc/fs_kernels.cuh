@@ -338,7 +338,9 @@ __device__ __forceinline__ uint64_t bitrev_bits(uint64_t x, uint32_t bits) {
 
 template <int D, int CONS, int B, bool KTAB>
 __global__ void __launch_bounds__(kBlock) fs_enum_kernel(const KParams P) {
-  constexpr bool NEED_AD = CONS != FS_CONSUMER_COUNT && CONS != kConsCountClosed;
+  constexpr bool CAND = CONS == kConsCountSkipOff || CONS == kConsCountSkipPaper;
+  constexpr bool COUNTLIKE = CONS == FS_CONSUMER_COUNT || CONS == kConsCountClosed || CAND;
+  constexpr bool NEED_AD = !COUNTLIKE;
   constexpr bool HISTLIKE = CONS == FS_CONSUMER_HIST || CONS == kConsHistClosed;
   constexpr int ALPHA = (CONS == FS_CONSUMER_ROWS || CONS == kConsRowsAny) ? 0 : 1;
   constexpr int INNER = Inner<CONS>::value;
@@ -415,7 +417,7 @@ __global__ void __launch_bounds__(kBlock) fs_enum_kernel(const KParams P) {
     const unsigned needm = __ballot_sync(kFull, need);
     if (needm) {
       if (need) {
-        if (CONS == FS_CONSUMER_COUNT || CONS == kConsCountClosed) {
+        if (COUNTLIKE) {
           acc += e_count.n;
           e_count.n = 0;
         } else if (HISTLIKE) {
@@ -458,6 +460,7 @@ __global__ void __launch_bounds__(kBlock) fs_enum_kernel(const KParams P) {
             budget = (uint32_t)(e - u);
             const uint64_t off = unrank<D, NEED_AD>(st, c, kt, u);
             budget -= position_in_node<D, NEED_AD>(st, c, off);
+            if (CAND) enter_candidates<D>(st, c);
             sync_k<D, ALPHA>(st, budget);
             if (CONS == FS_CONSUMER_ROWS) e_rows.start((u - P.unit0) * (uint64_t)EmitRows<D, B>::kRB);
           }
@@ -488,6 +491,10 @@ __global__ void __launch_bounds__(kBlock) fs_enum_kernel(const KParams P) {
           fast_step<D, NEED_AD, ALPHA>(st, c, kt, budget, e_count);
         } else if (CONS == kConsCountClosed) {
           fast_step_closed<D>(st, c, kt, budget, e_count);
+        } else if (CONS == kConsCountSkipOff) {
+          fast_step_cand<D, false>(st, c, kt, budget, e_count.n);
+        } else if (CONS == kConsCountSkipPaper) {
+          fast_step_cand<D, true>(st, c, kt, budget, e_count.n);
         } else if (CONS == kConsHistClosed) {
           fast_step_closed<D>(st, c, kt, budget, e_hcl);
         } else if (CONS == FS_CONSUMER_HIST) {
@@ -514,6 +521,7 @@ __global__ void __launch_bounds__(kBlock) fs_enum_kernel(const KParams P) {
       if (__any_sync(kFull, slow)) {
         if (slow) {
           slow_step<D, NEED_AD, ALPHA>(st, c, kt, budget);
+          if (CAND) enter_candidates<D>(st, c);
           sync_k<D, ALPHA>(st, budget);
           if (CONS == FS_CONSUMER_ROWS && budget == 0) rows_slice_done(P, e_rows, fin, fin_soff, fin_goff, fin_len);
         }
@@ -533,7 +541,7 @@ __global__ void __launch_bounds__(kBlock) fs_enum_kernel(const KParams P) {
 
   // ---------------------------------------------------------------- epilogue
   if (CONS == kConsRowsAny) e_cmp.finish(P);
-  if (CONS == FS_CONSUMER_COUNT || CONS == kConsCountClosed) {
+  if (COUNTLIKE) {
     acc += e_count.n;
 #pragma unroll
     for (int o = 16; o > 0; o >>= 1) acc += __shfl_xor_sync(kFull, acc, o);
@@ -561,7 +569,9 @@ __global__ void fs_d1_kernel(const KParams P) {
   if (threadIdx.x != 0 || blockIdx.x != 0) return;
   if (!(P.unit0 == 0 && P.unit1 > 0)) return;
   const uint32_t x = P.c.n / P.c.g[0];
-  if (CONS == FS_CONSUMER_COUNT || CONS == kConsCountClosed) atomicAdd(P.count_out, 1ull);
+  if (CONS == FS_CONSUMER_COUNT || CONS == kConsCountClosed || CONS == kConsCountSkipOff ||
+      CONS == kConsCountSkipPaper)
+    atomicAdd(P.count_out, 1ull);
   if (CONS == FS_CONSUMER_HIST || CONS == kConsHistClosed) atomicAdd(&P.hist_out[x], 1ull);
   if (CONS == FS_CONSUMER_ANY) {
     bool ok;

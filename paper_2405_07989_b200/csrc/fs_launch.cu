@@ -11,6 +11,8 @@ int fs_dispatch_hist(fs_plan *p, int B, const fs::KParams &kp, cudaStream_t s, b
 int fs_dispatch_any(fs_plan *p, int B, const fs::KParams &kp, cudaStream_t s, bool q, uint32_t *g);
 int fs_dispatch_rows(fs_plan *p, int B, const fs::KParams &kp, cudaStream_t s, bool q, uint32_t *g);
 int fs_dispatch_hist_closed(fs_plan *p, int B, const fs::KParams &kp, cudaStream_t s, bool q, uint32_t *g);
+int fs_dispatch_count_skip(fs_plan *p, int B, const fs::KParams &kp, cudaStream_t s, bool q, uint32_t *g,
+                          bool paper);
 int fs_dispatch_count_closed(fs_plan *p, int B, const fs::KParams &kp, cudaStream_t s, bool q, uint32_t *g);
 int fs_dispatch_rowsany(fs_plan *p, int B, const fs::KParams &kp, cudaStream_t s, bool q, uint32_t *g);
 
@@ -22,6 +24,8 @@ static int dispatch(fs_plan *p, int consumer, int B, const fs::KParams &kp, cuda
     case FS_CONSUMER_ROWS: return fs_dispatch_rows(p, B, kp, s, q, g);
     case fs::kConsRowsAny: return fs_dispatch_rowsany(p, B, kp, s, q, g);
     case fs::kConsCountClosed: return fs_dispatch_count_closed(p, B, kp, s, q, g);
+    case fs::kConsCountSkipOff: return fs_dispatch_count_skip(p, B, kp, s, q, g, false);
+    case fs::kConsCountSkipPaper: return fs_dispatch_count_skip(p, B, kp, s, q, g, true);
     case fs::kConsHistClosed: return fs_dispatch_hist_closed(p, B, kp, s, q, g);
   }
   return FS_EINVAL;

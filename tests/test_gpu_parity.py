@@ -97,6 +97,15 @@ def test_count_closed_tail(oracle_mod, inst):
 
 
 @pytest.mark.parametrize("inst", ALL, ids=ids)
+def test_count_skip_ablation(oracle_mod, inst):
+    n, g = inst.n, inst.gens
+    want = oracle.count(n, g)
+    for tail in (L.FS_TAIL_SKIP_OFF, L.FS_TAIL_SKIP_PAPER):
+        for T in (0, 2):
+            assert api.fs_count_ex(n, g, slice_units=T, tail=tail) == want
+
+
+@pytest.mark.parametrize("inst", ALL, ids=ids)
 def test_hist_closed_tail(oracle_mod, inst):
     n, g = inst.n, inst.gens
     want = oracle.hist(n, g)

@@ -78,6 +78,20 @@ def test_closed_tail_count(oracle_mod, inst):
 
 
 @pytest.mark.parametrize("inst", INSTANCES, ids=lambda i: "%s" % i.name)
+def test_skip_ablation_count(oracle_mod, inst):
+    """Skip=off / Skip=paper candidate loops (the paper's literal index-(d-1) loop): same
+    count and per-slice counts as the modulo-skip-at-entry rows."""
+    n, g = inst.n, inst.gens
+    want = oracle.count(n, g)
+    for tail in (L.FS_TAIL_SKIP_OFF, L.FS_TAIL_SKIP_PAPER):
+        for go in (0, 1):
+            a = host_model(n, g, L.FS_CONSUMER_COUNT, slice_units=3, want_slices=True, tail=tail, gen_order=go)
+            b = host_model(n, g, L.FS_CONSUMER_COUNT, slice_units=3, want_slices=True, gen_order=go)
+            assert a["count"] == want
+            assert a["slice_counts"] == b["slice_counts"]
+
+
+@pytest.mark.parametrize("inst", INSTANCES, ids=lambda i: "%s" % i.name)
 def test_closed_tail_hist(oracle_mod, inst):
     """Closed-tail histogram: strided difference array of each node's length progression."""
     n, g = inst.n, inst.gens
