@@ -14,11 +14,11 @@ namespace fs {
 
 constexpr int kBlock = 256;          // threads per persistent CTA
 // Materialise (M1) per-lane staging: two 64 B halves + room for one row spilling past them
-// (rows are <= 64 B); lane stride 208 B = 13 x 16 B, so the flush reads 16 B per LDS.128
-// (lanes at equal positions spread over 8 bank groups).
+// (rows are <= 64 B); lane stride 196 B = 49 words (odd) so lanes at equal positions hit
+// distinct shared-memory banks (measured faster than a 16 B-aligned stride with LDS.128).
 constexpr uint32_t kHalf = 64;                    // flush granule: one completed half
 constexpr uint32_t kStageBytes = 2 * kHalf + 64;  // 192 B usable per lane
-constexpr uint32_t kLaneStride = kStageBytes + 16;
+constexpr uint32_t kLaneStride = kStageBytes + 4;
 constexpr uint32_t kKtabMax = 2048;  // node tables in shared memory if g_{d-1} <= this (<= 24 KB)
 constexpr uint32_t kHistSmemMax = 24576;  // u32 histogram bins kept in shared memory
 constexpr int kConsRowsAny = 4;           // internal consumer: materialise, order = any (M2)

@@ -304,7 +304,12 @@ __device__ __forceinline__ void warp_flush(bool &pend, uint32_t soff, uint64_t g
     const uint64_t s_goff = __shfl_sync(kFull, goff, sl);
     if (src >= 0) {
       for (uint32_t o = (uint32_t)j * 16u; o < s_len; o += 16u * kLanesPerSeg) {
-        const uint4 v = *reinterpret_cast<const uint4 *>(warp_stage + src * kLaneStride + s_soff + o);
+        const uint32_t *r = reinterpret_cast<const uint32_t *>(warp_stage + src * kLaneStride + s_soff + o);
+        uint4 v;
+        v.x = r[0];
+        v.y = r[1];
+        v.z = r[2];
+        v.w = r[3];
         __stcs(reinterpret_cast<uint4 *>(out + s_goff + o), v);
       }
     }
