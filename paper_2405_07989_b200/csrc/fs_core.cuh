@@ -402,6 +402,27 @@ FS_HD void fast_step_closed(Lane<D> &st, const Consts &c, const KT &kt, uint32_t
   if (em) st.cur = -1;
 }
 
+// Count-only closed step: rows = floor(max(cur + s, 0) / s), which is floor(a*/s) + 1 for a
+// node with rows (cur = a* >= 0) and 0 otherwise (cur < 0), so no compare/select is needed
+// (cur + s <= n + g_d < 2^31 keeps the magic division exact).
+template <int D, class KT>
+FS_HD void fast_step_count_closed(Lane<D> &st, const Consts &c, const KT &kt, uint32_t &cnt) {
+  constexpr int L = D - 2;
+  if constexpr (L >= 1) {
+    const bool fa = st.cur < 0 && st.k != 0;
+    const Adv w = kt.step(st.rho, c);
+    if (fa) {
+      st.k -= 1u;
+      st.rho = w.next;
+      st.A += w.inc;
+      st.cur = (int32_t)st.A - (int32_t)w.k0;
+    }
+  }
+  const int32_t x = st.cur + (int32_t)c.s;
+  cnt += divq((uint32_t)(x > 0 ? x : 0), c.dvS);
+  st.cur = -1;
+}
+
 struct NodeCount {
   uint32_t n;
   template <int D>

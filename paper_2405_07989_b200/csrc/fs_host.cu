@@ -401,8 +401,15 @@ void host_model_d(const fs_plan *p, const KT &ktab, HostSink &sink, uint64_t *sl
     } else if (ALPHA && (p->consumer == FS_CONSUMER_COUNT || p->consumer == FS_CONSUMER_HIST) &&
                p->ex.tail == FS_TAIL_CLOSED) {
       HostNodeSink ns{p, &sink, 0};
+      const bool count_only = p->consumer == FS_CONSUMER_COUNT;
       while (!fs::needs_refill<D, ALPHA>(st, budget)) {
-        fs::fast_step_closed<D>(st, c, ktab, budget, ns);
+        if (count_only) {  // the kernels' count-only closed step
+          uint32_t cnt = 0;
+          fs::fast_step_count_closed<D>(st, c, ktab, cnt);
+          ns.n += cnt;
+        } else {
+          fs::fast_step_closed<D>(st, c, ktab, budget, ns);
+        }
         fs::sync_k<D, ALPHA>(st, budget);
         if (fs::needs_slow<D>(st, budget)) {
           fs::slow_step<D, true, ALPHA>(st, c, ktab, budget);

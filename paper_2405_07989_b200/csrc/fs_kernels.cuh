@@ -495,7 +495,7 @@ __global__ void __launch_bounds__(kBlock) fs_enum_kernel(const KParams P) {
         if (CONS == FS_CONSUMER_COUNT) {
           fast_step<D, NEED_AD, ALPHA>(st, c, kt, budget, e_count);
         } else if (CONS == kConsCountClosed) {
-          fast_step_closed<D>(st, c, kt, budget, e_count);
+          fast_step_count_closed<D>(st, c, kt, e_count.n);
         } else if (CONS == kConsCountSkipOff) {
           fast_step_cand<D, false>(st, c, kt, budget, e_count.n);
         } else if (CONS == kConsCountSkipPaper) {
