@@ -135,6 +135,35 @@ struct EmitAny {
   }
 };
 
+// Store one row (D coordinates, caller order) at a shared-memory address q.  B = 16: q is
+// 2-byte aligned; adjacent coordinates are packed into 32-bit stores on the 4-byte-aligned
+// side of the row (D/2 + 1 stores instead of D) -- shared-memory wavefronts are what bound
+// the materialise kernels.  B = 32: one 32-bit store per coordinate.
+template <int D, int B>
+__device__ __forceinline__ void store_row(unsigned char *q, const uint32_t (&v)[D]) {
+  if (B == 32) {
+#pragma unroll
+    for (int i = 0; i < D; ++i) *reinterpret_cast<uint32_t *>(q + 4 * i) = v[i];
+  } else if ((reinterpret_cast<uintptr_t>(q) & 2u) == 0) {
+#pragma unroll
+    for (int i = 0; i + 1 < D; i += 2) *reinterpret_cast<uint32_t *>(q + 2 * i) = (v[i] & 0xffffu) | (v[i + 1] << 16);
+    if (D & 1) *reinterpret_cast<uint16_t *>(q + 2 * (D - 1)) = (uint16_t)v[D - 1];
+  } else {
+    *reinterpret_cast<uint16_t *>(q) = (uint16_t)v[0];
+#pragma unroll
+    for (int i = 1; i + 1 < D; i += 2) *reinterpret_cast<uint32_t *>(q + 2 * i) = (v[i] & 0xffffu) | (v[i + 1] << 16);
+    if (!(D & 1)) *reinterpret_cast<uint16_t *>(q + 2 * (D - 1)) = (uint16_t)v[D - 1];
+  }
+}
+
+template <int D>
+__device__ __forceinline__ void row_values(const Lane<D> &st, const Consts &c, uint32_t (&v)[D]) {
+#pragma unroll
+  for (int j = 0; j < D - 2; ++j) v[j] = cur_coord<D>(st, j);
+  v[D - 2] = (uint32_t)st.cur;
+  v[D - 1] = row_ad<D>(st, c);
+}
+
 // M1 (canonical order).  Rows are appended LINEARLY to the lane's staging buffer at byte w
 // (w < 2 kHalf before a write, so a row never wraps and every coordinate is one STS with an
 // immediate offset).  When w crosses kHalf, half 0 is complete; when it crosses 2 kHalf,
@@ -164,11 +193,9 @@ struct EmitRows {
   }
   __device__ __forceinline__ void cond(bool em, const Lane<D> &st, const Consts &c) {
     if (!em) return;
-    unsigned char *q = buf + w;
-#pragma unroll
-    for (int j = 0; j < D - 2; ++j) put(q, j, cur_coord<D>(st, j));
-    put(q, D - 2, (uint32_t)st.cur);
-    put(q, D - 1, row_ad<D>(st, c));
+    uint32_t v[D];
+    row_values<D>(st, c, v);
+    store_row<D, B>(buf + w, v);
     const uint32_t nw = w + kRB;
     const bool c0 = w < kHalf && nw >= kHalf;          // half 0 complete
     const bool c1 = w < 2 * kHalf && nw >= 2 * kHalf;  // half 1 complete (both, for rows > kHalf)
@@ -236,10 +263,12 @@ struct EmitCompact {
         putb(q, poff[D - 2], (uint32_t)st.cur);
         putb(q, poff[D - 1], ad);
       } else {
+        uint32_t v[D];
 #pragma unroll
-        for (int j = 0; j < D - 2; ++j) put(q, j, cur_coord<D>(st, j));
-        put(q, D - 2, (uint32_t)st.cur);
-        put(q, D - 1, ad);
+        for (int j = 0; j < D - 2; ++j) v[j] = cur_coord<D>(st, j);
+        v[D - 2] = (uint32_t)st.cur;
+        v[D - 1] = ad;
+        store_row<D, B>(q, v);
       }
     }
     wrows += (uint32_t)__popc(m);
