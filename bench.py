@@ -32,11 +32,13 @@ from paper_2405_07989_b200 import workloads as W  # noqa: E402
 METRIC = "factorizations/sec (count, store) at 1/2/4/8 B200 vs INT-ALU/HBM roofline"
 UNIT = "factorizations/s"
 
-# Algorithmic integer-op model per unit of the method:
-#   node entry (advance to the next level-L prefix + solve its first valid a_{d-1}) : 10
-#   row (one valid factorization consumed + modulo-skip step)                      :  4
-#   deeper node (ascend to a level-k prefix, k < L, greedy re-solve)               : 12
-OPS_NODE, OPS_ROW, OPS_DEEP = 10, 4, 12
+# Algorithmic integer-op model per unit of the method, counting the
+# minimal operations of the residue/quotient representation R_L = A g_{d-1} + rho:
+#   node entry (advance to the next level-L prefix: transition load, residue, quotient;
+#     first valid a* = A - k0(rho); run counter)                                   :  5
+#   row (one valid factorization consumed, a_{d-1} -= s, compare, counter)           :  4
+#   deeper node (ascend to a level-k prefix, k < L, greedy re-solve)                 : 12
+OPS_NODE, OPS_ROW, OPS_DEEP = 5, 4, 12
 INT_LANES_PER_CLK_PER_SM = 128  # 4 SMSPs x 32 lanes, one warp-instruction / clk each
 NUM_SMS = 148
 
@@ -122,7 +124,7 @@ def microbench():
     return out
 
 
-OPS_NODE_CLOSED = 14  # node entry + closed-form row count floor(a*/s) + 1 (NEXT-1)
+OPS_NODE_CLOSED = 8  # node entry (5) + closed-form row count floor(a*/s) + 1: max, mulhi, add (NEXT-1)
 
 
 def ops_model(info, closed: bool = False) -> float:
@@ -433,14 +435,19 @@ def extras(args, world, rank, local, dev, stream, peaks, peaks_kind, barrier, ma
 
     # ---- store: C2-XL rows, u16; canonical layout (M1) and warp-compacted layout (M2)
     inst = W.C2XL
+    store_out = None  # one output buffer, reused by the three layouts (as a caller would)
     for order, key, go in ((L.FS_ORDER_CANONICAL, "store", 0), (L.FS_ORDER_ANY, "store_any", 0),
                            (L.FS_ORDER_ANY, "store_any_auto_order", L.FS_GENORDER_AUTO)):
         p = api.Plan(inst.n, inst.gens, L.FS_CONSUMER_ROWS, order=order, gen_order=go, **kw)
         info = p.info
         rows = info["row_end"] - info["row_begin"]
-        out = torch.empty((rows, inst.d), dtype=torch.uint16, device=dev)
+        if store_out is None or store_out.shape[0] < rows:
+            store_out = None
+            torch.cuda.empty_cache()
+            store_out = torch.empty((rows, inst.d), dtype=torch.uint16, device=dev)
+        out = store_out[:rows]
         p.enumerate_async(16, out, rows)
-        ms = _time_ms(lambda: p.enumerate_async(16, out, rows), stream, 3, barrier, max_over_ranks)
+        ms = _time_ms(lambda: p.enumerate_async(16, out, rows), stream, 5, barrier, max_over_ranks)
         total_rows = info["total_rows"]
         bytes_ = total_rows * inst.d * 2
         gbs_all = bytes_ / (ms / 1e3) / 1e9
@@ -454,7 +461,8 @@ def extras(args, world, rank, local, dev, stream, peaks, peaks_kind, barrier, ma
                                 "peak_source": "MEASURED_PEAKS.json hbm_gbs x %d (%s, copy r+w)" % (world, peaks_kind),
                                 "frac_of_write_microbench": (gbs_all / world / mb["hbm_write_gbs"]) if mb else None}}
         del out
-        torch.cuda.empty_cache()
+    del store_out
+    torch.cuda.empty_cache()
 
     # ---- count / hist / any on their configs; NEXT-1 (closed tail) and NEXT-2 (generator
     # order) variants of SURVEY 8(f) are labelled and reported beside the literal path

@@ -21,6 +21,8 @@ INCLUDE = [os.path.join(ROOT, "include", h) for h in ("fsgpu.h", "fsgpu_debug.h"
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 FLAGS = ["-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC,-O2", "-Xcompiler", "-fvisibility=default"]
+# experiments only (e.g. FS_NVCC_EXTRA="-DFS_CC_GROUP=8"); the shipped build sets none
+FLAGS += os.environ.get("FS_NVCC_EXTRA", "").split()
 
 
 def _newest(paths):

@@ -1,5 +1,7 @@
 // fs_capi.cu -- the extern "C" boundary declared in include/fsgpu.h.
 #include <cuda_runtime.h>
+
+#include <vector>
 #include <stdint.h>
 #include <string.h>
 
@@ -11,8 +13,9 @@
 
 namespace {
 
-// scratch layout (bytes): [0] queue u64, [8] count u64, [16] found i32, [64..128) witness
-constexpr size_t kOffCount = 8, kOffFound = 16, kOffFront = 24, kOffBack = 32, kOffWitness = 64;
+// scratch layout (bytes): [0] queue u64, [8] count u64, [16] found i32, [64..128) witness,
+// [1024] M2 front cursor, [1152] M2 back cursor (own 128 B lines: no contention with the queue)
+constexpr size_t kOffCount = 8, kOffFound = 16, kOffWitness = 64, kOffFront = 1024, kOffBack = 1152;
 
 struct DeviceGuard {
   int prev = -1;
@@ -222,7 +225,7 @@ int fs_plan_enumerate_async(fs_plan *p, int B, void *out_dev, uint64_t cap) {
   if (p->ex.order == FS_ORDER_ANY) {
     if (take < span) return FS_ERANGE;  // compaction writes all of the rank's rows
     char *base = reinterpret_cast<char *>(p->scratch_dev);
-    if (cudaMemsetAsync(base + kOffFront, 0, 16, p->stream) != cudaSuccess) return FS_ECUDA;
+    if (cudaMemsetAsync(base + kOffFront, 0, kOffBack + 8 - kOffFront, p->stream) != cudaSuccess) return FS_ECUDA;
     kp.front = reinterpret_cast<unsigned long long *>(base + kOffFront);
     kp.back = reinterpret_cast<unsigned long long *>(base + kOffBack);
     kp.rank_rows = span;
@@ -329,11 +332,13 @@ int64_t fs_enumerate_ex(uint64_t n, const uint32_t *gens, int d, int B, void *ou
     if (rc != FS_OK) return rc;
     if (h.p->ex.order == FS_ORDER_ANY && h.p->row_end > h.p->row_begin) {
       // M2 exactness check: the front and back cursors must meet at the rank's row count
-      unsigned long long cur[2] = {0, 0};
-      if (cudaMemcpy(cur, reinterpret_cast<char *>(h.p->scratch_dev) + kOffFront, 16, cudaMemcpyDeviceToHost) !=
-          cudaSuccess)
+      unsigned long long fr = 0, bk = 0;
+      char *base = reinterpret_cast<char *>(h.p->scratch_dev);
+      if (cudaMemcpy(&fr, base + kOffFront, 8, cudaMemcpyDeviceToHost) != cudaSuccess ||
+          cudaMemcpy(&bk, base + kOffBack, 8, cudaMemcpyDeviceToHost) != cudaSuccess)
         return FS_ECUDA;
-      if (cur[0] + cur[1] != h.p->row_end - h.p->row_begin) return FS_ECUDA;
+      if (fr + bk != h.p->row_end - h.p->row_begin)
+        return FS_ECUDA;
     }
   }
   if (global_row_offset_out) *global_row_offset_out = h.p->row_begin;

@@ -70,6 +70,8 @@ struct Consts {
   uint32_t alpha, beta;  // units per node entry / per row
   uint32_t ktab_len;     // 0: k0 by arithmetic; else words of the node tables (below)
   uint32_t adv_off;      // word offset of the advance table inside ktab (8 B aligned)
+  uint32_t cadv_off;     // word offset of the count-only group table (0: none; see fs_host.cu)
+  uint32_t mhi;          // ceil(2^32 / s) for the group table's umulhi division
   int32_t dl;            // t - s: change of a row's length from one valid a_{d-1} to the next
   uint32_t dstride;      // stride of the closed-tail length-difference array (|dl|, or 1 if 0)
   uint8_t perm[FS_MAX_D];  // internal coordinate j is the caller's coordinate perm[j]
@@ -161,6 +163,7 @@ struct Adv {
   uint32_t next, k0, inc;  // next residue, k0(next), increment of floor(R_L / g_{d-1})
 };
 constexpr uint32_t kAdvBits = 11;  // next < 2^11 in the packed table word
+constexpr uint32_t kCAdvShift = 16;  // count group table: byte offset < 2^16 below the increment
 FS_HD uint32_t adv_pack(uint32_t next, uint32_t inc) { return next | (inc << kAdvBits); }
 FS_HD Adv adv_unpack(uint32_t w0, uint32_t w1) {
   return Adv{w0 & ((1u << kAdvBits) - 1u), w1, w0 >> kAdvBits};

@@ -170,8 +170,31 @@ int fs_validate_and_build(fs_plan *p, uint64_t n, const uint32_t *gens, int d, i
         p->ktab[adv_off + 2 * rho] = fs::adv_pack(w.next, w.inc);
         p->ktab[adv_off + 2 * rho + 1] = w.k0;
       }
-      c.ktab_len = (uint32_t)p->ktab.size();
       c.adv_off = adv_off;
+      // Count-only closed-tail group table (count + tail=closed): per residue rho the entry
+      // {rel | (q + carry) << kCAdvShift, s - k0(next)} where rel = byte offset of next's
+      // entry from the table start (the kernel adds its shared-memory base when it copies
+      // the table, so one LDS.64 yields the next entry's address directly) and s - k0 is the
+      // row count's numerator offset (kNone -> INT32_MIN: no rows); 16 KB of the 64 KB
+      // offset field are left for the table's shared-memory base.  Exact division by
+      // umulhi(x, ceil(2^32 / s)) needs x s < 2^32 for x <= n / g_{d-1} + s.
+      const uint64_t xmax = n / c.gA + c.s;
+      const uint32_t cadv_off = (uint32_t)p->ktab.size();
+      if (consumer == FS_CONSUMER_COUNT && e.tail == FS_TAIL_CLOSED && L >= 1 && c.s >= 2 &&
+          xmax * c.s < (1ull << 32) && c.q + 1u < (1u << (32 - fs::kCAdvShift)) &&
+          4ull * cadv_off + 8ull * c.gA + 16384ull <= (1ull << fs::kCAdvShift)) {
+        p->ktab.resize(cadv_off + 2u * c.gA, 0u);
+        const fs::KTabArith ar{};
+        for (uint32_t rho = 0; rho < c.gA; ++rho) {
+          const fs::Adv w = ar.step(rho, c);
+          p->ktab[cadv_off + 2 * rho] = (4u * cadv_off + 8u * w.next) | (w.inc << fs::kCAdvShift);
+          p->ktab[cadv_off + 2 * rho + 1] =
+              w.k0 == fs::kNone ? 0x80000000u : (uint32_t)((int32_t)c.s - (int32_t)w.k0);
+        }
+        c.cadv_off = cadv_off;
+        c.mhi = (uint32_t)(((1ull << 32) + c.s - 1) / c.s);
+      }
+      c.ktab_len = (uint32_t)p->ktab.size();
       c.ktab = p->ktab.data();
     }
     const uint64_t N1 = n + 1;
@@ -288,7 +311,7 @@ int fs_plan_upload_impl(fs_plan *p) {
                         p->stream) != cudaSuccess)
       return FS_ECUDA;
   }
-  if (cudaMalloc(&p->scratch_dev, 256) != cudaSuccess) return FS_ENOMEM;
+  if (cudaMalloc(&p->scratch_dev, fs::kScratchBytes) != cudaSuccess) return FS_ENOMEM;
   p->uploaded = true;
   return FS_OK;
 }

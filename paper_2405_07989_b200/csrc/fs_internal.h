@@ -13,6 +13,12 @@
 namespace fs {
 
 constexpr int kBlock = 256;          // threads per persistent CTA
+#ifndef FS_CC_GROUP
+#define FS_CC_GROUP 16  // steps per group of the closed-tail count (cc_group)
+#endif
+#ifndef FS_CC_MINB
+#define FS_CC_MINB 1  // __launch_bounds__ min blocks per SM of the closed-tail count kernel
+#endif
 // Materialise (M1) per-lane staging: two 64 B halves + room for one row spilling past them
 // (rows are <= 64 B); lane stride 196 B = 49 words (odd) so lanes at equal positions hit
 // distinct shared-memory banks (measured faster than a 16 B-aligned stride with LDS.128).
@@ -22,7 +28,11 @@ constexpr uint32_t kLaneStride = kStageBytes + 4;
 constexpr uint32_t kKtabMax = 2048;  // node tables in shared memory if g_{d-1} <= this (<= 24 KB)
 constexpr uint32_t kHistSmemMax = 24576;  // u32 histogram bins kept in shared memory
 constexpr int kConsRowsAny = 4;           // internal consumer: materialise, order = any (M2)
-constexpr uint32_t kWarpBuf = 4096;       // M2 per-warp compaction buffer (bytes)
+#ifndef FS_WARPBUF
+#define FS_WARPBUF 6144
+#endif
+constexpr uint32_t kWarpBuf = FS_WARPBUF;  // M2 per-warp compaction ring (bytes)
+constexpr size_t kScratchBytes = 2048;    // per-plan device scratch (queue, results, M2 cursors)
 constexpr int kConsCountClosed = 5;       // internal consumer: count with the closed-form tail
 constexpr int kConsHistClosed = 6;        // internal consumer: histogram with the closed-form tail
 constexpr int kConsCountSkipOff = 7;      // internal consumer: count, Skip=off ablation

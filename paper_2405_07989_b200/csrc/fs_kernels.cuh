@@ -229,84 +229,156 @@ __device__ __forceinline__ uint32_t lanemask_lt() {
 // ranked with one ballot and appended contiguously to the warp's shared buffer; when the
 // buffer is nearly full the warp reserves a block of 8k rows with ONE atomicAdd on the front
 // cursor (8 rows keep every block 16 B aligned) and writes it with coalesced 16 B stores.
+#ifndef FS_M2_TH
+#define FS_M2_TH 6  // reserve when the ring holds FS_M2_TH / 8 of its capacity
+#endif
+// shared-memory stores/loads by 32-bit shared-window address
+__device__ __forceinline__ void sts16(uint32_t a, uint32_t v) {
+  asm volatile("st.shared.u16 [%0], %1;" ::"r"(a), "h"((unsigned short)v) : "memory");
+}
+__device__ __forceinline__ void sts32(uint32_t a, uint32_t v) {
+  asm volatile("st.shared.u32 [%0], %1;" ::"r"(a), "r"(v) : "memory");
+}
+__device__ __forceinline__ uint4 lds128(uint32_t a) {
+  uint4 v;
+  asm volatile("ld.shared.v4.u32 {%0, %1, %2, %3}, [%4];" : "=r"(v.x), "=r"(v.y), "=r"(v.z), "=r"(v.w) : "r"(a) : "memory");
+  return v;
+}
+__device__ __forceinline__ uint32_t lds16(uint32_t a) {
+  unsigned short v;
+  asm volatile("ld.shared.u16 %0, [%1];" : "=h"(v) : "r"(a) : "memory");
+  return v;
+}
+// keep a value in a register (the compiler may not re-derive it inside the loop)
+__device__ __forceinline__ void pin(uint32_t &x) { asm volatile("" : "+r"(x)); }
+
 template <int D, int B>
 struct EmitCompact {
+  // M2 (order = any): each warp appends its rows to a RING in shared memory (kRing bytes, a
+  // whole number of 8-row blocks, so a row never straddles the wrap and every 8-row block is
+  // a multiple of 16 B).  Once the ring holds FS_M2_TH/8 of its capacity the warp reserves
+  // those rows (a multiple of 8) on the front cursor with one atomicAdd whose result is not
+  // waited for: the warp keeps enumerating, and writes the reserved rows out (coalesced 16 B
+  // streaming stores) only when the ring runs out of room, so the atomic's latency under
+  // contention is hidden behind enumeration.  Each warp's final < 8 rows go to the back
+  // cursor; front and back meet exactly at the rank's row count.
   static constexpr uint32_t kRB = D * (B / 8);
-  static constexpr uint32_t kCap = kWarpBuf / kRB;
-  unsigned char *buf;
-  uint32_t wrows;           // warp-uniform
+  static constexpr uint32_t kBlk = 8 * kRB;
+  static constexpr uint32_t kRing = (kWarpBuf / kBlk) * kBlk;
+  static constexpr uint32_t kCap = kRing / kRB;
+  uint32_t sbuf;            // shared-window address of the warp's ring
+  uint32_t head, tail;      // warp-uniform row counters: rows [head, tail) are in the ring
+  uint32_t hpos, wpos;      // byte positions of rows head and tail in the ring
+  uint32_t resv;            // rows reserved by the pending atomic (0: none)
+  unsigned long long roff;  // lane 0: row offset returned by the pending atomic
   uint32_t poff[D];         // byte offset of internal coordinate j in the caller's row
-  __device__ __forceinline__ void init(const Consts &c) {
+  __device__ __forceinline__ void init(const Consts &c, const unsigned char *buf) {
+    sbuf = (uint32_t)__cvta_generic_to_shared(buf);
+    pin(sbuf);
+    head = tail = hpos = wpos = resv = 0;
+    roff = 0;
 #pragma unroll
-    for (int j = 0; j < D; ++j) poff[j] = (uint32_t)c.perm[j] * (B / 8);
+    for (int j = 0; j < D; ++j) {
+      poff[j] = (uint32_t)c.perm[j] * (B / 8);
+      pin(poff[j]);
+    }
   }
-  __device__ __forceinline__ void putb(unsigned char *q, uint32_t off, uint32_t v) {
+  __device__ __forceinline__ uint32_t rows() const { return tail - head; }
+  __device__ __forceinline__ void put(uint32_t a, uint32_t v) {
     if (B == 16)
-      *reinterpret_cast<uint16_t *>(q + off) = (uint16_t)v;
+      sts16(a, v);
     else
-      *reinterpret_cast<uint32_t *>(q + off) = v;
-  }
-  __device__ __forceinline__ void put(unsigned char *q, int i, uint32_t v) {
-    if (B == 16)
-      *reinterpret_cast<uint16_t *>(q + 2 * i) = (uint16_t)v;
-    else
-      *reinterpret_cast<uint32_t *>(q + 4 * i) = v;
+      sts32(a, v);
   }
   __device__ __forceinline__ void cond(bool em, const Lane<D> &st, const Consts &c) {
     const unsigned m = __ballot_sync(kFull, em);
     if (em) {  // coordinates written at the caller's positions (generator order may differ)
-      unsigned char *q = buf + (wrows + (uint32_t)__popc(m & lanemask_lt())) * kRB;
+      uint32_t pos = wpos + (uint32_t)__popc(m & lanemask_lt()) * kRB;
+      if (pos >= kRing) pos -= kRing;
+      const uint32_t q = sbuf + pos;
       const uint32_t ad = row_ad<D>(st, c);
       if (c.permuted) {
 #pragma unroll
-        for (int j = 0; j < D - 2; ++j) putb(q, poff[j], cur_coord<D>(st, j));
-        putb(q, poff[D - 2], (uint32_t)st.cur);
-        putb(q, poff[D - 1], ad);
-      } else {
+        for (int j = 0; j < D - 2; ++j) put(q + poff[j], cur_coord<D>(st, j));
+        put(q + poff[D - 2], (uint32_t)st.cur);
+        put(q + poff[D - 1], ad);
+      } else if (B == 32) {
+#pragma unroll
+        for (int j = 0; j < D - 2; ++j) sts32(q + 4 * j, cur_coord<D>(st, j));
+        sts32(q + 4 * (D - 2), (uint32_t)st.cur);
+        sts32(q + 4 * (D - 1), ad);
+      } else {  // u16 rows: adjacent coordinates packed into 32-bit stores
         uint32_t v[D];
 #pragma unroll
         for (int j = 0; j < D - 2; ++j) v[j] = cur_coord<D>(st, j);
         v[D - 2] = (uint32_t)st.cur;
         v[D - 1] = ad;
-        store_row<D, B>(q, v);
+        if ((q & 2u) == 0) {
+#pragma unroll
+          for (int i = 0; i + 1 < D; i += 2) sts32(q + 2 * i, (v[i] & 0xffffu) | (v[i + 1] << 16));
+          if (D & 1) sts16(q + 2 * (D - 1), v[D - 1]);
+        } else {
+          sts16(q, v[0]);
+#pragma unroll
+          for (int i = 1; i + 1 < D; i += 2) sts32(q + 2 * i, (v[i] & 0xffffu) | (v[i + 1] << 16));
+          if (!(D & 1)) sts16(q + 2 * (D - 1), v[D - 1]);
+        }
       }
     }
-    wrows += (uint32_t)__popc(m);
+    const uint32_t nr = (uint32_t)__popc(m);
+    tail += nr;
+    wpos += nr * kRB;
+    if (wpos >= kRing) wpos -= kRing;
   }
-  // converged; flush 8k rows when the buffer cannot take `room` more rows
-  __device__ __forceinline__ void flush(const KParams &P, bool final, uint32_t room = 32) {
-    if (!final && wrows + room <= kCap) return;
-    const uint32_t k = wrows & ~7u;
+  __device__ __forceinline__ void reserve(const KParams &P) {
+    const uint32_t k = rows() & ~7u;
     if (k == 0) return;
+    resv = k;
+    if ((threadIdx.x & 31) == 0) roff = atomicAdd(P.front, (unsigned long long)k);
+  }
+  // converged: copy the reserved rows [head, head + resv) to their global offset
+  __device__ __forceinline__ void write_out(const KParams &P) {
     __syncwarp();
-    const int lane = threadIdx.x & 31;
-    unsigned long long off = 0;
-    if (lane == 0) off = atomicAdd(P.front, (unsigned long long)k);
-    off = __shfl_sync(kFull, off, 0);
-    const uint32_t bytes = k * kRB;  // multiple of 16
+    const unsigned long long off = __shfl_sync(kFull, roff, 0);
+    const uint32_t chunks = resv * kRB / 16u;
     uint4 *dst = reinterpret_cast<uint4 *>(P.rows_out + off * kRB);
-    const uint4 *src = reinterpret_cast<const uint4 *>(buf);
-    for (uint32_t i = lane; i < bytes / 16; i += 32) __stcs(dst + i, src[i]);
+    const int lane = threadIdx.x & 31;
+    for (uint32_t i = (uint32_t)lane; i < chunks; i += 32u) {
+      uint32_t sp = hpos + 16u * i;
+      if (sp >= kRing) sp -= kRing;
+      __stcs(dst + i, lds128(sbuf + sp));
+    }
     __syncwarp();
-    const uint32_t rem = (wrows - k) * kRB;  // < 8 rows; source and destination do not overlap
-    for (uint32_t i = 2u * lane; i < rem; i += 64u)
-      *reinterpret_cast<uint16_t *>(buf + i) = *reinterpret_cast<const uint16_t *>(buf + bytes + i);
-    __syncwarp();
-    wrows -= k;
+    head += resv;
+    hpos += resv * kRB;
+    if (hpos >= kRing) hpos -= kRing;
+    resv = 0;
+  }
+  // converged; keeps room for `room` more rows
+  __device__ __forceinline__ void flush(const KParams &P, bool final, uint32_t room = 32) {
+    if (resv && (final || rows() + room > kCap)) write_out(P);
+    if (!resv && (final || rows() >= kCap * FS_M2_TH / 8u || rows() + room > kCap)) {
+      reserve(P);
+      if (resv && (final || rows() + room > kCap)) write_out(P);
+    }
   }
   // converged, at warp exit: the final < 8 rows go to the back cursor with plain stores
   __device__ __forceinline__ void finish(const KParams &P) {
     flush(P, true);
-    if (wrows == 0) return;
+    const uint32_t r = rows();
+    if (r == 0) return;
     const int lane = threadIdx.x & 31;
     unsigned long long b = 0;
-    if (lane == 0) b = atomicAdd(P.back, (unsigned long long)wrows);
+    if (lane == 0) b = atomicAdd(P.back, (unsigned long long)r);
     b = __shfl_sync(kFull, b, 0);
-    const uint64_t pos = P.rank_rows - b - wrows;
+    const uint64_t pos = P.rank_rows - b - r;
     unsigned char *dst = P.rows_out + pos * kRB;
-    for (uint32_t i = 2u * lane; i < wrows * kRB; i += 64u)
-      *reinterpret_cast<uint16_t *>(dst + i) = *reinterpret_cast<const uint16_t *>(buf + i);
-    wrows = 0;
+    for (uint32_t i = 2u * lane; i < r * kRB; i += 64u) {
+      uint32_t sp = hpos + i;
+      if (sp >= kRing) sp -= kRing;
+      *reinterpret_cast<uint16_t *>(dst + i) = (uint16_t)lds16(sbuf + sp);
+    }
+    head = tail;
   }
 };
 
@@ -370,8 +442,48 @@ __device__ __forceinline__ uint64_t bitrev_bits(uint64_t x, uint32_t bits) {
   return bits ? (__brevll(x) >> (64 - bits)) : 0ull;
 }
 
+// Count with the closed tail, group form (Consts::cadv_off != 0): the entered node's rows
+// are taken at once, so a group step is only "advance and count": k (= min(budget, a_L)
+// at the last sync) bounds the valid steps; the others run on harmlessly (a residue stays a
+// residue) and are masked out of the sum.  Per step: one LDS.64 (next entry's shared
+// address + quotient increment, s - k0(next)), one add, one max, one umulhi-accumulate.
+template <int D>
+__device__ __forceinline__ uint32_t take_entry_rows(Lane<D> &st, const Consts &c) {
+  const int32_t x = st.cur + (int32_t)c.s;
+  st.cur = -1;
+  return divq((uint32_t)(x > 0 ? x : 0), c.dvS);
+}
+
+template <int D, int G>
+__device__ __forceinline__ void cc_group(Lane<D> &st, const Consts &c, uint32_t tab, uint32_t &cnt) {
+  if constexpr (D >= 3) {
+    uint32_t h = tab + 8u * st.rho;
+    uint32_t A = st.A;
+    const uint32_t kk = st.k;
+    uint32_t n = cnt;
+#pragma unroll
+    for (int u = 0; u < G; ++u) {
+      uint32_t w0, w1;
+      asm("ld.shared.v2.u32 {%0, %1}, [%2];" : "=r"(w0), "=r"(w1) : "r"(h));
+      h = w0 & ((1u << kCAdvShift) - 1u);
+      A += w0 >> kCAdvShift;
+      int32_t x = (int32_t)(A + w1);
+      x = x > 0 ? x : 0;
+      // n += umulhi(x, ceil(2^32/s)) for the valid steps u < kk (predicated multiply-add)
+      asm("{\n\t.reg .pred p;\n\tsetp.lt.u32 p, %2, %3;\n\t@p mad.hi.u32 %0, %1, %4, %0;\n\t}"
+          : "+r"(n)
+          : "r"((uint32_t)x), "r"((uint32_t)u), "r"(kk), "r"(c.mhi));
+    }
+    cnt = n;
+    st.rho = (h - tab) >> 3;
+    st.A = A;
+    st.k = kk > (uint32_t)G ? kk - (uint32_t)G : 0u;
+  }
+}
+
 template <int D, int CONS, int B, bool KTAB>
-__global__ void __launch_bounds__(kBlock) fs_enum_kernel(const KParams P) {
+__global__ void __launch_bounds__(kBlock, (CONS == kConsRowsAny ? 4 : CONS == kConsCountClosed ? FS_CC_MINB : 1))
+    fs_enum_kernel(const KParams P) {
   constexpr bool CAND = CONS == kConsCountSkipOff || CONS == kConsCountSkipPaper;
   constexpr bool COUNTLIKE = CONS == FS_CONSUMER_COUNT || CONS == kConsCountClosed || CAND;
   constexpr bool NEED_AD = !COUNTLIKE;
@@ -381,7 +493,7 @@ __global__ void __launch_bounds__(kBlock) fs_enum_kernel(const KParams P) {
   // ROWS: a lane completes at most one ring half in kHalf / row_bytes steps, so the warp
   // flushes pending halves once per that many steps.
   constexpr int kRowsPerHalf = (int)(kHalf / (D * (B / 8))) > 0 ? (int)(kHalf / (D * (B / 8))) : 1;
-  constexpr int UNROLL = CONS == FS_CONSUMER_ROWS ? kRowsPerHalf : (CONS == kConsCountClosed ? 8 : 4);
+  constexpr int UNROLL = CONS == FS_CONSUMER_ROWS ? kRowsPerHalf : (CONS == kConsCountClosed ? FS_CC_GROUP : 4);
   extern __shared__ __align__(16) unsigned char smem[];
   __shared__ unsigned int hist_guard;
   const Consts &c = P.c;
@@ -394,7 +506,14 @@ __global__ void __launch_bounds__(kBlock) fs_enum_kernel(const KParams P) {
       : ((CONS == kConsHistClosed ? P.diff_len : P.hist_len) + 3u) & ~3u;
   unsigned char *stage = reinterpret_cast<unsigned char *>(hist_s + hist_words);
 
-  for (uint32_t i = threadIdx.x; i < c.ktab_len; i += blockDim.x) ktab_s[i] = c.ktab[i];
+  const uint32_t ktab_base = (uint32_t)__cvta_generic_to_shared(ktab_s);
+  // count-only group table (closed tail): its link words get the table's shared address
+  const bool cfast = KTAB && CONS == kConsCountClosed && c.cadv_off != 0 && ktab_base < 16384u;
+  for (uint32_t i = threadIdx.x; i < c.ktab_len; i += blockDim.x) {
+    uint32_t v = c.ktab[i];
+    if (cfast && i >= c.cadv_off && !((i - c.cadv_off) & 1u)) v += ktab_base;
+    ktab_s[i] = v;
+  }
   if (HISTLIKE) {
     for (uint32_t i = threadIdx.x; i < hist_words; i += blockDim.x) hist_s[i] = 0u;
     if (threadIdx.x == 0) hist_guard = 0u;
@@ -404,8 +523,10 @@ __global__ void __launch_bounds__(kBlock) fs_enum_kernel(const KParams P) {
   using KT = typename std::conditional<KTAB, KTabSmem, KTabArith>::type;
   KT kt;
   if constexpr (KTAB) {
-    kt.base = (uint32_t)__cvta_generic_to_shared(ktab_s);
+    kt.base = ktab_base;
     kt.adv = kt.base + 4u * c.adv_off;
+    pin(kt.base);
+    pin(kt.adv);
   }
   const int lane = threadIdx.x & 31;
   Lane<D> st;
@@ -442,9 +563,7 @@ __global__ void __launch_bounds__(kBlock) fs_enum_kernel(const KParams P) {
   // per-warp slot table of the M1 flush, after the staging buffers
   unsigned char *wslot = stage + kBlock * kLaneStride + (threadIdx.x >> 5) * 32;
   EmitCompact<D, B> e_cmp;
-  e_cmp.buf = stage + (threadIdx.x >> 5) * kWarpBuf;
-  e_cmp.wrows = 0;
-  if (CONS == kConsRowsAny) e_cmp.init(c);
+  e_cmp.init(c, stage + (threadIdx.x >> 5) * kWarpBuf);
 
   for (;;) {
     const bool need = alive && needs_refill<D, ALPHA>(st, budget);
@@ -497,6 +616,7 @@ __global__ void __launch_bounds__(kBlock) fs_enum_kernel(const KParams P) {
             if (CAND) enter_candidates<D>(st, c);
             sync_k<D, ALPHA>(st, budget);
             if (CONS == FS_CONSUMER_ROWS) e_rows.start((u - P.unit0) * (uint64_t)EmitRows<D, B>::kRB);
+            if (cfast) e_count.n += take_entry_rows<D>(st, c);
           }
         }
       }
@@ -519,6 +639,9 @@ __global__ void __launch_bounds__(kBlock) fs_enum_kernel(const KParams P) {
       const bool had = budget != 0;
       // UNROLL branch-free fast steps, then one (warp-uniform) check for lanes parked on an
       // ascend; the rare slow lanes run the generic successor step together.
+      if (cfast) {
+        cc_group<D, UNROLL>(st, c, ktab_base + 4u * c.cadv_off, e_count.n);
+      } else {
 #pragma unroll
       for (int u = 0; u < UNROLL; ++u) {
         if (CONS == FS_CONSUMER_COUNT) {
@@ -543,6 +666,7 @@ __global__ void __launch_bounds__(kBlock) fs_enum_kernel(const KParams P) {
           fast_step<D, NEED_AD, ALPHA>(st, c, kt, budget, e_rows);
         }
       }
+      }
       if (CONS == kConsRowsAny && EmitCompact<D, B>::kCap >= 32u * UNROLL + 8u) e_cmp.flush(P, false, 32u * UNROLL);
       if (CONS == FS_CONSUMER_ROWS) {
         if (had && budget == 0) rows_slice_done(P, e_rows, fin, fin_soff, fin_goff, fin_len);
@@ -557,6 +681,7 @@ __global__ void __launch_bounds__(kBlock) fs_enum_kernel(const KParams P) {
           slow_step<D, NEED_AD, ALPHA>(st, c, kt, budget);
           if (CAND) enter_candidates<D>(st, c);
           sync_k<D, ALPHA>(st, budget);
+          if (cfast) e_count.n += take_entry_rows<D>(st, c);
           if (CONS == FS_CONSUMER_ROWS && budget == 0) rows_slice_done(P, e_rows, fin, fin_soff, fin_goff, fin_len);
         }
         if (CONS == FS_CONSUMER_ROWS) {

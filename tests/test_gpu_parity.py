@@ -92,8 +92,11 @@ def test_tiny_slices(oracle_mod, inst, T):
 def test_count_closed_tail(oracle_mod, inst):
     n, g = inst.n, inst.gens
     want = oracle.count(n, g)
-    for T in (0, 1, 5):
-        assert api.fs_count_ex(n, g, slice_units=T, tail=L.FS_TAIL_CLOSED) == want
+    for go in (L.FS_GENORDER_GIVEN, L.FS_GENORDER_AUTO):
+        for T in (0, 1, 5, 37):
+            assert api.fs_count_ex(n, g, slice_units=T, tail=L.FS_TAIL_CLOSED, gen_order=go) == want
+        parts = [api.fs_count_ex(n, g, rank=r, world=3, tail=L.FS_TAIL_CLOSED, gen_order=go) for r in range(3)]
+        assert sum(parts) == want
 
 
 @pytest.mark.parametrize("inst", ALL, ids=ids)
