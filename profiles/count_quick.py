@@ -15,8 +15,11 @@ tag = sys.argv[1] if len(sys.argv) > 1 else ""
 stream = torch.cuda.current_stream()
 res = []
 for inst in (W.C3, W.C5):
+    T = int(os.environ.get("FS_T", "0"))
+    if T and inst.name != "C3":
+        T = 0
     p = api.Plan(inst.n, inst.gens, L.FS_CONSUMER_COUNT, tail=L.FS_TAIL_CLOSED, gen_order=L.FS_GENORDER_AUTO,
-                 stream=stream.cuda_stream)
+                 stream=stream.cuda_stream, slice_units=T)
     out = torch.zeros(1, dtype=torch.int64, device="cuda")
     ts = []
     for r in range(7):
