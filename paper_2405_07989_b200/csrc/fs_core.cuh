@@ -70,7 +70,9 @@ struct Consts {
   uint32_t alpha, beta;  // units per node entry / per row
   uint32_t ktab_len;     // 0: k0 by arithmetic; else words of the node tables (below)
   uint32_t adv_off;      // word offset of the advance table inside ktab (8 B aligned)
-  uint32_t cadv_off;     // word offset of the count-only group table (0: none; see fs_host.cu)
+  uint32_t cadv_off;     // word offset of the closed-tail group table (0: none; see fs_host.cu)
+  uint32_t cadv_words;   // words per group-table entry: 2 (count, packed histogram) or 4 (histogram)
+  uint32_t cadv_packed;  // histogram entry {link, (s - k0) | (ad0 - k0 + 2^15) << 16}
   uint32_t mhi;          // ceil(2^32 / s) for the group table's umulhi division
   int32_t dl;            // t - s: change of a row's length from one valid a_{d-1} to the next
   uint32_t dstride;      // stride of the closed-tail length-difference array (|dl|, or 1 if 0)

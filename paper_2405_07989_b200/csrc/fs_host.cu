@@ -171,27 +171,49 @@ int fs_validate_and_build(fs_plan *p, uint64_t n, const uint32_t *gens, int d, i
         p->ktab[adv_off + 2 * rho + 1] = w.k0;
       }
       c.adv_off = adv_off;
-      // Count-only closed-tail group table (count + tail=closed): per residue rho the entry
-      // {rel | (q + carry) << kCAdvShift, s - k0(next)} where rel = byte offset of next's
+      // Closed-tail group tables (count or histogram + tail=closed): per residue rho the entry
+      // {rel | (q + carry) << kCAdvShift, s - k0(next)} (count, 8 B), followed for the
+      // histogram by {ad0(next) - k0(next), 0} (16 B), where rel = byte offset of next's
       // entry from the table start (the kernel adds its shared-memory base when it copies
-      // the table, so one LDS.64 yields the next entry's address directly) and s - k0 is the
-      // row count's numerator offset (kNone -> INT32_MIN: no rows); 16 KB of the 64 KB
-      // offset field are left for the table's shared-memory base.  Exact division by
-      // umulhi(x, ceil(2^32 / s)) needs x s < 2^32 for x <= n / g_{d-1} + s.
+      // the table, so one shared load yields the next entry's address directly), s - k0 is
+      // the row count's numerator offset (kNone -> INT32_MIN: no rows) and
+      // ad0 = (k0 g_{d-1} + rho) / g_d is a_d of the node's first row minus nothing: the
+      // first row's length is lsum + A + ad0 - k0.  16 KB of the 64 KB offset field are left
+      // for the table's shared-memory base.  Exact division by umulhi(x, ceil(2^32 / s))
+      // needs x s < 2^32 for x <= n / g_{d-1} + s.
       const uint64_t xmax = n / c.gA + c.s;
-      const uint32_t cadv_off = (uint32_t)p->ktab.size();
-      if (consumer == FS_CONSUMER_COUNT && e.tail == FS_TAIL_CLOSED && L >= 1 && c.s >= 2 &&
+      const bool want_hist = consumer == FS_CONSUMER_HIST;
+      // histogram entries pack s - k0 and ad0 - k0 (biased by 2^15) into one word when no
+      // residue lacks a first row (gcd(g_{d-1}, g_d) = 1) and both fit 16 bits
+      bool packed = want_hist && c.h == 1 && c.s < 65536u;
+      for (uint32_t rho = 0; packed && rho < c.gA; ++rho) {
+        const uint32_t k0 = fs::k0_arith(rho, c);
+        const int64_t dv = (int64_t)((k0 * (uint64_t)c.gA + rho) / c.gB) - (int64_t)k0;
+        if (k0 == fs::kNone || dv < -32768 || dv > 32767) packed = false;
+      }
+      const uint32_t cw = want_hist && !packed ? 4u : 2u;  // words per entry
+      const uint32_t cadv_off = ((uint32_t)p->ktab.size() + 3u) & ~3u;
+      if ((consumer == FS_CONSUMER_COUNT || want_hist) && e.tail == FS_TAIL_CLOSED && L >= 1 && c.s >= 2 &&
           xmax * c.s < (1ull << 32) && c.q + 1u < (1u << (32 - fs::kCAdvShift)) &&
-          4ull * cadv_off + 8ull * c.gA + 16384ull <= (1ull << fs::kCAdvShift)) {
-        p->ktab.resize(cadv_off + 2u * c.gA, 0u);
+          4ull * cadv_off + 4ull * cw * c.gA + 16384ull <= (1ull << fs::kCAdvShift)) {
+        p->ktab.resize(cadv_off + cw * c.gA, 0u);
         const fs::KTabArith ar{};
         for (uint32_t rho = 0; rho < c.gA; ++rho) {
           const fs::Adv w = ar.step(rho, c);
-          p->ktab[cadv_off + 2 * rho] = (4u * cadv_off + 8u * w.next) | (w.inc << fs::kCAdvShift);
-          p->ktab[cadv_off + 2 * rho + 1] =
-              w.k0 == fs::kNone ? 0x80000000u : (uint32_t)((int32_t)c.s - (int32_t)w.k0);
+          uint32_t *ent = &p->ktab[cadv_off + cw * rho];
+          ent[0] = (4u * cadv_off + 4u * cw * w.next) | (w.inc << fs::kCAdvShift);
+          ent[1] = w.k0 == fs::kNone ? 0x80000000u : (uint32_t)((int32_t)c.s - (int32_t)w.k0);
+          if (packed) {
+            const uint32_t ad0 = (w.k0 * c.gA + w.next) / c.gB;
+            ent[1] = (c.s - w.k0) | ((ad0 - w.k0 + 32768u) << 16);
+          } else if (want_hist) {
+            const uint32_t ad0 = w.k0 == fs::kNone ? 0u : (w.k0 * c.gA + w.next) / c.gB;
+            ent[2] = w.k0 == fs::kNone ? 0u : ad0 - w.k0;
+          }
         }
         c.cadv_off = cadv_off;
+        c.cadv_words = cw;
+        c.cadv_packed = packed ? 1u : 0u;
         c.mhi = (uint32_t)(((1ull << 32) + c.s - 1) / c.s);
       }
       c.ktab_len = (uint32_t)p->ktab.size();

@@ -27,6 +27,7 @@ constexpr uint32_t kStageBytes = 2 * kHalf + 64;  // 192 B usable per lane
 constexpr uint32_t kLaneStride = kStageBytes + 4;
 constexpr uint32_t kKtabMax = 2048;  // node tables in shared memory if g_{d-1} <= this (<= 24 KB)
 constexpr uint32_t kHistSmemMax = 24576;  // u32 histogram bins kept in shared memory
+constexpr uint32_t kHistRepBytes = 49152; // lane-private difference-array copies if they fit in this
 constexpr int kConsRowsAny = 4;           // internal consumer: materialise, order = any (M2)
 #ifndef FS_WARPBUF
 #define FS_WARPBUF 6144
@@ -68,6 +69,7 @@ struct KParams {
   // values stored as two's-complement u64), resolved by the finalize kernel
   unsigned long long *diff_out;
   uint32_t diff_len;
+  uint32_t hist_rep;  // closed-tail histogram: 32 = one difference-array copy per lane (bank-private), else 1
 };
 
 }  // namespace fs

@@ -56,17 +56,18 @@ struct EmitCount {
 // difference array (shared-memory u32 with wrap-around, or global u64) replace one per row.
 template <int D>
 struct EmitHistClosed {
-  uint32_t *diff;
+  uint32_t *diff;  // shared: this lane's copy (index i at diff[i * rep])
   unsigned long long *gdiff;
   uint32_t smem;
+  uint32_t rep;    // shared copies (1, or 32 lane-private ones)
   uint32_t n;
   __device__ __forceinline__ void node(bool em, const Lane<D> &st, const Consts &c, uint32_t rows) {
     if (!em) return;
     uint32_t lo, hi, v;
     hist_diff_updates<D>(st, c, rows, lo, hi, v);
     if (smem) {
-      atomicAdd(&diff[lo], v);
-      atomicAdd(&diff[hi], 0u - v);
+      atomicAdd(&diff[lo * rep], v);
+      atomicAdd(&diff[hi * rep], 0u - v);
     } else {
       atomicAdd(&gdiff[lo], (unsigned long long)v);
       atomicAdd(&gdiff[hi], 0ull - (unsigned long long)v);
@@ -454,6 +455,14 @@ __device__ __forceinline__ uint32_t take_entry_rows(Lane<D> &st, const Consts &c
   return divq((uint32_t)(x > 0 ? x : 0), c.dvS);
 }
 
+template <int D, class E>
+__device__ __forceinline__ void take_entry_hist(Lane<D> &st, const Consts &c, E &e) {
+  const bool em = st.cur >= 0;
+  const uint32_t rows = divq((uint32_t)(em ? st.cur : 0), c.dvS) + 1u;
+  e.node(em, st, c, rows);
+  st.cur = -1;
+}
+
 template <int D, int G>
 __device__ __forceinline__ void cc_group(Lane<D> &st, const Consts &c, uint32_t tab, uint32_t &cnt) {
   if constexpr (D >= 3) {
@@ -481,6 +490,94 @@ __device__ __forceinline__ void cc_group(Lane<D> &st, const Consts &c, uint32_t 
   }
 }
 
+// Length histogram with the closed tail, group form (Consts::cadv_off set for a histogram
+// plan): per node one shared load gives the next entry's address, the quotient increment,
+// s - k0 and ad0 - k0 (packed into one word when both fit 16 bits), so the node's first-row
+// length is l0 = lsum + A + (ad0 - k0) with lsum = lsum0 - 1 - u at step u, and its lengths
+// l0 + j (t - s), j < rows, are two updates of the strided difference array, done only by
+// valid steps of nodes with rows (ptxas never predicates ATOMS, so this is a short branch;
+// unconditional updates of rowless / masked steps measured 23 % slower: the shared atomics
+// bound this kernel).  With KParams::hist_rep = 32 every lane updates its own bank-private
+// copy (index i of lane l at word 32 i + l), which removed the bank conflicts (8e9 -> 7e7 on
+// C4).
+struct HcConsts {
+  uint32_t dbase;  // shared address of this lane's copy of diff[0]
+  uint32_t dstr;   // bytes between consecutive indices (4 * copies)
+  uint32_t sstr;   // dstr * |t - s|: address step of one row along the length progression
+};
+__device__ __forceinline__ HcConsts hc_consts(const Consts &c, uint32_t diff, uint32_t rep) {
+  HcConsts k;
+  k.dbase = diff + (rep > 1u ? 4u * (threadIdx.x & 31u) : 0u);
+  k.dstr = 4u * rep;
+  k.sstr = k.dstr * (uint32_t)(c.dl < 0 ? -c.dl : c.dl);
+  return k;
+}
+
+// DLS = sign of t - s.  The node's lengths l0 + j (t - s), j < rows, as difference updates:
+//   t > s: +1 at l0, -1 at l0 + rows (t - s);  t < s: -1 at l0 + (s - t), +1 at that minus
+//   rows (s - t);  t = s: +rows at l0, -rows at l0 + 1.
+template <int D, int G, bool PACKED, int DLS>
+__device__ __forceinline__ void hc_group(Lane<D> &st, const Consts &c, uint32_t tab, const HcConsts &k,
+                                         uint32_t &nrows) {
+  if constexpr (D >= 3) {
+    constexpr uint32_t kEnt = PACKED ? 8u : 16u;
+    uint32_t h = tab + kEnt * st.rho;
+    uint32_t A = st.A;
+    const uint32_t kk = st.k;
+    // address of index l0 is base0 + dstr * (A + w2 - u): l0 = lsum0 - 1 - u + A + (ad0 - k0)
+    const uint32_t bofs = st.lsum - 1u - (PACKED ? 32768u : 0u) + (DLS < 0 ? (uint32_t)(-c.dl) : 0u);
+    const uint32_t base0 = k.dbase + k.dstr * bofs;
+    uint32_t n = nrows;
+#pragma unroll
+    for (int u = 0; u < G; ++u) {
+      uint32_t w0, w1, w2;
+      if (PACKED) {
+        uint32_t p1;
+        asm("ld.shared.v2.u32 {%0, %1}, [%2];" : "=r"(w0), "=r"(p1) : "r"(h));
+        w1 = p1 & 0xffffu;  // s - k0 >= 1: no residue lacks a row
+        w2 = p1 >> 16;      // ad0 - k0 + 2^15
+      } else {
+        uint32_t w3;
+        asm("ld.shared.v4.u32 {%0, %1, %2, %3}, [%4];" : "=r"(w0), "=r"(w1), "=r"(w2), "=r"(w3) : "r"(h));
+        (void)w3;
+      }
+      h = w0 & ((1u << kCAdvShift) - 1u);
+      A += w0 >> kCAdvShift;
+      const int32_t y = (int32_t)(A + w1);
+      const uint32_t rows = __umulhi((uint32_t)(y > 0 ? y : 0), c.mhi);
+      if ((uint32_t)u < kk && rows != 0u) {  // valid step with rows: both updates
+        n += rows;
+        const uint32_t a0 = base0 + k.dstr * (A + w2 - (uint32_t)u);  // l0 (t < s: l0 + s - t)
+        if (DLS > 0) {
+          asm volatile("red.shared.add.u32 [%0], %1;" ::"r"(a0), "r"(1u) : "memory");
+          asm volatile("red.shared.add.u32 [%0], %1;" ::"r"(a0 + rows * k.sstr), "r"(0xffffffffu) : "memory");
+        } else if (DLS < 0) {
+          asm volatile("red.shared.add.u32 [%0], %1;" ::"r"(a0 - rows * k.sstr), "r"(1u) : "memory");
+          asm volatile("red.shared.add.u32 [%0], %1;" ::"r"(a0), "r"(0xffffffffu) : "memory");
+        } else {
+          asm volatile("red.shared.add.u32 [%0], %1;" ::"r"(a0), "r"(rows) : "memory");
+          asm volatile("red.shared.add.u32 [%0], %1;" ::"r"(a0 + k.dstr), "r"(0u - rows) : "memory");
+        }
+      }
+    }
+    nrows = n;
+    st.rho = (h - tab) / kEnt;
+    st.A = A;
+    st.k = kk > (uint32_t)G ? kk - (uint32_t)G : 0u;
+  }
+}
+
+template <int D, int G, bool PACKED>
+__device__ __forceinline__ void hc_group_dl(Lane<D> &st, const Consts &c, uint32_t tab, const HcConsts &k,
+                                            uint32_t &nrows) {
+  if (c.dl > 0)
+    hc_group<D, G, PACKED, 1>(st, c, tab, k, nrows);
+  else if (c.dl < 0)
+    hc_group<D, G, PACKED, -1>(st, c, tab, k, nrows);
+  else
+    hc_group<D, G, PACKED, 0>(st, c, tab, k, nrows);
+}
+
 template <int D, int CONS, int B, bool KTAB>
 __global__ void __launch_bounds__(kBlock, (CONS == kConsRowsAny ? 4 : CONS == kConsCountClosed ? FS_CC_MINB : 1))
     fs_enum_kernel(const KParams P) {
@@ -493,7 +590,9 @@ __global__ void __launch_bounds__(kBlock, (CONS == kConsRowsAny ? 4 : CONS == kC
   // ROWS: a lane completes at most one ring half in kHalf / row_bytes steps, so the warp
   // flushes pending halves once per that many steps.
   constexpr int kRowsPerHalf = (int)(kHalf / (D * (B / 8))) > 0 ? (int)(kHalf / (D * (B / 8))) : 1;
-  constexpr int UNROLL = CONS == FS_CONSUMER_ROWS ? kRowsPerHalf : (CONS == kConsCountClosed ? FS_CC_GROUP : 4);
+  constexpr int UNROLL = CONS == FS_CONSUMER_ROWS                               ? kRowsPerHalf
+                         : (CONS == kConsCountClosed || CONS == kConsHistClosed) ? FS_CC_GROUP
+                                                                                 : 4;
   extern __shared__ __align__(16) unsigned char smem[];
   __shared__ unsigned int hist_guard;
   const Consts &c = P.c;
@@ -503,15 +602,16 @@ __global__ void __launch_bounds__(kBlock, (CONS == kConsRowsAny ? 4 : CONS == kC
   uint32_t *hist_s = ktab_s + kt_words;
   const uint32_t hist_words =
       !(HISTLIKE && P.hist_smem) ? 0u
-      : ((CONS == kConsHistClosed ? P.diff_len : P.hist_len) + 3u) & ~3u;
+      : ((CONS == kConsHistClosed ? (P.diff_len + 1u) * P.hist_rep : P.hist_len) + 3u) & ~3u;
   unsigned char *stage = reinterpret_cast<unsigned char *>(hist_s + hist_words);
 
   const uint32_t ktab_base = (uint32_t)__cvta_generic_to_shared(ktab_s);
   // count-only group table (closed tail): its link words get the table's shared address
   const bool cfast = KTAB && CONS == kConsCountClosed && c.cadv_off != 0 && ktab_base < 16384u;
+  const bool hfast = KTAB && CONS == kConsHistClosed && c.cadv_off != 0 && P.hist_smem && ktab_base < 16384u;
   for (uint32_t i = threadIdx.x; i < c.ktab_len; i += blockDim.x) {
     uint32_t v = c.ktab[i];
-    if (cfast && i >= c.cadv_off && !((i - c.cadv_off) & 1u)) v += ktab_base;
+    if ((cfast || hfast) && i >= c.cadv_off && (i - c.cadv_off) % c.cadv_words == 0u) v += ktab_base;
     ktab_s[i] = v;
   }
   if (HISTLIKE) {
@@ -547,7 +647,9 @@ __global__ void __launch_bounds__(kBlock, (CONS == kConsRowsAny ? 4 : CONS == kC
 
   EmitCount<D> e_count{0};
   EmitHist<D> e_hist{hist_s, P.hist_out, P.hist_smem, 0};
-  EmitHistClosed<D> e_hcl{hist_s, P.diff_out, P.hist_smem, 0};
+  const uint32_t hrep = CONS == kConsHistClosed && P.hist_rep > 1u ? P.hist_rep : 1u;
+  EmitHistClosed<D> e_hcl{hist_s + (hrep > 1u ? (threadIdx.x & 31u) : 0u), P.diff_out, P.hist_smem, hrep, 0};
+  const HcConsts hck = hc_consts(c, (uint32_t)__cvta_generic_to_shared(hist_s), hrep);
   EmitAny<D> e_any{P.pred, P.pred_arg, P.found, P.witness, false};
   EmitRows<D, B> e_rows;
   e_rows.buf = stage + threadIdx.x * kLaneStride;
@@ -583,9 +685,9 @@ __global__ void __launch_bounds__(kBlock, (CONS == kConsRowsAny ? 4 : CONS == kC
             const uint32_t old = atomicAdd(&hist_guard, rows);
             if ((old >> 30) != ((old + rows) >> 30)) {
               if (CONS == kConsHistClosed) {
-                for (uint32_t i = 0; i < P.diff_len; ++i) {
+                for (uint32_t i = 0; i < P.diff_len * hrep; ++i) {
                   const int32_t v = (int32_t)atomicExch(&hist_s[i], 0u);
-                  if (v) atomicAdd(&P.diff_out[i], (unsigned long long)(long long)v);
+                  if (v) atomicAdd(&P.diff_out[i / hrep], (unsigned long long)(long long)v);
                 }
               } else {
                 for (uint32_t i = 0; i < P.hist_len; ++i) {
@@ -617,6 +719,7 @@ __global__ void __launch_bounds__(kBlock, (CONS == kConsRowsAny ? 4 : CONS == kC
             sync_k<D, ALPHA>(st, budget);
             if (CONS == FS_CONSUMER_ROWS) e_rows.start((u - P.unit0) * (uint64_t)EmitRows<D, B>::kRB);
             if (cfast) e_count.n += take_entry_rows<D>(st, c);
+            if (hfast) take_entry_hist<D>(st, c, e_hcl);
           }
         }
       }
@@ -641,6 +744,11 @@ __global__ void __launch_bounds__(kBlock, (CONS == kConsRowsAny ? 4 : CONS == kC
       // ascend; the rare slow lanes run the generic successor step together.
       if (cfast) {
         cc_group<D, UNROLL>(st, c, ktab_base + 4u * c.cadv_off, e_count.n);
+      } else if (hfast) {
+        if (c.cadv_packed)
+          hc_group_dl<D, UNROLL, true>(st, c, ktab_base + 4u * c.cadv_off, hck, e_hcl.n);
+        else
+          hc_group_dl<D, UNROLL, false>(st, c, ktab_base + 4u * c.cadv_off, hck, e_hcl.n);
       } else {
 #pragma unroll
       for (int u = 0; u < UNROLL; ++u) {
@@ -682,6 +790,7 @@ __global__ void __launch_bounds__(kBlock, (CONS == kConsRowsAny ? 4 : CONS == kC
           if (CAND) enter_candidates<D>(st, c);
           sync_k<D, ALPHA>(st, budget);
           if (cfast) e_count.n += take_entry_rows<D>(st, c);
+          if (hfast) take_entry_hist<D>(st, c, e_hcl);
           if (CONS == FS_CONSUMER_ROWS && budget == 0) rows_slice_done(P, e_rows, fin, fin_soff, fin_goff, fin_len);
         }
         if (CONS == FS_CONSUMER_ROWS) {
@@ -716,8 +825,10 @@ __global__ void __launch_bounds__(kBlock, (CONS == kConsRowsAny ? 4 : CONS == kC
   if (CONS == kConsHistClosed && P.hist_smem) {
     __syncthreads();
     for (uint32_t i = threadIdx.x; i < P.diff_len; i += blockDim.x) {
-      const int32_t v = (int32_t)hist_s[i];
-      if (v) atomicAdd(&P.diff_out[i], (unsigned long long)(long long)v);
+      int64_t v = 0;
+      for (uint32_t j = 0; j < hrep; ++j)  // lane-private copies, rotated so lanes hit distinct banks
+        v += (int32_t)hist_s[i * hrep + ((j + threadIdx.x) & (hrep - 1u))];
+      if (v) atomicAdd(&P.diff_out[i], (unsigned long long)v);
     }
   }
 }
@@ -766,7 +877,8 @@ static __global__ void fs_hist_finalize_kernel(const unsigned long long *diff, u
 static size_t smem_bytes(const KParams &kp, int consumer) {
   size_t b = (size_t)((kp.c.ktab_len + 3u) & ~3u) * 4;
   if (consumer == FS_CONSUMER_HIST && kp.hist_smem) b += (size_t)((kp.hist_len + 3u) & ~3u) * 4;
-  if (consumer == kConsHistClosed && kp.hist_smem) b += (size_t)((kp.diff_len + 3u) & ~3u) * 4;
+  if (consumer == kConsHistClosed && kp.hist_smem)
+    b += (size_t)(((kp.diff_len + 1u) * (kp.hist_rep > 1u ? kp.hist_rep : 1u) + 3u) & ~3u) * 4;
   if (consumer == FS_CONSUMER_ROWS) b += (size_t)kBlock * kLaneStride + (kBlock / 32) * 32;
   if (consumer == kConsRowsAny) b += (size_t)(kBlock / 32) * kWarpBuf;
   return b;

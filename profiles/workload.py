@@ -16,9 +16,8 @@ from paper_2405_07989_b200 import api  # noqa: E402
 from paper_2405_07989_b200 import workloads as W  # noqa: E402
 
 
-def main():
-    name = sys.argv[1]
-    reps = int(sys.argv[2]) if len(sys.argv) > 2 else 2
+def build(name):
+    """A callable launching the workload once."""
     if name in ("c3count", "c3closed", "c5count", "c3auto", "c3autoclosed"):
         inst = W.C5 if name == "c5count" else W.C3
         p = api.Plan(inst.n, inst.gens, L.FS_CONSUMER_COUNT, tail=1 if "closed" in name else 0,
@@ -45,6 +44,24 @@ def main():
         fn = lambda: p.enumerate_async(16, out, rows)
     else:
         raise SystemExit("unknown workload " + name)
+    return fn
+
+
+def main():
+    name = sys.argv[1]
+    reps = int(sys.argv[2]) if len(sys.argv) > 2 else 2
+    fn = build(name)
+    if os.environ.get("FS_TIME"):  # diagnostic timing (CUDA events), never under ncu
+        ts = []
+        for _ in range(reps):
+            a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            a.record()
+            fn()
+            b.record()
+            torch.cuda.synchronize()
+            ts.append(round(a.elapsed_time(b), 3))
+        print(name, "ms", ts)
+        return
     for _ in range(reps):
         fn()
     torch.cuda.synchronize()
