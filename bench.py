@@ -514,7 +514,8 @@ def extras(args, world, rank, local, dev, stream, peaks, peaks_kind, barrier, ma
             pk_tops = max(v["tops"] for v in mb.values() if isinstance(v, dict))
             ex[key]["roofline"] = {"bound": "alu", "achieved": ach, "peak": pk_tops, "unit": "Tops/s",
                                    "frac": ach / pk_tops}
-    for order_name, pk in (("", {}), ("_auto_order", {"gen_order": AUTO})):
+    for order_name, pk in (("", {}), ("_auto_order", {"gen_order": AUTO}),
+                           ("_auto_order_closed", {"gen_order": AUTO, "tail": L.FS_TAIL_CLOSED})):
         pa = api.Plan(W.C5.n, W.C5.gens, L.FS_CONSUMER_ANY, **pk, **kw)
         for name, pred, arg in (("P_late", L.FS_PRED_LEN_LE, 20), ("P_none", L.FS_PRED_LEN_LE, 19),
                                 ("P_first", L.FS_PRED_LEN_GE, 19995)):
@@ -522,7 +523,7 @@ def extras(args, world, rank, local, dev, stream, peaks, peaks_kind, barrier, ma
                 pa.any_async(pred, arg, f, w)
                 allreduce(f, dist.ReduceOp.MAX if world > 1 else None)
 
-            ms = _time_ms(any_step, stream, 1, barrier, max_over_ranks)
+            ms = _time_ms(any_step, stream, 3, barrier, max_over_ranks)
             ex["c5_any_%s%s" % (name, order_name)] = {"pred": [pred, arg], "found": bool(f.item()), "ms": ms}
     return ex
 

@@ -90,10 +90,13 @@ enum {
  *               exact canonical offset; FS_ORDER_ANY (1) compacts rows per warp with
  *               warp-aggregated atomics into an arbitrary order (the same multiset of rows;
  *               requires cap >= the rank's rows, else FS_ERANGE).
- *   tail        count consumer only: FS_TAIL_ROWS (0, default) steps through every valid
+ *   tail        count / histogram / any: FS_TAIL_ROWS (0, default) steps through every valid
  *               factorization of a node (one modulo-skip step per row); FS_TAIL_CLOSED (1)
- *               counts a node's rows in O(1) as floor(a* / s) + 1 (the
- *               closed form of the paper's suffix-set idea).  Same result.
+ *               takes a node's rows at once (the closed form of the
+ *               paper's suffix-set idea): the count adds floor(a* / s) + 1,
+ *               the histogram adds the node's length progression l0 + j (t - s) as two
+ *               difference-array updates, the any-predicate tests the progression's extreme
+ *               row (or solves LEN_EQ for j).  Same result.
  *               Count-only ablations of PAPER.md Alg. 3.1's index-(d-1) loop (SURVEY 8(a)
  *               A6, E2): FS_TAIL_SKIP_OFF (2) visits every candidate a_{d-1} and tests it;
  *               FS_TAIL_SKIP_PAPER (3) adds the paper's modulo jump after a valid candidate.
@@ -125,7 +128,7 @@ enum { FS_GENORDER_GIVEN = 0, FS_GENORDER_AUTO = 1 };
  * north_star entry points: current CUDA device, default stream, whole instance.
  * All are synchronous: they return after the result is available.  They pick the fastest
  * exact configuration: fs_count / fs_length_set / fs_any run the stream with
- * gen_order = FS_GENORDER_AUTO (and fs_count with tail = FS_TAIL_CLOSED); fs_enumerate
+ * gen_order = FS_GENORDER_AUTO and tail = FS_TAIL_CLOSED; fs_enumerate
  * keeps the caller's generator order (it defines the canonical row order).  The _ex
  * variants run exactly the configuration their fs_exec_t asks for.
  * --------------------------------------------------------------------------------- */

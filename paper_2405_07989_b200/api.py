@@ -116,9 +116,9 @@ def fs_length_set_ex(n, gens, hist=None, *, device=None, stream=None, rank=0, wo
 
 
 def fs_any_ex(n, gens, pred, pred_arg, *, device=None, stream=None, rank=0, world=1, slice_units=0,
-              ctas_per_sm=0, gen_order=L.FS_GENORDER_GIVEN):
+              ctas_per_sm=0, gen_order=L.FS_GENORDER_GIVEN, tail=L.FS_TAIL_ROWS):
     g, d = L.gens_array(gens)
-    ex = _exec(device, _stream_handle(stream), rank, world, slice_units, ctas_per_sm, 0, 0, gen_order)
+    ex = _exec(device, _stream_handle(stream), rank, world, slice_units, ctas_per_sm, 0, tail, gen_order)
     found = ctypes.c_int(0)
     wit = (ctypes.c_uint32 * max(1, d))()
     L.check(L.lib().fs_any_ex(int(n), g, d, ctypes.byref(ex), int(pred), int(pred_arg), ctypes.byref(found),

@@ -202,7 +202,9 @@ int fs_plan_any_async(fs_plan *p, int pred, uint64_t pred_arg, int *found_dev, u
   kp.permute = 1;
   kp.claim_bits = bits;
   kp.num_claims = kp.num_slices ? (1ull << bits) : 0;
-  return finish(p, fs_launch(p, FS_CONSUMER_ANY, 16, kp, p->stream));
+  // closed tail: each node decided at once (any_closed_pick), a kernel of its own
+  return finish(p, fs_launch(p, p->ex.tail == FS_TAIL_CLOSED ? fs::kConsAnyClosed : FS_CONSUMER_ANY, 16, kp,
+                             p->stream));
 }
 
 int fs_plan_enumerate_async(fs_plan *p, int B, void *out_dev, uint64_t cap) {
@@ -318,6 +320,7 @@ int fs_any(uint64_t n, const uint32_t *gens, int d, int pred, uint64_t pred_arg,
   ex.device = -1;
   ex.world = 1;
   ex.gen_order = FS_GENORDER_AUTO;
+  ex.tail = FS_TAIL_CLOSED;  // each node's rows decided at once (NEXT-1)
   return fs_any_ex(n, gens, d, &ex, pred, pred_arg, found_out, witness_or_null);
 }
 

@@ -428,6 +428,57 @@ FS_HD void fast_step_count_closed(Lane<D> &st, const Consts &c, const KT &kt, ui
   st.cur = -1;
 }
 
+// NEXT-1 for the any-predicate (fs_any): a node's rows j < rows are (a_1..a_L, a* - j s,
+// ad* + j t) with lengths l0 + j (t - s), so each predicate of fs_any holds for some row of the
+// node iff it holds at the row where the tested quantity is extreme -- or, for LEN_EQ, at the
+// one j solving l0 + j (t - s) = X.  Decided in O(1) per node; jw = a witness row's index.
+// (COORD_GE's coordinate index is the stream's internal index, remapped on the host.)
+template <int D>
+FS_HD bool any_closed_pick(const Lane<D> &st, const Consts &c, uint32_t rows, int pred, uint64_t arg,
+                           uint32_t &jw) {
+  const uint32_t ad = row_ad<D>(st, c);  // a_d of row 0 (a_{d-1} = a* = cur)
+  const int64_t l0 = (int64_t)cur_lsum<D>(st) + (int64_t)(uint32_t)st.cur + (int64_t)ad;
+  const int64_t dl = c.dl;
+  const uint32_t last = rows - 1u;
+  switch (pred) {
+    case FS_PRED_LEN_LE:
+      jw = dl >= 0 ? 0u : last;
+      return (uint64_t)(l0 + (int64_t)jw * dl) <= arg;
+    case FS_PRED_LEN_GE:
+      jw = dl > 0 ? last : 0u;
+      return (uint64_t)(l0 + (int64_t)jw * dl) >= arg;
+    case FS_PRED_LEN_EQ: {
+      if (arg >= (1ull << 40)) return false;  // lengths are < 2^32
+      const int64_t diff = (int64_t)arg - l0;
+      if (dl == 0) {
+        jw = 0u;
+        return diff == 0;
+      }
+      if (diff % dl != 0) return false;
+      const int64_t j = diff / dl;
+      if (j < 0 || j > (int64_t)last) return false;
+      jw = (uint32_t)j;
+      return true;
+    }
+    default: {
+      const uint32_t i = (uint32_t)(arg >> 32), k = (uint32_t)(arg & 0xffffffffu);
+      if (i + 2u < (uint32_t)D) {
+        jw = 0u;
+        return cur_coord<D>(st, (int)i) >= k;
+      }
+      if (i + 2u == (uint32_t)D) {  // a_{d-1}: largest at row 0
+        jw = 0u;
+        return (uint32_t)st.cur >= k;
+      }
+      if (i + 1u == (uint32_t)D) {  // a_d: largest at the last row
+        jw = last;
+        return (uint64_t)ad + (uint64_t)last * c.t >= (uint64_t)k;
+      }
+      return false;
+    }
+  }
+}
+
 struct NodeCount {
   uint32_t n;
   template <int D>

@@ -36,6 +36,7 @@ constexpr uint32_t kWarpBuf = FS_WARPBUF;  // M2 per-warp compaction ring (bytes
 constexpr size_t kScratchBytes = 2048;    // per-plan device scratch (queue, results, M2 cursors)
 constexpr int kConsCountClosed = 5;       // internal consumer: count with the closed-form tail
 constexpr int kConsHistClosed = 6;        // internal consumer: histogram with the closed-form tail
+constexpr int kConsAnyClosed = 9;         // internal consumer: any-predicate with the closed-form tail
 constexpr int kConsCountSkipOff = 7;      // internal consumer: count, Skip=off ablation
 constexpr int kConsCountSkipPaper = 8;    // internal consumer: count, Skip=paper ablation
 

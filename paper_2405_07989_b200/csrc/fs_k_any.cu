@@ -6,3 +6,7 @@
 int fs_dispatch_any(fs_plan *p, int B, const fs::KParams &kp, cudaStream_t s, bool q, uint32_t *g) {
   (void)B; return fs::dispatch_kt<FS_CONSUMER_ANY, 16>(p, kp, s, q, g);
 }
+
+int fs_dispatch_any_closed(fs_plan *p, int B, const fs::KParams &kp, cudaStream_t s, bool q, uint32_t *g) {
+  (void)B; return fs::dispatch_kt<fs::kConsAnyClosed, 16>(p, kp, s, q, g);
+}

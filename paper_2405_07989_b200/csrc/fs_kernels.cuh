@@ -134,6 +134,20 @@ struct EmitAny {
       }
     }
   }
+  // closed tail (fast_step_closed): the node's rows decided at once (any_closed_pick)
+  __device__ __forceinline__ void node(bool em, const Lane<D> &st, const Consts &c, uint32_t rows) {
+    if (!em || hit) return;
+    uint32_t j;
+    if (!any_closed_pick<D>(st, c, rows, pred, arg, j)) return;
+    hit = true;
+    if (atomicCAS(found, 0, 1) == 0 && wit) {
+      const uint32_t ad = row_ad<D>(st, c);
+#pragma unroll
+      for (int q = 0; q < D - 2; ++q) wit[c.perm[q]] = cur_coord<D>(st, q);
+      wit[c.perm[D - 2]] = (uint32_t)st.cur - j * c.s;
+      wit[c.perm[D - 1]] = ad + j * c.t;
+    }
+  }
 };
 
 // Store one row (D coordinates, caller order) at a shared-memory address q.  B = 16: q is
@@ -585,6 +599,7 @@ __global__ void __launch_bounds__(kBlock, (CONS == kConsRowsAny ? 4 : CONS == kC
   constexpr bool COUNTLIKE = CONS == FS_CONSUMER_COUNT || CONS == kConsCountClosed || CAND;
   constexpr bool NEED_AD = !COUNTLIKE;
   constexpr bool HISTLIKE = CONS == FS_CONSUMER_HIST || CONS == kConsHistClosed;
+  constexpr bool ANYLIKE = CONS == FS_CONSUMER_ANY || CONS == kConsAnyClosed;
   constexpr int ALPHA = (CONS == FS_CONSUMER_ROWS || CONS == kConsRowsAny) ? 0 : 1;
   constexpr int INNER = Inner<CONS>::value;
   // ROWS: a lane completes at most one ring half in kHalf / row_bytes steps, so the warp
@@ -724,7 +739,7 @@ __global__ void __launch_bounds__(kBlock, (CONS == kConsRowsAny ? 4 : CONS == kC
         }
       }
     }
-    if (CONS == FS_CONSUMER_ANY) {
+    if (ANYLIKE) {
       int f = 0;
       if (lane == 0) f = *reinterpret_cast<volatile int *>(P.found);
       f = __shfl_sync(kFull, f, 0);
@@ -744,6 +759,9 @@ __global__ void __launch_bounds__(kBlock, (CONS == kConsRowsAny ? 4 : CONS == kC
       // ascend; the rare slow lanes run the generic successor step together.
       if (cfast) {
         cc_group<D, UNROLL>(st, c, ktab_base + 4u * c.cadv_off, e_count.n);
+      } else if (CONS == kConsAnyClosed) {
+#pragma unroll
+        for (int u = 0; u < UNROLL; ++u) fast_step_closed<D>(st, c, kt, budget, e_any);
       } else if (hfast) {
         if (c.cadv_packed)
           hc_group_dl<D, UNROLL, true>(st, c, ktab_base + 4u * c.cadv_off, hck, e_hcl.n);
@@ -798,7 +816,7 @@ __global__ void __launch_bounds__(kBlock, (CONS == kConsRowsAny ? 4 : CONS == kC
           warp_flush(fin, fin_soff, fin_goff, fin_len, warp_stage, P.rows_out, wslot);
         }
       }
-      if (CONS == FS_CONSUMER_ANY && e_any.hit) {
+      if (ANYLIKE && e_any.hit) {
         budget = 0;
         st.cur = -1;
         st.k = st.kb = 0;
@@ -843,7 +861,7 @@ __global__ void fs_d1_kernel(const KParams P) {
       CONS == kConsCountSkipPaper)
     atomicAdd(P.count_out, 1ull);
   if (CONS == FS_CONSUMER_HIST || CONS == kConsHistClosed) atomicAdd(&P.hist_out[x], 1ull);
-  if (CONS == FS_CONSUMER_ANY) {
+  if (CONS == FS_CONSUMER_ANY || CONS == kConsAnyClosed) {
     bool ok;
     switch (P.pred) {
       case FS_PRED_LEN_LE: ok = x <= P.pred_arg; break;

@@ -14,6 +14,7 @@ int fs_dispatch_hist_closed(fs_plan *p, int B, const fs::KParams &kp, cudaStream
 int fs_dispatch_count_skip(fs_plan *p, int B, const fs::KParams &kp, cudaStream_t s, bool q, uint32_t *g,
                           bool paper);
 int fs_dispatch_count_closed(fs_plan *p, int B, const fs::KParams &kp, cudaStream_t s, bool q, uint32_t *g);
+int fs_dispatch_any_closed(fs_plan *p, int B, const fs::KParams &kp, cudaStream_t s, bool q, uint32_t *g);
 int fs_dispatch_rowsany(fs_plan *p, int B, const fs::KParams &kp, cudaStream_t s, bool q, uint32_t *g);
 
 static int dispatch(fs_plan *p, int consumer, int B, const fs::KParams &kp, cudaStream_t s, bool q, uint32_t *g) {
@@ -21,6 +22,7 @@ static int dispatch(fs_plan *p, int consumer, int B, const fs::KParams &kp, cuda
     case FS_CONSUMER_COUNT: return fs_dispatch_count(p, B, kp, s, q, g);
     case FS_CONSUMER_HIST: return fs_dispatch_hist(p, B, kp, s, q, g);
     case FS_CONSUMER_ANY: return fs_dispatch_any(p, B, kp, s, q, g);
+    case fs::kConsAnyClosed: return fs_dispatch_any_closed(p, B, kp, s, q, g);
     case FS_CONSUMER_ROWS: return fs_dispatch_rows(p, B, kp, s, q, g);
     case fs::kConsRowsAny: return fs_dispatch_rowsany(p, B, kp, s, q, g);
     case fs::kConsCountClosed: return fs_dispatch_count_closed(p, B, kp, s, q, g);

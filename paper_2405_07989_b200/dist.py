@@ -98,7 +98,8 @@ def any_pred(n: int, gens: Sequence[int], pred: int, arg: int) -> bool:
 
     rank, world = _world()
     p = Plan(n, gens, L.FS_CONSUMER_ANY, device=torch.cuda.current_device(),
-             stream=torch.cuda.current_stream().cuda_stream, rank=rank, world=world, gen_order=L.FS_GENORDER_AUTO)
+             stream=torch.cuda.current_stream().cuda_stream, rank=rank, world=world, gen_order=L.FS_GENORDER_AUTO,
+             tail=L.FS_TAIL_CLOSED)  # same configuration as fs_any
     f = torch.zeros(1, dtype=torch.int32, device="cuda")
     p.any_async(pred, arg, f)
     return bool(combine_max(f).item())

@@ -165,14 +165,29 @@ def test_any(oracle_mod, inst):
     preds = [(L.FS_PRED_LEN_LE, lens[0] if lens else 0), (L.FS_PRED_LEN_LE, max(0, (lens[0] if lens else 1) - 1)),
              (L.FS_PRED_LEN_GE, lens[-1] if lens else 0), (L.FS_PRED_LEN_EQ, lens[len(lens) // 2] if lens else 3),
              (L.FS_PRED_COORD_GE, ((len(g) - 1) << 32) | 2), (L.FS_PRED_COORD_GE, (0 << 32) | 1)]
+    # closed tail decides LEN_EQ by solving l0 + j (t - s) = X, COORD_GE at the extreme row:
+    # every length and every coordinate index, around the attained bounds
+    d = len(g)
+    distinct = sorted(set(lens))
+    preds += [(L.FS_PRED_LEN_EQ, x) for x in distinct[:3] + distinct[-3:]]
+    preds += [(L.FS_PRED_LEN_EQ, distinct[0] - 1 if distinct else 0), (L.FS_PRED_LEN_GE, lens[-1] + 1 if lens else 1)]
+    for i in range(d):
+        top = max((r[i] for r in rows), default=0)
+        preds += [(L.FS_PRED_COORD_GE, (i << 32) | top), (L.FS_PRED_COORD_GE, (i << 32) | (top + 1))]
+    rowset = set(rows)
+    runs = [lambda pr, a: api.fs_any(n, g, pr, a),
+            lambda pr, a: api.fs_any_ex(n, g, pr, a),
+            lambda pr, a: api.fs_any_ex(n, g, pr, a, tail=L.FS_TAIL_CLOSED),
+            lambda pr, a: api.fs_any_ex(n, g, pr, a, tail=L.FS_TAIL_CLOSED, slice_units=1)]
     for pred, arg in preds:
         want = any(oracle.pred_holds(r, pred, arg) for r in rows)
-        found, wit = api.fs_any(n, g, pred, arg)
-        assert found == want, (pred, arg)
-        if found:
-            assert sum(a * b for a, b in zip(wit, g)) == n
-            assert oracle.pred_holds(wit, pred, arg)
-            assert tuple(wit) in set(rows)
+        for run in runs:
+            found, wit = run(pred, arg)
+            assert found == want, (pred, arg)
+            if found:
+                assert sum(a * b for a, b in zip(wit, g)) == n
+                assert oracle.pred_holds(wit, pred, arg)
+                assert tuple(wit) in rowset
 
 
 @pytest.mark.parametrize("inst", ALL[:40], ids=ids)
@@ -279,6 +294,13 @@ def test_c5_any_predicates():
     assert not found and wit is None
     found, wit = api.fs_any(n, g, L.FS_PRED_LEN_GE, 19995)   # P_first
     assert found and sum(wit) >= 19995 and sum(a * b for a, b in zip(wit, g)) == n
+    # the per-row tail, generator order auto (the closed tail is fs_any's default)
+    AUTO = L.FS_GENORDER_AUTO
+    found, wit = api.fs_any_ex(n, g, L.FS_PRED_LEN_LE, 20, gen_order=AUTO)
+    assert found and wit == [0, 0, 0, 0, 20]
+    assert not api.fs_any_ex(n, g, L.FS_PRED_LEN_LE, 19, gen_order=AUTO)[0]
+    found, wit = api.fs_any_ex(n, g, L.FS_PRED_LEN_EQ, 10001, gen_order=AUTO, tail=L.FS_TAIL_CLOSED)
+    assert found and sum(wit) == 10001 and sum(a * b for a, b in zip(wit, g)) == n
 
 
 def test_c2l_rows_sampled(oracle_mod):
