@@ -30,6 +30,12 @@ extern "C" {
 int fsdbg_host_model(const fs_plan *plan, uint64_t *count_out, uint64_t *hist, uint64_t hist_cap,
                      int B, void *rows, uint64_t cap, uint64_t *slice_counts, uint32_t *slice_first_row);
 
+/* The any-predicate through the same host model (plan made for FS_CONSUMER_ANY): per row with
+ * tail = FS_TAIL_ROWS, per node in closed form (the kernels' any_closed_pick) with tail =
+ * FS_TAIL_CLOSED.  *found_out = 1 iff some row satisfies pred; then witness (d host uint32,
+ * caller's coordinates, may be NULL) receives one such row.  pred/pred_arg as for fs_any. */
+int fsdbg_host_any(const fs_plan *plan, int pred, uint64_t pred_arg, int *found_out, uint32_t *witness);
+
 /* Host unranking: the lane state at unit `unit` (global unit index) -> the prefix vector
  * a_1..a_L, the row offset within the node (or -1 for the node-entry unit).  Returns
  * FS_OK.  prefix_out: uint32[d]. */

@@ -87,6 +87,7 @@ EXPORTS = {
     "fs_version": (ctypes.c_int, []),
     # test/introspection (include/fsgpu_debug.h)
     "fsdbg_host_model": (ctypes.c_int, [vp, u64p, u64p, u64, ctypes.c_int, vp, u64, u64p, u32p]),
+    "fsdbg_host_any": (ctypes.c_int, [vp, ctypes.c_int, u64, ctypes.POINTER(ctypes.c_int), u32p]),
     "fsdbg_unrank": (ctypes.c_int, [vp, u64, u32p, ctypes.POINTER(ctypes.c_int64)]),
     "fsdbg_magic": (ctypes.c_int, [ctypes.c_uint32, u32p, u32p]),
     "fsdbg_magic_div": (ctypes.c_uint32, [ctypes.c_uint32, ctypes.c_uint32]),

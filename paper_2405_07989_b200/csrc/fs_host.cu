@@ -355,9 +355,33 @@ struct HostSink {
   int64_t *diff = nullptr;
   uint32_t first[FS_MAX_D];
   bool have_first = false;
+  // any-predicate (fsdbg_host_any): pred_arg in the caller's coordinates; pred_arg_int with
+  // COORD_GE's index remapped to the stream's order (closed-form node test)
+  int pred = 0;
+  uint64_t pred_arg = 0, pred_arg_int = 0;
+  bool found = false;
+  uint32_t wit[FS_MAX_D];
+  void hit(const uint32_t *v) {  // v in the caller's coordinates
+    if (found) return;
+    found = true;
+    memcpy(wit, v, sizeof(uint32_t) * d);
+  }
   void put(const uint32_t *vi) {
     uint32_t v[FS_MAX_D];
     for (int j = 0; j < d; ++j) v[perm ? perm[j] : j] = vi[j];
+    if (pred) {
+      uint64_t len = 0;
+      for (int i = 0; i < d; ++i) len += v[i];
+      bool ok = false;
+      const uint64_t ci = pred_arg >> 32;
+      switch (pred) {
+        case FS_PRED_LEN_LE: ok = len <= pred_arg; break;
+        case FS_PRED_LEN_GE: ok = len >= pred_arg; break;
+        case FS_PRED_LEN_EQ: ok = len == pred_arg; break;
+        default: ok = ci < (uint64_t)d && v[ci] >= (uint32_t)(pred_arg & 0xffffffffu);
+      }
+      if (ok) hit(v);
+    }
     uint64_t len = 0;
     for (int i = 0; i < d; ++i) len += v[i];
     if (hist && len < hist_cap) hist[len]++;
@@ -401,6 +425,17 @@ struct HostNodeSink {
   void node(bool em, const fs::Lane<D> &st, const fs::Consts &c, uint32_t rows) {
     if (!em) return;
     n += rows;
+    if (sink->pred) {  // the kernels' closed-form any test of the node
+      uint32_t j;
+      if (fs::any_closed_pick<D>(st, c, rows, sink->pred, sink->pred_arg_int, j)) {
+        uint32_t vi[FS_MAX_D], v[FS_MAX_D];
+        for (int q = 0; q < D - 2; ++q) vi[q] = fs::cur_coord<D>(st, q);
+        vi[D - 2] = (uint32_t)st.cur - j * c.s;
+        vi[D - 1] = fs::row_ad<D>(st, c) + j * c.t;
+        for (int q = 0; q < D; ++q) v[c.perm[q]] = vi[q];
+        sink->hit(v);
+      }
+    }
     if (sink->diff) {
       uint32_t lo, hi, v;
       fs::hist_diff_updates<D>(st, c, rows, lo, hi, v);
@@ -443,10 +478,11 @@ void host_model_d(const fs_plan *p, const KT &ktab, HostSink &sink, uint64_t *sl
       }
       sink.count += cnt;
       sink.slice_rows = cnt;
-    } else if (ALPHA && (p->consumer == FS_CONSUMER_COUNT || p->consumer == FS_CONSUMER_HIST) &&
+    } else if (ALPHA &&
+               (p->consumer == FS_CONSUMER_COUNT || p->consumer == FS_CONSUMER_HIST || p->consumer == FS_CONSUMER_ANY) &&
                p->ex.tail == FS_TAIL_CLOSED) {
       HostNodeSink ns{p, &sink, 0};
-      const bool count_only = p->consumer == FS_CONSUMER_COUNT;
+      const bool count_only = p->consumer == FS_CONSUMER_COUNT && !sink.pred;
       while (!fs::needs_refill<D, ALPHA>(st, budget)) {
         if (count_only) {  // the kernels' count-only closed step
           uint32_t cnt = 0;
@@ -551,6 +587,43 @@ extern "C" int fsdbg_host_model(const fs_plan *p, uint64_t *count_out, uint64_t 
     }
   }
   if (count_out) *count_out = sink.count;
+  return FS_OK;
+}
+
+// The any-predicate through the host model: per row (tail rows) or per node in closed form
+// (tail closed, any_closed_pick), in the kernels' schedule.  *found_out and one witness row
+// (caller's coordinates; which one is unspecified, as for fs_any).
+extern "C" int fsdbg_host_any(const fs_plan *p, int pred, uint64_t pred_arg, int *found_out, uint32_t *witness) {
+  if (!p || !found_out || pred < FS_PRED_LEN_LE || pred > FS_PRED_COORD_GE) return FS_EINVAL;
+  if (p->consumer != FS_CONSUMER_ANY) return FS_EINVAL;
+  HostSink sink;
+  sink.d = p->d;
+  sink.perm = p->c.perm;
+  sink.pred = pred;
+  sink.pred_arg = pred_arg;
+  sink.pred_arg_int = pred_arg;
+  if (pred == FS_PRED_COORD_GE && (pred_arg >> 32) < (uint64_t)p->d)
+    sink.pred_arg_int = ((uint64_t)p->iperm[pred_arg >> 32] << 32) | (pred_arg & 0xffffffffull);
+  if (p->d == 1) {
+    for (uint64_t sl = 0; sl < p->num_slices; ++sl) {
+      uint32_t v = (uint32_t)(p->n / p->g[0]);
+      sink.put(&v);
+    }
+  } else {
+    switch (p->d) {
+#define FS_CASE(DD) \
+  case DD:          \
+    host_model_alpha<DD>(p, sink, nullptr, nullptr); \
+    break;
+      FS_CASE(2) FS_CASE(3) FS_CASE(4) FS_CASE(5) FS_CASE(6) FS_CASE(7) FS_CASE(8) FS_CASE(9)
+      FS_CASE(10) FS_CASE(11) FS_CASE(12) FS_CASE(13) FS_CASE(14) FS_CASE(15) FS_CASE(16)
+#undef FS_CASE
+      default:
+        return FS_EINVAL;
+    }
+  }
+  *found_out = sink.found ? 1 : 0;
+  if (sink.found && witness) memcpy(witness, sink.wit, sizeof(uint32_t) * p->d);
   return FS_OK;
 }
 

@@ -36,6 +36,18 @@ def host_model(n, gens, consumer=L.FS_CONSUMER_COUNT, *, rank=0, world=1, slice_
     return out
 
 
+def host_any(n, gens, pred, arg, *, tail=0, gen_order=0, slice_units=0, rank=0, world=1):
+    """(found, witness) of the any-predicate through the host model (per row, or per node in
+    closed form with tail=FS_TAIL_CLOSED)."""
+    p = Plan(n, gens, L.FS_CONSUMER_ANY, rank=rank, world=world, slice_units=slice_units, tail=tail,
+             gen_order=gen_order)
+    d = len(gens)
+    found = ctypes.c_int(0)
+    wit = (ctypes.c_uint32 * max(1, d))()
+    L.check(L.lib().fsdbg_host_any(p.handle, int(pred), int(arg), ctypes.byref(found), wit), "fsdbg_host_any")
+    return bool(found.value), ([int(x) for x in wit[:d]] if found.value else None)
+
+
 def unrank(plan, unit):
     d = len(plan.gens)
     pre = (ctypes.c_uint32 * max(1, d))()

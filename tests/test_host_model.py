@@ -11,7 +11,7 @@ from paper_2405_07989_b200 import _lib as L
 from paper_2405_07989_b200 import workloads as W
 from paper_2405_07989_b200.api import Plan
 
-from .fsdbg import host_model, magic, unrank
+from .fsdbg import host_any, host_model, magic, unrank
 
 
 def small_instances(count, seed, d_max=6, g_max=30, n_max=300, max_rows=20000):
@@ -101,6 +101,36 @@ def test_closed_tail_hist(oracle_mod, inst):
             r = host_model(n, g, L.FS_CONSUMER_HIST, slice_units=T, want_hist=True, tail=L.FS_TAIL_CLOSED,
                            gen_order=go)
             assert r["hist"] == want
+
+
+@pytest.mark.parametrize("inst", INSTANCES[:40] + INSTANCES[-11:], ids=lambda i: "%s" % i.name)
+def test_any_predicate_rows_and_closed(oracle_mod, inst):
+    """fs_any's decision per row (tail rows) and per node in closed form (tail closed: the
+    extreme row of the node's progression, LEN_EQ solved for j) against the oracle's rows,
+    for every predicate kind around the attained bounds, given and auto generator order."""
+    n, g = inst.n, inst.gens
+    d = len(g)
+    rows = oracle.rows_as_tuples(oracle.rows(n, g, B=32), d, 32)
+    lens = sorted(set(sum(r) for r in rows))
+    preds = [(L.FS_PRED_LEN_LE, 0), (L.FS_PRED_LEN_GE, 1 << 33), (L.FS_PRED_LEN_EQ, 1 << 41)]
+    for x in lens[:2] + lens[-2:] + lens[len(lens) // 2:len(lens) // 2 + 1]:
+        preds += [(L.FS_PRED_LEN_LE, x), (L.FS_PRED_LEN_LE, x - 1), (L.FS_PRED_LEN_GE, x), (L.FS_PRED_LEN_GE, x + 1),
+                  (L.FS_PRED_LEN_EQ, x), (L.FS_PRED_LEN_EQ, x + 1)]
+    for i in range(d):
+        top = max((r[i] for r in rows), default=0)
+        preds += [(L.FS_PRED_COORD_GE, (i << 32) | top), (L.FS_PRED_COORD_GE, (i << 32) | (top + 1)),
+                  (L.FS_PRED_COORD_GE, (i << 32) | (top // 2))]
+    rowset = set(rows)
+    for pred, arg in preds:
+        if arg < 0:
+            continue
+        want = any(oracle.pred_holds(r, pred, arg) for r in rows)
+        for tail in (L.FS_TAIL_ROWS, L.FS_TAIL_CLOSED):
+            for go in (L.FS_GENORDER_GIVEN, L.FS_GENORDER_AUTO):
+                found, wit = host_any(n, g, pred, arg, tail=tail, gen_order=go, slice_units=3)
+                assert found == want, (pred, arg, tail, go)
+                if found:
+                    assert tuple(wit) in rowset and oracle.pred_holds(wit, pred, arg)
 
 
 @pytest.mark.parametrize("inst", INSTANCES, ids=lambda i: "%s" % i.name)
