@@ -74,6 +74,7 @@ struct Consts {
   uint32_t cadv_words;   // words per group-table entry: 2 (count, packed histogram) or 4 (histogram)
   uint32_t cadv_packed;  // histogram entry {link, (s - k0) | (ad0 - k0 + 2^15) << 16}
   uint32_t mhi;          // ceil(2^32 / s) for the group table's umulhi division
+  uint32_t t2_off;       // word offset of the count's one-level ascend table (0: none; fs_host.cu)
   int32_t dl;            // t - s: change of a row's length from one valid a_{d-1} to the next
   uint32_t dstride;      // stride of the closed-tail length-difference array (|dl|, or 1 if 0)
   uint8_t perm[FS_MAX_D];  // internal coordinate j is the caller's coordinate perm[j]

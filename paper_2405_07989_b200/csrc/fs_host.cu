@@ -215,6 +215,28 @@ int fs_validate_and_build(fs_plan *p, uint64_t n, const uint32_t *gens, int d, i
         c.cadv_words = cw;
         c.cadv_packed = packed ? 1u : 0u;
         c.mhi = (uint32_t)(((1ull << 32) + c.s - 1) / c.s);
+        // Count: one-level ascend table over r = R_{L-1} mod g_L (L >= 2).  The ascend
+        // a_{L-1} -= 1, R_{L-1} += g_{L-1} moves r to r' = (r + g_{L-1}) mod g_L and the
+        // quotient Q = floor(R_{L-1} / g_L) (= the new run's a_L) up by dQ; the new run's
+        // entry node has R_L = r', hence A0 = floor(r' / g_{d-1}), rho0, and rows0 -- all
+        // functions of r.  Entry {rel(r') | dQ << 16, rho0 | A0 << 16, rows0, 0}.
+        const uint32_t gL = L >= 2 ? gens[L - 1] : 0u, gL1 = L >= 2 ? gens[L - 2] : 0u;
+        const uint32_t t2_off = (uint32_t)p->ktab.size();  // multiple of 2 words; padded to 4 below
+        const uint32_t t2o = (t2_off + 3u) & ~3u;
+        if (consumer == FS_CONSUMER_COUNT && L >= 2 && gL <= 2048u && gL1 / gL + 1u < 65536u && c.gA < 65536u &&
+            4ull * t2o + 16ull * gL + 16384ull <= (1ull << fs::kCAdvShift)) {
+          p->ktab.resize(t2o + 4u * gL, 0u);
+          for (uint32_t r = 0; r < gL; ++r) {
+            const uint32_t R2 = r + gL1, dQ = R2 / gL, r2 = R2 % gL;
+            const uint32_t A0 = r2 / c.gA, rho0 = r2 % c.gA, k0 = fs::k0_arith(rho0, c);
+            const uint32_t rows0 = (k0 == fs::kNone || k0 > A0) ? 0u : (A0 - k0) / c.s + 1u;
+            uint32_t *ent = &p->ktab[t2o + 4u * r];
+            ent[0] = (4u * t2o + 16u * r2) | (dQ << 16);
+            ent[1] = rho0 | (A0 << 16);
+            ent[2] = rows0;
+          }
+          c.t2_off = t2o;
+        }
       }
       c.ktab_len = (uint32_t)p->ktab.size();
       c.ktab = p->ktab.data();

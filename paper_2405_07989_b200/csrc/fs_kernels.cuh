@@ -477,6 +477,46 @@ __device__ __forceinline__ void take_entry_hist(Lane<D> &st, const Consts &c, E 
   st.cur = -1;
 }
 
+// Count: the one-level ascend (a_{L-1} -= 1, R_{L-1} += g_{L-1}, a_L = floor(R_{L-1}/g_L) and
+// the entry of the new run) as one LDS.128 of the ascend table (Consts::t2_off, fs_host.cu),
+// instead of two magic divisions and the k0 lookup.  t2a/q2 track r = R_{L-1} mod g_L and
+// Q = floor(R_{L-1} / g_L); t2_sync re-derives them after a refill or a deeper ascend.
+template <int D>
+__device__ __forceinline__ bool t2_can_ascend(const Lane<D> &st) {
+  if constexpr (D >= 4)
+    return st.a[D - 4] > 0u;
+  else
+    return false;
+}
+template <int D>
+__device__ __forceinline__ void t2_sync(const Lane<D> &st, const Consts &c, uint32_t t2base, uint32_t &t2a,
+                                        uint32_t &q2) {
+  if constexpr (D >= 4) {
+    constexpr int L = D - 2;
+    const uint32_t R1 = st.R[L - 2];
+    q2 = divq(R1, c.dv[L - 1]);
+    t2a = t2base + 16u * (R1 - q2 * c.g[L - 1]);
+  }
+}
+template <int D>
+__device__ __forceinline__ void t2_ascend(Lane<D> &st, const Consts &c, uint32_t &t2a, uint32_t &q2,
+                                          uint32_t &cnt) {
+  if constexpr (D >= 4) {
+    constexpr int L = D - 2;
+    const uint4 w = lds128(t2a);
+    t2a = w.x & ((1u << kCAdvShift) - 1u);
+    q2 += w.x >> 16;
+    st.a[L - 2] -= 1u;
+    st.R[L - 2] += c.g[L - 2];
+    st.a[L - 1] = q2;
+    st.lsum = st.lsum - 1u + q2;
+    st.rho = w.y & 0xffffu;
+    st.A = w.y >> 16;
+    st.cur = -1;  // the entry node's rows are taken here
+    cnt += w.z;
+  }
+}
+
 template <int D, int G>
 __device__ __forceinline__ void cc_group(Lane<D> &st, const Consts &c, uint32_t tab, uint32_t &cnt) {
   if constexpr (D >= 3) {
@@ -624,9 +664,15 @@ __global__ void __launch_bounds__(kBlock, (CONS == kConsRowsAny ? 4 : CONS == kC
   // count-only group table (closed tail): its link words get the table's shared address
   const bool cfast = KTAB && CONS == kConsCountClosed && c.cadv_off != 0 && ktab_base < 16384u;
   const bool hfast = KTAB && CONS == kConsHistClosed && c.cadv_off != 0 && P.hist_smem && ktab_base < 16384u;
+  const bool t2fast = cfast && D >= 4 && c.t2_off != 0;
+  const uint32_t t2base = ktab_base + 4u * c.t2_off;
+  uint32_t t2a = t2base, q2 = 0;  // count: ascend-table entry of r = R_{L-1} mod g_L, Q = R_{L-1} / g_L
   for (uint32_t i = threadIdx.x; i < c.ktab_len; i += blockDim.x) {
     uint32_t v = c.ktab[i];
-    if ((cfast || hfast) && i >= c.cadv_off && (i - c.cadv_off) % c.cadv_words == 0u) v += ktab_base;
+    if ((cfast || hfast) && i >= c.cadv_off && (i - c.cadv_off) % c.cadv_words == 0u &&
+        (c.t2_off == 0u || i < c.t2_off))
+      v += ktab_base;
+    if (cfast && c.t2_off != 0u && i >= c.t2_off && ((i - c.t2_off) & 3u) == 0u) v += ktab_base;
     ktab_s[i] = v;
   }
   if (HISTLIKE) {
@@ -734,6 +780,7 @@ __global__ void __launch_bounds__(kBlock, (CONS == kConsRowsAny ? 4 : CONS == kC
             sync_k<D, ALPHA>(st, budget);
             if (CONS == FS_CONSUMER_ROWS) e_rows.start((u - P.unit0) * (uint64_t)EmitRows<D, B>::kRB);
             if (cfast) e_count.n += take_entry_rows<D>(st, c);
+            if (t2fast) t2_sync<D>(st, c, t2base, t2a, q2);
             if (hfast) take_entry_hist<D>(st, c, e_hcl);
           }
         }
@@ -804,10 +851,17 @@ __global__ void __launch_bounds__(kBlock, (CONS == kConsRowsAny ? 4 : CONS == kC
       const bool slow = needs_slow<D>(st, budget);
       if (__any_sync(kFull, slow)) {
         if (slow) {
+          if (t2fast && t2_can_ascend<D>(st)) {  // one-level ascend by table (count)
+            t2_ascend<D>(st, c, t2a, q2, e_count.n);
+            budget -= 1u;
+            sync_k<D, ALPHA>(st, budget);
+          } else {
           slow_step<D, NEED_AD, ALPHA>(st, c, kt, budget);
           if (CAND) enter_candidates<D>(st, c);
           sync_k<D, ALPHA>(st, budget);
           if (cfast) e_count.n += take_entry_rows<D>(st, c);
+          if (t2fast) t2_sync<D>(st, c, t2base, t2a, q2);
+          }
           if (hfast) take_entry_hist<D>(st, c, e_hcl);
           if (CONS == FS_CONSUMER_ROWS && budget == 0) rows_slice_done(P, e_rows, fin, fin_soff, fin_goff, fin_len);
         }
