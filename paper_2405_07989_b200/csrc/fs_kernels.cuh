@@ -418,15 +418,19 @@ __device__ __forceinline__ void warp_flush(bool &pend, uint32_t soff, uint64_t g
     const uint32_t s_soff = __shfl_sync(kFull, soff, sl);
     const uint32_t s_len = __shfl_sync(kFull, len, sl);
     const uint64_t s_goff = __shfl_sync(kFull, goff, sl);
-    if (src >= 0) {
-      for (uint32_t o = (uint32_t)j * 16u; o < s_len; o += 16u * kLanesPerSeg) {
-        const uint32_t *r = reinterpret_cast<const uint32_t *>(warp_stage + src * kLaneStride + s_soff + o);
-        uint4 v;
-        v.x = r[0];
-        v.y = r[1];
-        v.z = r[2];
-        v.w = r[3];
-        __stcs(reinterpret_cast<uint4 *>(out + s_goff + o), v);
+    if (src >= 0) {  // a segment is at most 2 kHalf = 128 B: at most two 16 B chunks per lane
+#pragma unroll
+      for (int q = 0; q < (int)(2 * kHalf / (16u * kLanesPerSeg)); ++q) {
+        const uint32_t o = (uint32_t)j * 16u + (uint32_t)q * 16u * kLanesPerSeg;
+        if (o < s_len) {
+          const uint32_t *r = reinterpret_cast<const uint32_t *>(warp_stage + src * kLaneStride + s_soff + o);
+          uint4 v;
+          v.x = r[0];
+          v.y = r[1];
+          v.z = r[2];
+          v.w = r[3];
+          __stcs(reinterpret_cast<uint4 *>(out + s_goff + o), v);
+        }
       }
     }
   }
@@ -633,7 +637,9 @@ __device__ __forceinline__ void hc_group_dl(Lane<D> &st, const Consts &c, uint32
 }
 
 template <int D, int CONS, int B, bool KTAB>
-__global__ void __launch_bounds__(kBlock, (CONS == kConsRowsAny ? 4 : CONS == kConsCountClosed ? FS_CC_MINB : 1))
+__global__ void __launch_bounds__(kBlock, (CONS == kConsRowsAny || CONS == FS_CONSUMER_ROWS ? 4
+                                           : CONS == kConsCountClosed              ? FS_CC_MINB
+                                                                                   : 1))
     fs_enum_kernel(const KParams P) {
   constexpr bool CAND = CONS == kConsCountSkipOff || CONS == kConsCountSkipPaper;
   constexpr bool COUNTLIKE = CONS == FS_CONSUMER_COUNT || CONS == kConsCountClosed || CAND;
