@@ -106,7 +106,13 @@ enum {
  *               (largest generators first; "regardless of
  *               order").  Results are reported in the caller's coordinates (witnesses,
  *               COORD_GE predicates, row coordinates); canonical-order materialise always
- *               uses the given order. */
+ *               uses the given order.
+ *   rows_impl   materialise kernel: FS_ROWS_BATCH (0, default) -- every lane emits exactly
+ *               one row per step into a 16 B-aligned register batch, whole batches go to a
+ *               per-lane shared-memory slot with 16 B stores and the warp copies all 32
+ *               lanes' slots out with coalesced 16 B stores (row shapes whose batch is at
+ *               most 112 B; others use the next kernel); FS_ROWS_STAGED (1) -- the round-1
+ *               kernels (per-step emission, per-lane linear staging / per-warp ring). */
 typedef struct {
     int device;
     void *cuda_stream;
@@ -117,12 +123,14 @@ typedef struct {
     int order;
     int tail;
     int gen_order;
-    int reserved[5];
+    int rows_impl;
+    int reserved[4];
 } fs_exec_t;
 
 enum { FS_ORDER_CANONICAL = 0, FS_ORDER_ANY = 1 };
 enum { FS_TAIL_ROWS = 0, FS_TAIL_CLOSED = 1, FS_TAIL_SKIP_OFF = 2, FS_TAIL_SKIP_PAPER = 3 };
 enum { FS_GENORDER_GIVEN = 0, FS_GENORDER_AUTO = 1 };
+enum { FS_ROWS_BATCH = 0, FS_ROWS_STAGED = 1 };
 
 /* ---------------------------------------------------------------------------------
  * north_star entry points: current CUDA device, default stream, whole instance.

@@ -18,6 +18,7 @@ FS_MAX_D = 16
 FS_ORDER_CANONICAL, FS_ORDER_ANY = 0, 1
 FS_TAIL_ROWS, FS_TAIL_CLOSED, FS_TAIL_SKIP_OFF, FS_TAIL_SKIP_PAPER = 0, 1, 2, 3
 FS_GENORDER_GIVEN, FS_GENORDER_AUTO = 0, 1
+FS_ROWS_BATCH, FS_ROWS_STAGED = 0, 1
 
 u64 = ctypes.c_uint64
 i64 = ctypes.c_int64
@@ -37,7 +38,8 @@ class ExecT(ctypes.Structure):
         ("order", ctypes.c_int),
         ("tail", ctypes.c_int),
         ("gen_order", ctypes.c_int),
-        ("reserved", ctypes.c_int * 5),
+        ("rows_impl", ctypes.c_int),
+        ("reserved", ctypes.c_int * 4),
     ]
 
 

@@ -20,7 +20,7 @@ def _torch():
 
 def _exec(device: Optional[int] = None, stream=None, rank: int = 0, world: int = 1,
           slice_units: int = 0, ctas_per_sm: int = 0, order: int = 0, tail: int = 0,
-          gen_order: int = 0) -> L.ExecT:
+          gen_order: int = 0, rows_impl: int = 0) -> L.ExecT:
     ex = L.ExecT()
     ex.device = -1 if device is None else int(device)
     ex.cuda_stream = None if stream is None else ctypes.c_void_p(int(stream))
@@ -31,6 +31,7 @@ def _exec(device: Optional[int] = None, stream=None, rank: int = 0, world: int =
     ex.order = int(order)
     ex.tail = int(tail)
     ex.gen_order = int(gen_order)
+    ex.rows_impl = int(rows_impl)
     return ex
 
 
@@ -127,12 +128,15 @@ def fs_any_ex(n, gens, pred, pred_arg, *, device=None, stream=None, rank=0, worl
 
 
 def fs_enumerate_ex(n, gens, B=16, cap=None, out=None, *, device=None, stream=None, rank=0, world=1,
-                    slice_units=0, ctas_per_sm=0, order=L.FS_ORDER_CANONICAL, gen_order=L.FS_GENORDER_GIVEN):
+                    slice_units=0, ctas_per_sm=0, order=L.FS_ORDER_CANONICAL, gen_order=L.FS_GENORDER_GIVEN,
+                    rows_impl=L.FS_ROWS_BATCH):
     """This rank's block of rows.  Returns (rank_rows, global_row_offset, rows_tensor).
-    order=FS_ORDER_ANY: warp-compacted (M2) layout, same multiset of rows, arbitrary order."""
+    order=FS_ORDER_ANY: warp-compacted (M2) layout, same multiset of rows, arbitrary order.
+    rows_impl: FS_ROWS_BATCH (default) or FS_ROWS_STAGED (the round-1 kernels)."""
     torch = _torch()
     g, d = L.gens_array(gens)
-    ex = _exec(device, _stream_handle(stream), rank, world, slice_units, ctas_per_sm, order, 0, gen_order)
+    ex = _exec(device, _stream_handle(stream), rank, world, slice_units, ctas_per_sm, order, 0, gen_order,
+               rows_impl)
     if cap is None:
         info = Plan(n, gens, L.FS_CONSUMER_ROWS, rank=rank, world=world).info
         cap = info["row_end"] - info["row_begin"]
@@ -154,13 +158,14 @@ class Plan:
     def __init__(self, n: int, gens: Sequence[int], consumer: int = L.FS_CONSUMER_COUNT, *,
                  device: Optional[int] = None, stream=None, rank: int = 0, world: int = 1,
                  slice_units: int = 0, ctas_per_sm: int = 0, order: int = 0, tail: int = 0,
-                 gen_order: int = 0):
+                 gen_order: int = 0, rows_impl: int = 0):
         self.n = int(n)
         self.gens = tuple(int(x) for x in gens)
         self.consumer = consumer
         g, d = L.gens_array(gens)
         self._stream = stream
-        ex = _exec(device, _stream_handle(stream), rank, world, slice_units, ctas_per_sm, order, tail, gen_order)
+        ex = _exec(device, _stream_handle(stream), rank, world, slice_units, ctas_per_sm, order, tail, gen_order,
+                   rows_impl)
         h = ctypes.c_void_p()
         L.check(L.lib().fs_plan_create(self.n, g, d, int(consumer), ctypes.byref(ex), ctypes.byref(h)),
                 "fs_plan_create")

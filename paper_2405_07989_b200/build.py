@@ -14,8 +14,8 @@ ROOT = os.path.dirname(HERE)
 CSRC = os.path.join(HERE, "csrc")
 BUILD = os.path.join(ROOT, "build")
 LIB = os.path.join(HERE, "libfsgpu.so")
-SOURCES = ["fs_host.cu", "fs_capi.cu", "fs_launch.cu", "fs_k_count.cu", "fs_k_hist.cu", "fs_k_any.cu", "fs_k_rows.cu", "fs_k_rowsany.cu", "fs_micro.cu"]
-HEADERS = ["fs_core.cuh", "fs_internal.h", "fs_kernels.cuh"]
+SOURCES = ["fs_host.cu", "fs_capi.cu", "fs_launch.cu", "fs_k_count.cu", "fs_k_hist.cu", "fs_k_any.cu", "fs_k_rows.cu", "fs_k_rowsany.cu", "fs_k_rowsb.cu", "fs_micro.cu"]
+HEADERS = ["fs_core.cuh", "fs_internal.h", "fs_kernels.cuh", "fs_rows_batch.cuh"]
 INCLUDE = [os.path.join(ROOT, "include", h) for h in ("fsgpu.h", "fsgpu_debug.h")]
 
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")

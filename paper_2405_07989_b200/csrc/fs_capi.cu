@@ -227,6 +227,27 @@ int fs_plan_enumerate_async(fs_plan *p, int B, void *out_dev, uint64_t cap) {
   kp.num_claims = kp.num_slices;
   kp.rows_out = reinterpret_cast<unsigned char *>(out_dev);
   kp.row_bytes = (uint32_t)(p->d * (B / 8));
+  if (p->ex.rows_impl == FS_ROWS_BATCH && fs_rows_batch_supported(p, B)) {
+    // lockstep batch kernel over the full slices + the ragged-tail kernel
+    kp.num_slices = take / p->T;
+    kp.num_claims = kp.num_slices;
+    if (p->ex.order == FS_ORDER_ANY) {
+      if (take < span) return FS_ERANGE;
+      char *base = reinterpret_cast<char *>(p->scratch_dev);
+      if (cudaMemsetAsync(base + kOffFront, 0, kOffBack + 8 - kOffFront, p->stream) != cudaSuccess) return FS_ECUDA;
+      kp.front = reinterpret_cast<unsigned long long *>(base + kOffFront);
+      kp.back = reinterpret_cast<unsigned long long *>(base + kOffBack);
+      kp.rank_rows = span;
+    }
+    int launches = 0;
+    uint32_t grid = 0;
+    rc = fs_dispatch_rows_batch(p, B, p->ex.order == FS_ORDER_ANY, kp, p->stream, false, &grid, &launches);
+    if (rc != FS_OK) return rc;
+    p->grid = grid;
+    g_fs_total_launches += (unsigned long long)launches;
+    p->last_launches = launches;
+    return FS_OK;
+  }
   if (p->ex.order == FS_ORDER_ANY) {
     if (take < span) return FS_ERANGE;  // compaction writes all of the rank's rows
     char *base = reinterpret_cast<char *>(p->scratch_dev);

@@ -75,6 +75,8 @@ struct Consts {
   uint32_t cadv_packed;  // histogram entry {link, (s - k0) | (ad0 - k0 + 2^15) << 16}
   uint32_t mhi;          // ceil(2^32 / s) for the group table's umulhi division
   uint32_t t2_off;       // word offset of the count's one-level ascend table (0: none; fs_host.cu)
+  uint32_t radv_off;     // word offset of the materialise advance table (0: none; fs_host.cu):
+                         //   4 words per rho {next | inc << 11, k0(next), ad0(next), 0}
   int32_t dl;            // t - s: change of a row's length from one valid a_{d-1} to the next
   uint32_t dstride;      // stride of the closed-tail length-difference array (|dl|, or 1 if 0)
   uint8_t perm[FS_MAX_D];  // internal coordinate j is the caller's coordinate perm[j]
@@ -207,8 +209,9 @@ FS_HD uint32_t row_ad(const Lane<D> &st, const Consts &c) {
 
 // Deeper ascend of Alg. 3.1 steps 2-11: rightmost nonzero index i < L, a_i -= 1,
 // re-solve a_{i+1}..a_L greedily (floor) -- returns false at end of stream.
-template <int D>
-FS_HD bool ascend(Lane<D> &st, const Consts &c) {
+// (CC: Consts, or any struct with the same g / dv / gA / dvA members, e.g. a register copy)
+template <int D, class CC = Consts>
+FS_HD bool ascend(Lane<D> &st, const CC &c) {
   constexpr int L = D - 2;
   if constexpr (L <= 1) {
     return false;

@@ -171,6 +171,22 @@ int fs_validate_and_build(fs_plan *p, uint64_t n, const uint32_t *gens, int d, i
         p->ktab[adv_off + 2 * rho + 1] = w.k0;
       }
       c.adv_off = adv_off;
+      // Materialise (batch kernel): the advance transition extended by ad0(next) =
+      // (k0(next) g_{d-1} + next) / g_d, a_d of the next node's first row (a function of the
+      // residue alone: R_L - (A - k0) g_{d-1} = k0 g_{d-1} + rho), so a node entry needs no
+      // division.  One 16 B shared load per advance.
+      if (consumer == FS_CONSUMER_ROWS && c.gA <= 1024u) {
+        const uint32_t radv_off = ((uint32_t)p->ktab.size() + 3u) & ~3u;
+        p->ktab.resize(radv_off + 4u * c.gA, 0u);
+        for (uint32_t rho = 0; rho < c.gA; ++rho) {
+          const fs::Adv w = ar.step(rho, c);
+          uint32_t *ent = &p->ktab[radv_off + 4u * rho];
+          ent[0] = fs::adv_pack(w.next, w.inc);
+          ent[1] = w.k0;
+          ent[2] = w.k0 == fs::kNone ? 0u : (uint32_t)(((uint64_t)w.k0 * c.gA + w.next) / c.gB);
+        }
+        c.radv_off = radv_off;
+      }
       // Closed-tail group tables (count or histogram + tail=closed): per residue rho the entry
       // {rel | (q + carry) << kCAdvShift, s - k0(next)} (count, 8 B), followed for the
       // histogram by {ad0(next) - k0(next), 0} (16 B), where rel = byte offset of next's

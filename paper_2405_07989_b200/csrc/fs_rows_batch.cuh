@@ -1,0 +1,352 @@
+// fs_rows_batch.cuh -- materialise (the paper's "saving the factorizations",
+// P:55) with one row per lane per step, in lockstep across the warp.
+//
+// Row-unit slices hold exactly T rows (T a multiple of 64), so once every lane of a warp has a
+// full slice, every lane emits exactly one row per step: the step first moves an exhausted
+// lane to the next node that has rows (Alg. 3.1 at index L -- a 16 B shared-table advance --
+// or the rare ascend at an index < L, with the modulo skip applied at entry,
+// P:170-176), then takes the node's next row (a_{d-1} -= s, a_d += t).  Because the row index
+// inside a batch is a compile-time constant, a batch of NB rows (NB * row_bytes a multiple of
+// 16) is assembled in registers with fixed shifts, written to the lane's shared-memory slot
+// with 16 B stores (a lane stride of an odd number of 16 B units keeps each quarter-warp on
+// distinct banks), and after NBUF batches the warp copies all 32 slots out with 16 B stores:
+//   canonical (M1): lane l's slot goes to its slice's exact byte offset (a contiguous
+//                   segment of NBUF * NB rows per lane),
+//   any (M2):       the warp reserves 32 * NBUF * NB rows on the front cursor with one
+//                   atomicAdd and writes its whole staging area as ONE contiguous block.
+// The rank's ragged last slice (< T rows) is written by fs_rows_tail_kernel.
+#pragma once
+
+#include "fs_kernels.cuh"
+
+namespace fs {
+
+constexpr int cgcd(int a, int b) { return b == 0 ? a : cgcd(b, a % b); }
+
+#ifndef FS_RB_GMAX
+#define FS_RB_GMAX 320  // bytes per lane per flush group (upper bound)
+#endif
+
+template <int D, int B>
+struct RowsBatchGeom {
+  static constexpr int RB = D * (B / 8);              // row bytes
+  static constexpr int NB = 16 / cgcd(RB, 16);        // rows per 16 B-aligned batch (1, 2, 4 or 8)
+  static constexpr int BB = NB * RB;                  // batch bytes
+  static constexpr int BW = BB / 4;                   // batch words
+  static constexpr bool kOk = D >= 2 && BB <= 112;    // register budget of the batch
+  static constexpr int nbuf_(int p) { return (2 * p * NB <= 64 && 2 * p * BB <= FS_RB_GMAX) ? nbuf_(2 * p) : p; }
+  static constexpr int NBUF = nbuf_(1);               // batches per flush group (power of two)
+  static constexpr int GR = NB * NBUF;                // rows per lane per group (divides 64)
+  static constexpr int FG = NBUF * BB;                // bytes per lane per group
+  static constexpr int C = FG / 16;                   // 16 B chunks per lane per group
+  static constexpr int STRIDE = (C & 1) ? FG : FG + 16;  // odd number of 16 B units
+  static constexpr size_t kWarpStage = 32u * STRIDE;
+  static constexpr size_t smem_stage(int warps) { return (size_t)warps * (kWarpStage + 32u * 8u); }
+};
+
+__device__ __forceinline__ void sts128(uint32_t a, uint32_t x, uint32_t y, uint32_t z, uint32_t w) {
+  asm volatile("st.shared.v4.u32 [%0], {%1, %2, %3, %4};" ::"r"(a), "r"(x), "r"(y), "r"(z), "r"(w) : "memory");
+}
+__device__ __forceinline__ uint4 lds128_nv(uint32_t a) {
+  uint4 v;
+  asm volatile("ld.shared.v4.u32 {%0, %1, %2, %3}, [%4];" : "=r"(v.x), "=r"(v.y), "=r"(v.z), "=r"(v.w) : "r"(a));
+  return v;
+}
+
+// Node transition with the first row's a_d: table (shared memory) or arithmetic.
+struct RAdvSmem {
+  uint32_t base;  // shared-window address of the radv table
+  __device__ __forceinline__ void step(uint32_t rho, const Consts &, uint32_t &next, uint32_t &inc, uint32_t &k0,
+                                       uint32_t &ad0) const {
+    const uint4 w = lds128_nv(base + rho * 16u);
+    next = w.x & ((1u << kAdvBits) - 1u);
+    inc = w.x >> kAdvBits;
+    k0 = w.y;
+    ad0 = w.z;
+  }
+};
+struct RAdvArith {
+  __device__ __forceinline__ void step(uint32_t rho, const Consts &c, uint32_t &next, uint32_t &inc, uint32_t &k0,
+                                       uint32_t &ad0) const {
+    const Adv w = KTabArith{}.step(rho, c);
+    next = w.next;
+    inc = w.inc;
+    k0 = w.k0;
+    ad0 = divq(w.k0 * c.gA + w.next, c.dvB);  // garbage when k0 = none (the node has no rows)
+  }
+};
+
+// Register copy of the constants the row step and ascend() read.  They are staged through
+// shared memory and read back once: ptxas would otherwise re-load a kernel parameter (LDCU)
+// at every use inside the row loop (it sees through register moves and shuffles).
+template <int D>
+struct RegC {
+  static constexpr int LA = Lane<D>::LA;
+  uint32_t g[LA];
+  Div dv[LA];
+  uint32_t gA;
+  Div dvA, dvB;
+  static constexpr int kWords = 3 * LA + 5;
+  // w: kWords words of shared memory; every thread calls put() then (after a barrier) get()
+  __device__ __forceinline__ static void put(const Consts &c, uint32_t *w) {
+    if (threadIdx.x == 0) {
+      for (int j = 0; j < LA; ++j) {
+        w[3 * j] = c.g[j];
+        w[3 * j + 1] = c.dv[j].m;
+        w[3 * j + 2] = c.dv[j].sh;
+      }
+      w[3 * LA] = c.gA;
+      w[3 * LA + 1] = c.dvA.m;
+      w[3 * LA + 2] = c.dvA.sh;
+      w[3 * LA + 3] = c.dvB.m;
+      w[3 * LA + 4] = c.dvB.sh;
+    }
+  }
+  __device__ __forceinline__ void get(const uint32_t *w) {
+#pragma unroll
+    for (int j = 0; j < LA; ++j) {
+      g[j] = w[3 * j];
+      dv[j].m = w[3 * j + 1];
+      dv[j].sh = w[3 * j + 2];
+    }
+    gA = w[3 * LA];
+    dvA.m = w[3 * LA + 1];
+    dvA.sh = w[3 * LA + 2];
+    dvB.m = w[3 * LA + 3];
+    dvB.sh = w[3 * LA + 4];
+  }
+};
+
+// a_d of the current row by division (slice entry and after an ascend only)
+template <int D, class CC>
+__device__ __forceinline__ uint32_t rb_solve_ad(const Lane<D> &st, const CC &c) {
+  return divq((st.A - (uint32_t)st.cur) * c.gA + st.rho, c.dvB);
+}
+
+// Make the lane's current row valid: while its node is exhausted, move to the next node in
+// decreasing lex order (Alg. 3.1 at index L by table, or an ascend at an index < L) and
+// enter it with the modulo skip.  Inside a full row slice the stream cannot end here.
+// (R_L is not tracked: ascend() re-derives it from R_{L-1}.)
+template <int D, class KT, class RA, class CC>
+__device__ __forceinline__ void rb_slow(Lane<D> &st, uint32_t &ad, const Consts &c, const CC &rc, const KT &kt,
+                                        const RA &ra) {
+  constexpr int L = D - 2;
+  if constexpr (L >= 1) {
+    while (st.cur < 0) {
+      if (st.a[L - 1] > 0) {
+        uint32_t next, inc, k0, ad0;
+        ra.step(st.rho, c, next, inc, k0, ad0);
+        st.a[L - 1] -= 1u;
+        st.rho = next;
+        st.A += inc;
+        st.cur = (int32_t)st.A - (int32_t)k0;
+        ad = ad0;
+      } else {
+        if (!ascend<D>(st, rc)) {  // end of stream: impossible inside a full slice
+          st.cur = 0x3fffffff;
+          break;
+        }
+        st.cur = (int32_t)st.A - (int32_t)kt(st.rho, c);
+        ad = rb_solve_ad<D>(st, rc);
+      }
+    }
+  }
+}
+
+// The common case branch-free: a lane whose node is exhausted and whose a_L > 0 advances one
+// node under a predicate (every lane issues the one table load); the rare lanes that land on
+// a node without rows or need an ascend are finished by rb_slow() behind one warp vote.
+template <int D, class KT, class RA, class CC>
+__device__ __forceinline__ void rb_ensure_row(Lane<D> &st, uint32_t &ad, const Consts &c, const CC &rc, const KT &kt,
+                                              const RA &ra) {
+  constexpr int L = D - 2;
+  if constexpr (L >= 1) {
+    const bool fa = st.cur < 0 && st.a[L - 1] != 0u;
+    uint32_t next, inc, k0, ad0;
+    ra.step(st.rho, c, next, inc, k0, ad0);
+    if (fa) {
+      st.a[L - 1] -= 1u;
+      st.rho = next;
+      st.A += inc;
+      st.cur = (int32_t)st.A - (int32_t)k0;
+      ad = ad0;
+    }
+    if (__any_sync(kFull, st.cur < 0)) rb_slow<D>(st, ad, c, rc, kt, ra);
+  }
+}
+
+template <int D, int B, bool ANY, bool KTAB>
+__global__ void __launch_bounds__(kBlock, 1) fs_rows_batch_kernel(const KParams P) {
+  using G = RowsBatchGeom<D, B>;
+  constexpr int L = D - 2;
+  constexpr int kWarps = kBlock / 32;
+  extern __shared__ __align__(16) unsigned char smem[];
+  const Consts &c = P.c;
+  uint32_t *ktab_s = reinterpret_cast<uint32_t *>(smem);
+  const uint32_t kt_words = (c.ktab_len + 3u) & ~3u;
+  for (uint32_t i = threadIdx.x; i < c.ktab_len; i += blockDim.x) ktab_s[i] = c.ktab[i];
+  __shared__ uint32_t kc[RegC<D>::kWords + 2];
+  RegC<D>::put(c, kc);
+  if (threadIdx.x == 0) {
+    kc[RegC<D>::kWords] = c.s;
+    kc[RegC<D>::kWords + 1] = c.t;
+  }
+  __syncthreads();
+  RegC<D> rc;
+  rc.get(kc);
+  const uint32_t s = kc[RegC<D>::kWords], t = kc[RegC<D>::kWords + 1];
+  unsigned char *stage = reinterpret_cast<unsigned char *>(ktab_s + kt_words);
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const uint32_t wstage = (uint32_t)__cvta_generic_to_shared(stage + (size_t)warp * G::kWarpStage);
+  uint64_t *soff = reinterpret_cast<uint64_t *>(stage + (size_t)kWarps * G::kWarpStage) + warp * 32;
+  const uint32_t myslot = wstage + (uint32_t)lane * G::STRIDE;
+
+  using KT = typename std::conditional<KTAB, KTabSmem, KTabArith>::type;
+  KT kt;
+  const uint32_t ktab_base = (uint32_t)__cvta_generic_to_shared(ktab_s);
+  if constexpr (KTAB) {
+    kt.base = ktab_base;
+    kt.adv = ktab_base + 4u * c.adv_off;
+  }
+  using RA = typename std::conditional<KTAB, RAdvSmem, RAdvArith>::type;
+  RA ra;
+  if constexpr (KTAB) ra.base = ktab_base + 4u * c.radv_off;
+
+  Lane<D> st;
+#pragma unroll
+  for (int j = 0; j < Lane<D>::LA; ++j) {
+    st.a[j] = 0;
+    st.R[j] = 0;
+  }
+  st.A = st.rho = 0;
+  st.cur = 0;
+  st.k = st.kb = 0;
+  st.lsum = 0;
+  uint32_t ad = 0;
+  const uint32_t groups = (uint32_t)(P.T / (uint64_t)G::GR);
+
+
+  for (;;) {
+    // one claim of 32 consecutive full slices per warp
+    unsigned long long base = 0;
+    if (lane == 0) base = atomicAdd(P.queue, 32ull);
+    base = __shfl_sync(kFull, base, 0);
+    if (base >= P.num_slices) break;
+    const uint64_t idx = base + (uint64_t)lane;
+    const bool live = idx < P.num_slices;
+    const uint64_t rem = P.num_slices - base;
+    const uint32_t nlive = rem < 32u ? (uint32_t)rem : 32u;
+    if (live) {
+      const uint64_t u = P.unit0 + idx * P.T;
+      const uint64_t off = unrank<D, true>(st, c, kt, u);
+      st.cur -= (int32_t)((uint32_t)off * s);  // row units: skip to row `off` of the node
+      ad = rb_solve_ad<D>(st, c);
+      soff[lane] = (u - P.unit0) * (uint64_t)G::RB;
+    } else {
+      st.cur = 0x3fffffff;  // an idle lane: a node that never runs out (never flushed)
+      if constexpr (L >= 1) st.a[L - 1] = 0;
+    }
+    __syncwarp();
+    for (uint32_t grp = 0; grp < groups; ++grp) {
+#pragma unroll 1
+      for (int b = 0; b < G::NBUF; ++b) {
+        uint32_t wd[G::BW];
+#pragma unroll
+        for (int u = 0; u < G::NB; ++u) {
+          rb_ensure_row<D>(st, ad, c, rc, kt, ra);
+          uint32_t v[D];
+#pragma unroll
+          for (int j = 0; j < L; ++j) v[j] = st.a[j];
+          v[D - 2] = (uint32_t)st.cur;
+          v[D - 1] = ad;
+#pragma unroll
+          for (int j = 0; j < D; ++j) {
+            if (B == 32) {
+              wd[u * D + j] = v[j];
+            } else {
+              const int h = u * D + j;
+              if (h & 1)
+                wd[h >> 1] |= v[j] << 16;
+              else
+                wd[h >> 1] = v[j];
+            }
+          }
+          st.cur -= (int32_t)s;
+          ad += t;
+        }
+#pragma unroll
+        for (int i = 0; i < G::BW / 4; ++i)
+          sts128(myslot + (uint32_t)b * G::BB + 16u * i, wd[4 * i], wd[4 * i + 1], wd[4 * i + 2], wd[4 * i + 3]);
+      }
+      __syncwarp();
+      if (ANY) {
+        unsigned long long blk = 0;
+        if (lane == 0) blk = atomicAdd(P.front, (unsigned long long)nlive * G::GR);
+        blk = __shfl_sync(kFull, blk, 0);
+        uint4 *dst = reinterpret_cast<uint4 *>(P.rows_out + blk * (uint64_t)G::RB);
+#pragma unroll 4
+        for (int it = 0; it < G::C; ++it) {
+          const uint32_t q = (uint32_t)it * 32u + (uint32_t)lane;
+          const uint32_t l = q / (uint32_t)G::C, part = q - l * (uint32_t)G::C;
+          if (l < nlive) __stcs(dst + q, lds128_nv(wstage + l * G::STRIDE + part * 16u));
+        }
+      } else {
+        const uint64_t gbase = (uint64_t)grp * G::FG;
+#pragma unroll 4
+        for (int it = 0; it < G::C; ++it) {
+          const uint32_t q = (uint32_t)it * 32u + (uint32_t)lane;
+          const uint32_t l = q / (uint32_t)G::C, part = q - l * (uint32_t)G::C;
+          if (l < nlive) {
+            const uint4 v = lds128_nv(wstage + l * G::STRIDE + part * 16u);
+            __stcs(reinterpret_cast<uint4 *>(P.rows_out + soff[l] + gbase + part * 16u), v);
+          }
+        }
+      }
+      __syncwarp();
+    }
+  }
+}
+
+// The rank's ragged last slice: rows [unit0 + first, unit1) (fewer than T), split across the
+// threads of one CTA; each thread unranks its first row and stores its rows coordinate by
+// coordinate (M1: at their canonical offsets; M2: at the back of the rank's block, where the
+// back cursor grows down from rank_rows).
+template <int D, int B, bool ANY>
+__global__ void fs_rows_tail_kernel(const KParams P, uint64_t first) {
+  const Consts &c = P.c;
+  const uint64_t rows = P.unit1 - (P.unit0 + first);
+  const uint64_t per = (rows + blockDim.x - 1) / blockDim.x;
+  const uint64_t r0 = (uint64_t)threadIdx.x * per;
+  if (ANY && threadIdx.x == 0) atomicAdd(P.back, (unsigned long long)rows);
+  if (r0 >= rows) return;
+  const uint64_t r1 = r0 + per < rows ? r0 + per : rows;
+  Lane<D> st;
+  KTabArith kt;
+  RAdvArith ra;
+  const uint64_t u = P.unit0 + first + r0;
+  const uint64_t off = unrank<D, true>(st, c, kt, u);
+  st.cur -= (int32_t)((uint32_t)off * c.s);
+  uint32_t ad = rb_solve_ad<D>(st, c);
+  const uint64_t out_row = ANY ? (P.rank_rows - rows + r0) : (first + r0);
+  unsigned char *q = P.rows_out + out_row * (uint64_t)(D * (B / 8));
+  for (uint64_t r = r0; r < r1; ++r) {
+    rb_slow<D>(st, ad, c, c, kt, ra);  // per thread (threads diverge here)
+    uint32_t v[D];
+#pragma unroll
+    for (int j = 0; j < D - 2; ++j) v[j] = st.a[j];
+    v[D - 2] = (uint32_t)st.cur;
+    v[D - 1] = ad;
+#pragma unroll
+    for (int j = 0; j < D; ++j) {
+      if (B == 16)
+        reinterpret_cast<uint16_t *>(q)[j] = (uint16_t)v[j];
+      else
+        reinterpret_cast<uint32_t *>(q)[j] = v[j];
+    }
+    q += D * (B / 8);
+    st.cur -= (int32_t)c.s;
+    ad += c.t;
+  }
+}
+
+}  // namespace fs

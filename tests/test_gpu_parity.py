@@ -202,6 +202,42 @@ def test_rows_order_any(oracle_mod, inst):
         assert rows_bytes(api.sort_rows_desc(t)) == oracle.rows(n, g, B=B)
 
 
+@pytest.mark.parametrize("inst", ALL[:40], ids=ids)
+@pytest.mark.parametrize("impl", [L.FS_ROWS_BATCH, L.FS_ROWS_STAGED])
+def test_rows_impls(oracle_mod, inst, impl):
+    """Both materialise kernels, both layouts, several slice sizes (many claims, partial warp
+    claims, a ragged last slice for the tail kernel): byte-identical canonical rows."""
+    n, g = inst.n, inst.gens
+    for B in (16, 32):
+        if B == 16 and max(n // x for x in g) > 65535:
+            continue
+        want = oracle.rows(n, g, B=B)
+        for T in (64, 192, 0):
+            rows, off, t = api.fs_enumerate_ex(n, g, B=B, slice_units=T, rows_impl=impl)
+            assert rows_bytes(t) == want
+            rows, off, t = api.fs_enumerate_ex(n, g, B=B, slice_units=T, rows_impl=impl, order=L.FS_ORDER_ANY)
+            assert rows_bytes(api.sort_rows_desc(t)) == want
+
+
+@pytest.mark.parametrize("impl", [L.FS_ROWS_BATCH, L.FS_ROWS_STAGED])
+def test_rows_impls_c2(oracle_mod, impl):
+    """C2 (681,152 rows): every supported batch shape's neighbour d = 5 at B = 16/32, both
+    layouts, several world sizes (rank blocks with ragged ends)."""
+    n, g = W.C2.n, W.C2.gens
+    for B in (16, 32):
+        want = oracle.rows(n, g, B=B)
+        for world in (1, 3):
+            blob, blob_any = b"", []
+            for r in range(world):
+                rows, off, t = api.fs_enumerate_ex(n, g, B=B, rank=r, world=world, rows_impl=impl)
+                blob += rows_bytes(t)
+                rows, off, t = api.fs_enumerate_ex(n, g, B=B, rank=r, world=world, rows_impl=impl,
+                                                   order=L.FS_ORDER_ANY)
+                blob_any.append(rows_bytes(api.sort_rows_desc(t)))
+            assert blob == want
+            assert b"".join(blob_any) == want
+
+
 def test_rows_order_any_c2(oracle_mod):
     n, g = W.C2.n, W.C2.gens
     rows, off, t = api.fs_enumerate_ex(n, g, B=16, order=L.FS_ORDER_ANY)
