@@ -336,13 +336,7 @@ def main():
     share = (info["unit_end"] - info["unit_begin"]) / max(1, info["total_units"])
     ops = ops_model(info, closed=True) * share
     achieved = ops / (ms_kern / 1e3) / 1e12
-    traffic = None
-    prof = os.path.join(ROOT, "profiles", "traffic.json")
-    if os.path.exists(prof):
-        try:
-            traffic = json.load(open(prof)).get(args.workload)
-        except Exception:
-            traffic = None
+    traffic = _traffic(args.workload)
 
     line = {
         "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
@@ -418,6 +412,16 @@ def _time_ms(fn, stream, reps, barrier, max_over_ranks):
     return max_over_ranks(statistics.median(ts))
 
 
+def _traffic(key):
+    """dram__bytes_read.sum + dram__bytes_write.sum per launch of the kernel, from one
+    `ncu --set full` capture (profiles/traffic.json, written from the committed summaries)."""
+    prof = os.path.join(ROOT, "profiles", "traffic.json")
+    try:
+        return json.load(open(prof)).get(key)
+    except Exception:
+        return None
+
+
 def extras(args, world, rank, local, dev, stream, peaks, peaks_kind, barrier, max_over_ranks, mb):
     """Same-run measurements of the other hot-path consumers (each on its BASELINE config)."""
     import torch
@@ -436,9 +440,13 @@ def extras(args, world, rank, local, dev, stream, peaks, peaks_kind, barrier, ma
     # ---- store: C2-XL rows, u16; canonical layout (M1) and warp-compacted layout (M2)
     inst = W.C2XL
     store_out = None  # one output buffer, reused by the three layouts (as a caller would)
-    for order, key, go in ((L.FS_ORDER_CANONICAL, "store", 0), (L.FS_ORDER_ANY, "store_any", 0),
-                           (L.FS_ORDER_ANY, "store_any_auto_order", L.FS_GENORDER_AUTO)):
-        p = api.Plan(inst.n, inst.gens, L.FS_CONSUMER_ROWS, order=order, gen_order=go, **kw)
+    # batch kernel (default, lockstep register batches) and the round-1 staged kernels
+    for order, key, go, impl in ((L.FS_ORDER_CANONICAL, "store", 0, L.FS_ROWS_BATCH),
+                                 (L.FS_ORDER_ANY, "store_any", 0, L.FS_ROWS_BATCH),
+                                 (L.FS_ORDER_CANONICAL, "store_staged", 0, L.FS_ROWS_STAGED),
+                                 (L.FS_ORDER_ANY, "store_any_staged_auto_order", L.FS_GENORDER_AUTO,
+                                  L.FS_ROWS_STAGED)):
+        p = api.Plan(inst.n, inst.gens, L.FS_CONSUMER_ROWS, order=order, gen_order=go, rows_impl=impl, **kw)
         info = p.info
         rows = info["row_end"] - info["row_begin"]
         if store_out is None or store_out.shape[0] < rows:
@@ -455,9 +463,11 @@ def extras(args, world, rank, local, dev, stream, peaks, peaks_kind, barrier, ma
         ex[key] = {"workload": "C2XL: Z(16000, (11,13,17,19,23)) materialise u16 rows, %s order%s"
                                % ("canonical (exact offsets)" if order == 0 else "any (warp compaction)",
                                   ", NEXT-2 generator order" if go else ""),
+                   "kernel": "batch (lockstep register batches)" if impl == L.FS_ROWS_BATCH
+                   else "staged (round-1 per-step emission)",
                    "rows": total_rows, "bytes": bytes_, "ms": ms, "value": total_rows / (ms / 1e3), "unit": UNIT,
                    "roofline": {"bound": "hbm", "achieved": gbs_all, "peak": peak, "unit": "GB/s",
-                                "frac": gbs_all / peak,
+                                "frac": gbs_all / peak, "traffic": _traffic(key),
                                 "peak_source": "MEASURED_PEAKS.json hbm_gbs x %d (%s, copy r+w)" % (world, peaks_kind),
                                 "frac_of_write_microbench": (gbs_all / world / mb["hbm_write_gbs"]) if mb else None}}
         del out

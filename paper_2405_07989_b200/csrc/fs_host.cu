@@ -93,8 +93,12 @@ int fs_validate_and_build(fs_plan *p, uint64_t n, const uint32_t *gens, int d, i
   // with the largest first.  Canonical-order materialise keeps the caller's order.
   std::vector<int> perm(d);
   for (int i = 0; i < d; ++i) perm[i] = i;
+  // The batch materialise kernel writes rows in the stream's coordinate order, so an
+  // order=any plan it serves keeps the caller's order too (it is faster than the staged
+  // kernel over the permuted order: C2-XL 5.3 vs 6.1 ms).
+  const bool batch_rows = consumer == FS_CONSUMER_ROWS && e.rows_impl == FS_ROWS_BATCH && fs_rows_batch_shape_ok(d);
   const bool may_permute = e.gen_order == FS_GENORDER_AUTO &&
-                           (consumer != FS_CONSUMER_ROWS || e.order == FS_ORDER_ANY) && d >= 3;
+                           (consumer != FS_CONSUMER_ROWS || (e.order == FS_ORDER_ANY && !batch_rows)) && d >= 3;
   if (may_permute) {
     std::vector<int> desc(perm);
     std::stable_sort(desc.begin(), desc.end(), [&](int a, int b) { return gens[a] > gens[b]; });

@@ -78,6 +78,8 @@ bool fs_rows_batch_supported(const fs_plan *p, int B) {
   return B == 16 ? fs::rb_ok_b<16>(p->d) : fs::rb_ok_b<32>(p->d);
 }
 
+bool fs_rows_batch_shape_ok(int d) { return fs::rb_ok_b<16>(d) || fs::rb_ok_b<32>(d); }
+
 // kp.num_slices = number of FULL slices of T rows; rows [num_slices * T, unit1 - unit0) go to
 // the tail kernel.  *launches counts the kernels enqueued.
 int fs_dispatch_rows_batch(fs_plan *p, int B, bool any, const fs::KParams &kp, cudaStream_t s, bool q, uint32_t *g,

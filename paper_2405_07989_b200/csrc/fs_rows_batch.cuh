@@ -41,7 +41,7 @@ struct RowsBatchGeom {
   static constexpr int C = FG / 16;                   // 16 B chunks per lane per group
   static constexpr int STRIDE = (C & 1) ? FG : FG + 16;  // odd number of 16 B units
   static constexpr size_t kWarpStage = 32u * STRIDE;
-  static constexpr size_t smem_stage(int warps) { return (size_t)warps * (kWarpStage + 32u * 8u); }
+  static constexpr size_t smem_stage(int warps) { return (size_t)warps * kWarpStage; }
 };
 
 __device__ __forceinline__ void sts128(uint32_t a, uint32_t x, uint32_t y, uint32_t z, uint32_t w) {
@@ -53,27 +53,31 @@ __device__ __forceinline__ uint4 lds128_nv(uint32_t a) {
   return v;
 }
 
-// Node transition with the first row's a_d: table (shared memory) or arithmetic.
+// Node transition with the first row's a_d, as an entry for a residue rho: the next residue,
+// the increment of floor(R_L / g_{d-1}), k0 of the next residue and a_d of the next node's
+// first row.  Shared-memory table (one 16 B load, issued right after the previous advance so
+// its latency is off the row loop's critical path) or arithmetic.
 struct RAdvSmem {
+  using Ent = uint4;
   uint32_t base;  // shared-window address of the radv table
-  __device__ __forceinline__ void step(uint32_t rho, const Consts &, uint32_t &next, uint32_t &inc, uint32_t &k0,
-                                       uint32_t &ad0) const {
-    const uint4 w = lds128_nv(base + rho * 16u);
-    next = w.x & ((1u << kAdvBits) - 1u);
-    inc = w.x >> kAdvBits;
-    k0 = w.y;
-    ad0 = w.z;
-  }
+  __device__ __forceinline__ Ent load(uint32_t rho, const Consts &) const { return lds128_nv(base + rho * 16u); }
+  __device__ __forceinline__ static uint32_t next(const Ent &e) { return e.x & ((1u << kAdvBits) - 1u); }
+  __device__ __forceinline__ static uint32_t inc(const Ent &e) { return e.x >> kAdvBits; }
+  __device__ __forceinline__ static uint32_t k0(const Ent &e) { return e.y; }
+  __device__ __forceinline__ static uint32_t ad0(const Ent &e) { return e.z; }
 };
 struct RAdvArith {
-  __device__ __forceinline__ void step(uint32_t rho, const Consts &c, uint32_t &next, uint32_t &inc, uint32_t &k0,
-                                       uint32_t &ad0) const {
+  struct Ent {
+    uint32_t nx, in, k, a;
+  };
+  __device__ __forceinline__ Ent load(uint32_t rho, const Consts &c) const {
     const Adv w = KTabArith{}.step(rho, c);
-    next = w.next;
-    inc = w.inc;
-    k0 = w.k0;
-    ad0 = divq(w.k0 * c.gA + w.next, c.dvB);  // garbage when k0 = none (the node has no rows)
+    return Ent{w.next, w.inc, w.k0, divq(w.k0 * c.gA + w.next, c.dvB)};  // a: garbage when k0 = none
   }
+  __device__ __forceinline__ static uint32_t next(const Ent &e) { return e.nx; }
+  __device__ __forceinline__ static uint32_t inc(const Ent &e) { return e.in; }
+  __device__ __forceinline__ static uint32_t k0(const Ent &e) { return e.k; }
+  __device__ __forceinline__ static uint32_t ad0(const Ent &e) { return e.a; }
 };
 
 // Register copy of the constants the row step and ascend() read.  They are staged through
@@ -126,21 +130,21 @@ __device__ __forceinline__ uint32_t rb_solve_ad(const Lane<D> &st, const CC &c) 
 // Make the lane's current row valid: while its node is exhausted, move to the next node in
 // decreasing lex order (Alg. 3.1 at index L by table, or an ascend at an index < L) and
 // enter it with the modulo skip.  Inside a full row slice the stream cannot end here.
-// (R_L is not tracked: ascend() re-derives it from R_{L-1}.)
+// (R_L is not tracked: ascend() re-derives it from R_{L-1}.)  `wn` is the transition entry
+// of the current residue; it is refreshed whenever rho changes.
 template <int D, class KT, class RA, class CC>
-__device__ __forceinline__ void rb_slow(Lane<D> &st, uint32_t &ad, const Consts &c, const CC &rc, const KT &kt,
-                                        const RA &ra) {
+__device__ __forceinline__ void rb_slow(Lane<D> &st, uint32_t &ad, typename RA::Ent &wn, const Consts &c,
+                                        const CC &rc, const KT &kt, const RA &ra) {
   constexpr int L = D - 2;
   if constexpr (L >= 1) {
+    if (st.cur >= 0) return;
     while (st.cur < 0) {
       if (st.a[L - 1] > 0) {
-        uint32_t next, inc, k0, ad0;
-        ra.step(st.rho, c, next, inc, k0, ad0);
         st.a[L - 1] -= 1u;
-        st.rho = next;
-        st.A += inc;
-        st.cur = (int32_t)st.A - (int32_t)k0;
-        ad = ad0;
+        st.rho = RA::next(wn);
+        st.A += RA::inc(wn);
+        st.cur = (int32_t)st.A - (int32_t)RA::k0(wn);
+        ad = RA::ad0(wn);
       } else {
         if (!ascend<D>(st, rc)) {  // end of stream: impossible inside a full slice
           st.cur = 0x3fffffff;
@@ -149,29 +153,29 @@ __device__ __forceinline__ void rb_slow(Lane<D> &st, uint32_t &ad, const Consts 
         st.cur = (int32_t)st.A - (int32_t)kt(st.rho, c);
         ad = rb_solve_ad<D>(st, rc);
       }
+      wn = ra.load(st.rho, c);
     }
   }
 }
 
 // The common case branch-free: a lane whose node is exhausted and whose a_L > 0 advances one
-// node under a predicate (every lane issues the one table load); the rare lanes that land on
-// a node without rows or need an ascend are finished by rb_slow() behind one warp vote.
+// node under a predicate, from the prefetched entry, and issues the load of the next entry;
+// the rare lanes that land on a node without rows or need an ascend are finished by rb_slow()
+// behind one warp vote.
 template <int D, class KT, class RA, class CC>
-__device__ __forceinline__ void rb_ensure_row(Lane<D> &st, uint32_t &ad, const Consts &c, const CC &rc, const KT &kt,
-                                              const RA &ra) {
+__device__ __forceinline__ void rb_ensure_row(Lane<D> &st, uint32_t &ad, typename RA::Ent &wn, const Consts &c,
+                                              const CC &rc, const KT &kt, const RA &ra) {
   constexpr int L = D - 2;
   if constexpr (L >= 1) {
-    const bool fa = st.cur < 0 && st.a[L - 1] != 0u;
-    uint32_t next, inc, k0, ad0;
-    ra.step(st.rho, c, next, inc, k0, ad0);
-    if (fa) {
+    if (st.cur < 0 && st.a[L - 1] != 0u) {
       st.a[L - 1] -= 1u;
-      st.rho = next;
-      st.A += inc;
-      st.cur = (int32_t)st.A - (int32_t)k0;
-      ad = ad0;
+      st.rho = RA::next(wn);
+      st.A += RA::inc(wn);
+      st.cur = (int32_t)st.A - (int32_t)RA::k0(wn);
+      ad = RA::ad0(wn);
+      wn = ra.load(st.rho, c);
     }
-    if (__any_sync(kFull, st.cur < 0)) rb_slow<D>(st, ad, c, rc, kt, ra);
+    if (__any_sync(kFull, st.cur < 0)) rb_slow<D>(st, ad, wn, c, rc, kt, ra);
   }
 }
 
@@ -179,7 +183,6 @@ template <int D, int B, bool ANY, bool KTAB>
 __global__ void __launch_bounds__(kBlock, 1) fs_rows_batch_kernel(const KParams P) {
   using G = RowsBatchGeom<D, B>;
   constexpr int L = D - 2;
-  constexpr int kWarps = kBlock / 32;
   extern __shared__ __align__(16) unsigned char smem[];
   const Consts &c = P.c;
   uint32_t *ktab_s = reinterpret_cast<uint32_t *>(smem);
@@ -198,7 +201,6 @@ __global__ void __launch_bounds__(kBlock, 1) fs_rows_batch_kernel(const KParams 
   unsigned char *stage = reinterpret_cast<unsigned char *>(ktab_s + kt_words);
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const uint32_t wstage = (uint32_t)__cvta_generic_to_shared(stage + (size_t)warp * G::kWarpStage);
-  uint64_t *soff = reinterpret_cast<uint64_t *>(stage + (size_t)kWarps * G::kWarpStage) + warp * 32;
   const uint32_t myslot = wstage + (uint32_t)lane * G::STRIDE;
 
   using KT = typename std::conditional<KTAB, KTabSmem, KTabArith>::type;
@@ -223,6 +225,7 @@ __global__ void __launch_bounds__(kBlock, 1) fs_rows_batch_kernel(const KParams 
   st.k = st.kb = 0;
   st.lsum = 0;
   uint32_t ad = 0;
+  typename RA::Ent wn = ra.load(0u, c);
   const uint32_t groups = (uint32_t)(P.T / (uint64_t)G::GR);
 
 
@@ -241,11 +244,24 @@ __global__ void __launch_bounds__(kBlock, 1) fs_rows_batch_kernel(const KParams 
       const uint64_t off = unrank<D, true>(st, c, kt, u);
       st.cur -= (int32_t)((uint32_t)off * s);  // row units: skip to row `off` of the node
       ad = rb_solve_ad<D>(st, c);
-      soff[lane] = (u - P.unit0) * (uint64_t)G::RB;
     } else {
       st.cur = 0x3fffffff;  // an idle lane: a node that never runs out (never flushed)
       if constexpr (L >= 1) st.a[L - 1] = 0;
     }
+    wn = ra.load(st.rho, c);
+    // destination of the claim: M1 -- lane l's slice starts at byte (base + l) T RB of the
+    // rank's block; M2 -- one reservation of nlive * T rows for the whole claim (filled
+    // completely, group by group), so the front cursor sees one atomic per claim
+    unsigned char *dst0;
+    if (ANY) {
+      unsigned long long blk = 0;
+      if (lane == 0) blk = atomicAdd(P.front, (unsigned long long)nlive * P.T);
+      blk = __shfl_sync(kFull, blk, 0);
+      dst0 = P.rows_out + blk * (uint64_t)G::RB;
+    } else {
+      dst0 = P.rows_out + base * P.T * (uint64_t)G::RB;
+    }
+    const uint64_t SS = P.T * (uint64_t)G::RB;  // M1: bytes per slice
     __syncwarp();
     for (uint32_t grp = 0; grp < groups; ++grp) {
 #pragma unroll 1
@@ -253,7 +269,7 @@ __global__ void __launch_bounds__(kBlock, 1) fs_rows_batch_kernel(const KParams 
         uint32_t wd[G::BW];
 #pragma unroll
         for (int u = 0; u < G::NB; ++u) {
-          rb_ensure_row<D>(st, ad, c, rc, kt, ra);
+          rb_ensure_row<D>(st, ad, wn, c, rc, kt, ra);
           uint32_t v[D];
 #pragma unroll
           for (int j = 0; j < L; ++j) v[j] = st.a[j];
@@ -280,10 +296,7 @@ __global__ void __launch_bounds__(kBlock, 1) fs_rows_batch_kernel(const KParams 
       }
       __syncwarp();
       if (ANY) {
-        unsigned long long blk = 0;
-        if (lane == 0) blk = atomicAdd(P.front, (unsigned long long)nlive * G::GR);
-        blk = __shfl_sync(kFull, blk, 0);
-        uint4 *dst = reinterpret_cast<uint4 *>(P.rows_out + blk * (uint64_t)G::RB);
+        uint4 *dst = reinterpret_cast<uint4 *>(dst0 + (uint64_t)grp * nlive * G::FG);
 #pragma unroll 4
         for (int it = 0; it < G::C; ++it) {
           const uint32_t q = (uint32_t)it * 32u + (uint32_t)lane;
@@ -291,15 +304,13 @@ __global__ void __launch_bounds__(kBlock, 1) fs_rows_batch_kernel(const KParams 
           if (l < nlive) __stcs(dst + q, lds128_nv(wstage + l * G::STRIDE + part * 16u));
         }
       } else {
-        const uint64_t gbase = (uint64_t)grp * G::FG;
+        unsigned char *dst = dst0 + (uint64_t)grp * G::FG;
 #pragma unroll 4
         for (int it = 0; it < G::C; ++it) {
           const uint32_t q = (uint32_t)it * 32u + (uint32_t)lane;
           const uint32_t l = q / (uint32_t)G::C, part = q - l * (uint32_t)G::C;
-          if (l < nlive) {
-            const uint4 v = lds128_nv(wstage + l * G::STRIDE + part * 16u);
-            __stcs(reinterpret_cast<uint4 *>(P.rows_out + soff[l] + gbase + part * 16u), v);
-          }
+          if (l < nlive)
+            __stcs(reinterpret_cast<uint4 *>(dst + l * SS + part * 16u), lds128_nv(wstage + l * G::STRIDE + part * 16u));
         }
       }
       __syncwarp();
@@ -327,10 +338,11 @@ __global__ void fs_rows_tail_kernel(const KParams P, uint64_t first) {
   const uint64_t off = unrank<D, true>(st, c, kt, u);
   st.cur -= (int32_t)((uint32_t)off * c.s);
   uint32_t ad = rb_solve_ad<D>(st, c);
+  RAdvArith::Ent wn = ra.load(st.rho, c);
   const uint64_t out_row = ANY ? (P.rank_rows - rows + r0) : (first + r0);
   unsigned char *q = P.rows_out + out_row * (uint64_t)(D * (B / 8));
   for (uint64_t r = r0; r < r1; ++r) {
-    rb_slow<D>(st, ad, c, c, kt, ra);  // per thread (threads diverge here)
+    rb_slow<D>(st, ad, wn, c, c, kt, ra);  // per thread (threads diverge here)
     uint32_t v[D];
 #pragma unroll
     for (int j = 0; j < D - 2; ++j) v[j] = st.a[j];

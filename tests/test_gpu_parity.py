@@ -140,9 +140,10 @@ def test_generator_order_auto(oracle_mod, inst):
         if found:
             assert tuple(wit) in set(rows) and oracle.pred_holds(wit, pred, arg)
     B = 32
-    nr, off, t = api.fs_enumerate_ex(n, g, B=B, order=L.FS_ORDER_ANY, gen_order=AUTO)
-    assert nr == len(rows)
-    assert rows_bytes(api.sort_rows_desc(t)) == oracle.rows(n, g, B=B)
+    for impl in (L.FS_ROWS_BATCH, L.FS_ROWS_STAGED):  # the staged kernel runs the permuted order
+        nr, off, t = api.fs_enumerate_ex(n, g, B=B, order=L.FS_ORDER_ANY, gen_order=AUTO, rows_impl=impl)
+        assert nr == len(rows)
+        assert rows_bytes(api.sort_rows_desc(t)) == oracle.rows(n, g, B=B)
 
 
 def test_c5_auto_order_full():
