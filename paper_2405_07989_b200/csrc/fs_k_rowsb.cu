@@ -12,24 +12,24 @@ static int rb_launch(fs_plan *p, const KParams &kp, cudaStream_t stream, bool qu
     return FS_EINVAL;
   } else {
     auto kern = fs_rows_batch_kernel<D, B, ANY, KTAB>;
-    const size_t smem = (size_t)((kp.c.ktab_len + 3u) & ~3u) * 4 + G::smem_stage(kBlock / 32);
+    const size_t smem = (size_t)((kp.c.ktab_len + 3u) & ~3u) * 4 + G::smem_stage(kRbBlock / 32);
     if (cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem) != cudaSuccess)
       return FS_ECUDA;
     int per_sm = 0;
-    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, kBlock, smem) != cudaSuccess) return FS_ECUDA;
+    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, kRbBlock, smem) != cudaSuccess) return FS_ECUDA;
     if (per_sm < 1) return FS_ECUDA;
     if (p->ex.ctas_per_sm > 0 && p->ex.ctas_per_sm < per_sm) per_sm = p->ex.ctas_per_sm;
     int sms = 0;
     if (cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, p->device) != cudaSuccess) return FS_ECUDA;
     uint64_t grid = (uint64_t)sms * (uint64_t)per_sm;
-    const uint64_t need = (kp.num_slices + kBlock - 1) / kBlock;  // one slice per lane at least
+    const uint64_t need = (kp.num_slices + kRbBlock - 1) / kRbBlock;  // one slice per lane at least
     if (grid > need) grid = need ? need : 1;
     if (grid_out) *grid_out = (uint32_t)grid;
     if (query_only) return FS_OK;
     const uint64_t full_rows = kp.num_slices * kp.T;
     const uint64_t span = kp.unit1 - kp.unit0;
     if (kp.num_slices) {
-      kern<<<(unsigned)grid, kBlock, smem, stream>>>(kp);
+      kern<<<(unsigned)grid, kRbBlock, smem, stream>>>(kp);
       if (cudaGetLastError() != cudaSuccess) return FS_ECUDA;
       ++*launches;
     }

@@ -23,6 +23,11 @@ namespace fs {
 
 constexpr int cgcd(int a, int b) { return b == 0 ? a : cgcd(b, a % b); }
 
+#ifndef FS_RB_BLOCK
+#define FS_RB_BLOCK 128  // threads per CTA of the batch kernel (measured: 128 > 192 > 256)
+#endif
+constexpr int kRbBlock = FS_RB_BLOCK;
+
 #ifndef FS_RB_GMAX
 #define FS_RB_GMAX 320  // bytes per lane per flush group (upper bound)
 #endif
@@ -180,7 +185,7 @@ __device__ __forceinline__ void rb_ensure_row(Lane<D> &st, uint32_t &ad, typenam
 }
 
 template <int D, int B, bool ANY, bool KTAB>
-__global__ void __launch_bounds__(kBlock, 1) fs_rows_batch_kernel(const KParams P) {
+__global__ void __launch_bounds__(kRbBlock, 1) fs_rows_batch_kernel(const KParams P) {
   using G = RowsBatchGeom<D, B>;
   constexpr int L = D - 2;
   extern __shared__ __align__(16) unsigned char smem[];
