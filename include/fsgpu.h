@@ -178,6 +178,20 @@ int fs_any_ex(uint64_t n, const uint32_t *gens, int d, const fs_exec_t *ex, int 
 int64_t fs_enumerate_ex(uint64_t n, const uint32_t *gens, int d, int B, void *out_dev,
                         uint64_t cap, const fs_exec_t *ex, uint64_t *global_row_offset_out);
 
+/* Filtered materialise (the paper's consumers combine saving with a
+ * predicate): the rows of this rank's share of Z(n, gens) that satisfy
+ * pred(pred_arg) -- the fs_any predicates, COORD_GE's index in the caller's coordinates --
+ * packed like fs_enumerate's rows (B = 16 | 32) but in ARBITRARY order (warp-aggregated
+ * compaction, the order = any layout; sorting them gives the canonical order).  Two passes
+ * over the rank's slices: the first counts the matching rows, the second writes them (only
+ * if they fit).  Returns the number of matching rows m >= 0 and writes all m rows when
+ * m <= cap, none otherwise; or an FS_E* code (FS_EINVAL: bad B / predicate / alignment;
+ * FS_ERANGE as fs_enumerate).  out_dev: caller-owned device memory, 16-byte aligned, cap rows;
+ * may be NULL when cap = 0 (count only). */
+int64_t fs_enumerate_filtered_ex(uint64_t n, const uint32_t *gens, int d, int B, int pred,
+                                 uint64_t pred_arg, void *out_dev, uint64_t cap,
+                                 const fs_exec_t *ex);
+
 /* ---------------------------------------------------------------------------------
  * Plans: host work (validation, constants, exact DP tables, partition) done once;
  * kernels enqueued asynchronously on ex->cuda_stream with results left in DEVICE memory,

@@ -76,6 +76,8 @@ EXPORTS = {
     "fs_any_ex": (ctypes.c_int, [u64, u32p, ctypes.c_int, ctypes.POINTER(ExecT), ctypes.c_int, u64,
                                  ctypes.POINTER(ctypes.c_int), u32p]),
     "fs_enumerate_ex": (i64, [u64, u32p, ctypes.c_int, ctypes.c_int, vp, u64, ctypes.POINTER(ExecT), u64p]),
+    "fs_enumerate_filtered_ex": (i64, [u64, u32p, ctypes.c_int, ctypes.c_int, ctypes.c_int, u64, vp, u64,
+                                       ctypes.POINTER(ExecT)]),
     "fs_plan_create": (ctypes.c_int, [u64, u32p, ctypes.c_int, ctypes.c_int, ctypes.POINTER(ExecT),
                                       ctypes.POINTER(vp)]),
     "fs_plan_info": (ctypes.c_int, [vp, ctypes.POINTER(PlanInfoT)]),

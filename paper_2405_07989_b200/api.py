@@ -150,6 +150,26 @@ def fs_enumerate_ex(n, gens, B=16, cap=None, out=None, *, device=None, stream=No
     return int(rows), int(off.value), out[: min(int(cap), int(rows))]
 
 
+def fs_enumerate_filtered(n, gens, pred, pred_arg, B=16, cap=None, out=None, *, device=None, stream=None, rank=0,
+                          world=1, slice_units=0, ctas_per_sm=0, gen_order=L.FS_GENORDER_GIVEN):
+    """Rows of (this rank's share of) Z(n, gens) satisfying pred(pred_arg), in arbitrary order
+    (SURVEY 8(f) NEXT-4).  Returns (matches, rows_tensor); rows_tensor holds all matches when
+    they fit in cap (default: counted first, then allocated exactly), else it is empty."""
+    torch = _torch()
+    g, d = L.gens_array(gens)
+    ex = _exec(device, _stream_handle(stream), rank, world, slice_units, ctas_per_sm, L.FS_ORDER_ANY, 0, gen_order)
+    fn = L.lib().fs_enumerate_filtered_ex
+    if cap is None:
+        cap = L.check(fn(int(n), g, d, int(B), int(pred), int(pred_arg), None, 0, ctypes.byref(ex)),
+                      "fs_enumerate_filtered_ex")
+    dt = torch.uint16 if B == 16 else torch.int32
+    if out is None:
+        out = torch.empty((max(1, int(cap)), d), dtype=dt, device="cuda" if device is None else "cuda:%d" % device)
+    m = L.check(fn(int(n), g, d, int(B), int(pred), int(pred_arg), ctypes.c_void_p(out.data_ptr()), int(cap),
+                   ctypes.byref(ex)), "fs_enumerate_filtered_ex")
+    return int(m), out[: int(m) if m <= cap else 0]
+
+
 # ------------------------------------------------------------------ plans
 class Plan:
     """Host work (validation, constants, exact DP tables, partition) done once; kernels

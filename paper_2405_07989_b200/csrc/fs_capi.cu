@@ -372,6 +372,91 @@ int64_t fs_enumerate_ex(uint64_t n, const uint32_t *gens, int d, int B, void *ou
   return (int64_t)(h.p->row_end - h.p->row_begin);
 }
 
+int64_t fs_enumerate_filtered_ex(uint64_t n, const uint32_t *gens, int d, int B, int pred, uint64_t pred_arg,
+                                 void *out_dev, uint64_t cap, const fs_exec_t *ex) {
+  if (B != 16 && B != 32) return FS_EINVAL;
+  if (pred < FS_PRED_LEN_LE || pred > FS_PRED_COORD_GE) return FS_EINVAL;
+  if (cap && (!out_dev || ((uintptr_t)out_dev & 15u) != 0)) return FS_EINVAL;
+  fs_exec_t e;
+  if (ex)
+    e = *ex;
+  else {
+    memset(&e, 0, sizeof(e));
+    e.device = -1;
+    e.world = 1;
+  }
+  e.order = FS_ORDER_ANY;         // compaction: the matching rows' positions are not known a priori
+  e.rows_impl = FS_ROWS_STAGED;   // per-step ballot compaction (emission is filtered per row)
+  PlanHolder h;
+  int rc = fs_plan_create(n, gens, d, FS_CONSUMER_ROWS, &e, &h.p);
+  if (rc != FS_OK) return rc;
+  fs_plan *p = h.p;
+  if (B == 16) {
+    for (int i = 0; i < p->d; ++i)
+      if (p->n / p->g[i] > 65535) return FS_ERANGE;
+  }
+  const uint64_t span = p->unit_end - p->unit_begin;
+  if (span == 0) return 0;
+  if (p->d == 1) {  // Z = {(n/g)} iff g | n: decided on the host
+    const uint64_t x = p->n / p->g[0];
+    bool ok;
+    switch (pred) {
+      case FS_PRED_LEN_LE: ok = x <= pred_arg; break;
+      case FS_PRED_LEN_GE: ok = x >= pred_arg; break;
+      case FS_PRED_LEN_EQ: ok = x == pred_arg; break;
+      default: ok = (pred_arg >> 32) == 0 && x >= (pred_arg & 0xffffffffull);
+    }
+    if (!ok) return 0;
+    if (cap >= 1) {
+      DeviceGuard g(p->device);
+      if (B == 16) {
+        const uint16_t v = (uint16_t)x;
+        if (cudaMemcpy(out_dev, &v, 2, cudaMemcpyHostToDevice) != cudaSuccess) return FS_ECUDA;
+      } else {
+        const uint32_t v = (uint32_t)x;
+        if (cudaMemcpy(out_dev, &v, 4, cudaMemcpyHostToDevice) != cudaSuccess) return FS_ECUDA;
+      }
+    }
+    return 1;
+  }
+  unsigned long long cur[2] = {0, 0};
+  uint64_t matches = 0;
+  for (int pass = 0; pass < 2; ++pass) {
+    rc = prepare(p, true);
+    if (rc != FS_OK) return rc;
+    DeviceGuard g(p->device);
+    fs::KParams kp = base_params(p);
+    kp.rows_out = reinterpret_cast<unsigned char *>(out_dev);
+    kp.row_bytes = (uint32_t)(p->d * (B / 8));
+    kp.filt_pred = pred;
+    kp.filt_arg = pred_arg;
+    if (pred == FS_PRED_COORD_GE) {  // caller's coordinate index -> the stream's index
+      const uint64_t i = pred_arg >> 32;
+      if (i < (uint64_t)p->d) kp.filt_arg = ((uint64_t)p->iperm[i] << 32) | (pred_arg & 0xffffffffull);
+    }
+    kp.count_only = pass == 0 ? 1 : 0;
+    char *base = reinterpret_cast<char *>(p->scratch_dev);
+    if (cudaMemsetAsync(base + kOffFront, 0, kOffBack + 8 - kOffFront, p->stream) != cudaSuccess) return FS_ECUDA;
+    kp.front = reinterpret_cast<unsigned long long *>(base + kOffFront);
+    kp.back = reinterpret_cast<unsigned long long *>(base + kOffBack);
+    kp.rank_rows = matches;
+    rc = fs_launch(p, fs::kConsRowsAny, B, kp, p->stream);
+    if (rc != FS_OK) return rc;
+    rc = sync_plan(p);
+    if (rc != FS_OK) return rc;
+    if (cudaMemcpy(&cur[0], base + kOffFront, 8, cudaMemcpyDeviceToHost) != cudaSuccess ||
+        cudaMemcpy(&cur[1], base + kOffBack, 8, cudaMemcpyDeviceToHost) != cudaSuccess)
+      return FS_ECUDA;
+    if (pass == 0) {
+      matches = cur[0];
+      if (matches == 0 || matches > cap) return (int64_t)matches;
+    } else if (cur[0] + cur[1] != matches) {
+      return FS_ECUDA;  // the cursors must meet exactly at the pass-1 count
+    }
+  }
+  return (int64_t)matches;
+}
+
 int64_t fs_enumerate(uint64_t n, const uint32_t *gens, int d, int B, void *out_dev, uint64_t cap) {
   fs_exec_t ex;
   memset(&ex, 0, sizeof(ex));

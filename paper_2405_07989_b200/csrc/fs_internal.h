@@ -71,6 +71,11 @@ struct KParams {
   unsigned long long *diff_out;
   uint32_t diff_len;
   uint32_t hist_rep;  // closed-tail histogram: 32 = one difference-array copy per lane (bank-private), else 1
+  // filtered materialise (M2 staged kernel): only rows satisfying
+  // filt_pred(filt_arg) are compacted; count_only = pass 1 (count them into *front)
+  int filt_pred;
+  uint64_t filt_arg;
+  int count_only;
 };
 
 }  // namespace fs

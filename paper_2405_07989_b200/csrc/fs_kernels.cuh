@@ -103,6 +103,22 @@ __device__ __forceinline__ uint32_t coord(const Lane<D> &st, uint32_t i, uint32_
   return v;
 }
 
+// pred(row) for the current row (a_d = ad): the fs_any predicates ("setting a boolean
+// variable based on a predicate"); COORD_GE's index is the stream's internal coordinate.
+template <int D>
+__device__ __forceinline__ bool pred_row_holds(const Lane<D> &st, uint32_t ad, int pred, uint64_t arg) {
+  const uint64_t len = (uint64_t)cur_lsum<D>(st) + (uint32_t)st.cur + ad;
+  switch (pred) {
+    case FS_PRED_LEN_LE: return len <= arg;
+    case FS_PRED_LEN_GE: return len >= arg;
+    case FS_PRED_LEN_EQ: return len == arg;
+    default: {
+      const uint32_t i = (uint32_t)(arg >> 32);
+      return i < (uint32_t)D && coord<D>(st, i, ad) >= (uint32_t)(arg & 0xffffffffu);
+    }
+  }
+}
+
 template <int D>
 struct EmitAny {
   int pred;
@@ -113,17 +129,7 @@ struct EmitAny {
   __device__ __forceinline__ void cond(bool em, const Lane<D> &st, const Consts &c) {
     if (!em) return;
     const uint32_t ad = row_ad<D>(st, c);
-    const uint64_t len = (uint64_t)cur_lsum<D>(st) + (uint32_t)st.cur + ad;
-    bool ok;
-    switch (pred) {
-      case FS_PRED_LEN_LE: ok = len <= arg; break;
-      case FS_PRED_LEN_GE: ok = len >= arg; break;
-      case FS_PRED_LEN_EQ: ok = len == arg; break;
-      default: {
-        const uint32_t i = (uint32_t)(arg >> 32);
-        ok = i < (uint32_t)D && coord<D>(st, i, ad) >= (uint32_t)(arg & 0xffffffffu);
-      }
-    }
+    const bool ok = pred_row_holds<D>(st, ad, pred, arg);
     if (ok && !hit) {
       hit = true;
       if (atomicCAS(found, 0, 1) == 0 && wit) {  // caller's coordinate order
@@ -305,8 +311,16 @@ struct EmitCompact {
     else
       sts32(a, v);
   }
+  int filt_pred;        // 0: every row; else only rows satisfying this fs_any predicate (NEXT-4)
+  uint64_t filt_arg;
+  bool count_only;      // filtered pass 1: count the warp's matching rows, write nothing
   __device__ __forceinline__ void cond(bool em, const Lane<D> &st, const Consts &c) {
+    if (filt_pred) em = em && pred_row_holds<D>(st, row_ad<D>(st, c), filt_pred, filt_arg);
     const unsigned m = __ballot_sync(kFull, em);
+    if (count_only) {
+      tail += (uint32_t)__popc(m);
+      return;
+    }
     if (em) {  // coordinates written at the caller's positions (generator order may differ)
       uint32_t pos = wpos + (uint32_t)__popc(m & lanemask_lt()) * kRB;
       if (pos >= kRing) pos -= kRing;
@@ -371,6 +385,7 @@ struct EmitCompact {
   }
   // converged; keeps room for `room` more rows
   __device__ __forceinline__ void flush(const KParams &P, bool final, uint32_t room = 32) {
+    if (count_only) return;
     if (resv && (final || rows() + room > kCap)) write_out(P);
     if (!resv && (final || rows() >= kCap * FS_M2_TH / 8u || rows() + room > kCap)) {
       reserve(P);
@@ -379,6 +394,10 @@ struct EmitCompact {
   }
   // converged, at warp exit: the final < 8 rows go to the back cursor with plain stores
   __device__ __forceinline__ void finish(const KParams &P) {
+    if (count_only) {
+      if ((threadIdx.x & 31) == 0 && rows()) atomicAdd(P.front, (unsigned long long)rows());
+      return;
+    }
     flush(P, true);
     const uint32_t r = rows();
     if (r == 0) return;
@@ -733,6 +752,9 @@ __global__ void __launch_bounds__(kBlock, (CONS == kConsRowsAny || CONS == FS_CO
   unsigned char *wslot = stage + kBlock * kLaneStride + (threadIdx.x >> 5) * 32;
   EmitCompact<D, B> e_cmp;
   e_cmp.init(c, stage + (threadIdx.x >> 5) * kWarpBuf);
+  e_cmp.filt_pred = P.filt_pred;
+  e_cmp.filt_arg = P.filt_arg;
+  e_cmp.count_only = P.count_only != 0;
 
   for (;;) {
     const bool need = alive && needs_refill<D, ALPHA>(st, budget);

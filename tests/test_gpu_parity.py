@@ -191,6 +191,54 @@ def test_any(oracle_mod, inst):
                 assert tuple(wit) in rowset
 
 
+def _pack(rows, d, B):
+    fmt = "<%d%s" % (d, "H" if B == 16 else "I")
+    return b"".join(struct.pack(fmt, *r) for r in rows)
+
+
+@pytest.mark.parametrize("inst", ALL[:40], ids=ids)
+def test_rows_filtered(oracle_mod, inst):
+    """Filtered materialise (NEXT-4): exactly the oracle rows satisfying the predicate (sorted =
+    the canonical order of that subset), for every predicate kind around the attained bounds,
+    both coordinate widths, given and auto generator order, tiny slices, and the count-only /
+    too-small-cap contract."""
+    n, g = inst.n, inst.gens
+    d = len(g)
+    rows = oracle.rows_as_tuples(oracle.rows(n, g, B=32), d, 32)
+    lens = sorted(set(sum(r) for r in rows)) or [0]
+    preds = [(L.FS_PRED_LEN_LE, lens[0]), (L.FS_PRED_LEN_LE, lens[len(lens) // 2]), (L.FS_PRED_LEN_GE, lens[-1]),
+             (L.FS_PRED_LEN_EQ, lens[len(lens) // 2]), (L.FS_PRED_LEN_EQ, lens[0] - 1 if lens[0] else 1 << 40),
+             (L.FS_PRED_COORD_GE, ((d - 1) << 32) | 2), (L.FS_PRED_COORD_GE, (0 << 32) | 1)]
+    for i in range(d):
+        top = max((r[i] for r in rows), default=0)
+        preds.append((L.FS_PRED_COORD_GE, (i << 32) | max(0, top - 1)))
+    for B in (16, 32):
+        if B == 16 and max(n // x for x in g) > 65535:
+            continue
+        for k, (pred, arg) in enumerate(preds):
+            want = [r for r in rows if oracle.pred_holds(r, pred, arg)]
+            kw = [{}, {"gen_order": L.FS_GENORDER_AUTO}, {"slice_units": 64}][k % 3]
+            m, t = api.fs_enumerate_filtered(n, g, pred, arg, B=B, **kw)
+            assert m == len(want), (pred, arg)
+            assert rows_bytes(api.sort_rows_desc(t)) == _pack(want, d, B)
+            if want:  # too small a cap: the count, nothing written
+                m2, t2 = api.fs_enumerate_filtered(n, g, pred, arg, B=B, cap=len(want) - 1)
+                assert m2 == len(want) and t2.shape[0] == 0
+
+
+def test_rows_filtered_c2(oracle_mod):
+    """C2 (681,152 rows): one length class, sharded over 3 virtual ranks."""
+    n, g = W.C2.n, W.C2.gens
+    rows = oracle.rows_as_tuples(oracle.rows(n, g, B=16), 5, 16)
+    X = 120
+    want = [r for r in rows if sum(r) == X]
+    got = []
+    for r in range(3):
+        m, t = api.fs_enumerate_filtered(n, g, L.FS_PRED_LEN_EQ, X, B=16, rank=r, world=3)
+        got += oracle.rows_as_tuples(rows_bytes(t), 5, 16)
+    assert sorted(got, reverse=True) == want
+
+
 @pytest.mark.parametrize("inst", ALL[:40], ids=ids)
 def test_rows_order_any(oracle_mod, inst):
     """M2 layout (warp-aggregated compaction): same multiset of rows; sorted = canonical."""
