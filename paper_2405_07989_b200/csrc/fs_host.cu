@@ -257,6 +257,27 @@ int fs_validate_and_build(fs_plan *p, uint64_t n, const uint32_t *gens, int d, i
           }
           c.t2_off = t2o;
         }
+        // Count: the closed-tail table for TWO node advances per entry (4 words per rho):
+        // {rel(next^2(rho)) | (inc1 + inc2) << 16, inc1 + s - k0(next(rho)),
+        //  inc1 + inc2 + s - k0(next^2(rho)), 0}, where inc1/inc2 are the quotient increments
+        // of the two advances; k0 = none -> INT32_MIN (no rows).  With A the quotient before
+        // the pair, the two nodes' rows are umulhi(max(A + w, 0), ceil(2^32 / s)) and the
+        // quotient after it is A + (inc1 + inc2): one 16 B shared load serves two nodes.
+        const uint32_t c2o = ((uint32_t)p->ktab.size() + 3u) & ~3u;
+        if (consumer == FS_CONSUMER_COUNT && 2u * (c.q + 1u) < (1u << 15) &&
+            4ull * c2o + 16ull * c.gA + 16384ull <= (1ull << fs::kCAdvShift)) {
+          p->ktab.resize(c2o + 4u * c.gA, 0u);
+          for (uint32_t rho = 0; rho < c.gA; ++rho) {
+            const fs::Adv w1 = ar.step(rho, c);
+            const fs::Adv w2 = ar.step(w1.next, c);
+            uint32_t *ent = &p->ktab[c2o + 4u * rho];
+            ent[0] = (4u * c2o + 16u * w2.next) | ((w1.inc + w2.inc) << fs::kCAdvShift);
+            ent[1] = w1.k0 == fs::kNone ? 0x80000000u : (uint32_t)((int32_t)(w1.inc + c.s) - (int32_t)w1.k0);
+            ent[2] = w2.k0 == fs::kNone ? 0x80000000u
+                                        : (uint32_t)((int32_t)(w1.inc + w2.inc + c.s) - (int32_t)w2.k0);
+          }
+          c.cadv2_off = c2o;
+        }
       }
       c.ktab_len = (uint32_t)p->ktab.size();
       c.ktab = p->ktab.data();

@@ -567,6 +567,42 @@ __device__ __forceinline__ void cc_group(Lane<D> &st, const Consts &c, uint32_t 
   }
 }
 
+// The same group over the paired table (Consts::cadv2_off): one LDS.128 per TWO nodes gives
+// the link two advances ahead, both nodes' row-count numerators relative to the quotient
+// before the pair, and the pair's quotient increment -- per node: half a shared load, one
+// add-max, one predicated umulhi-accumulate (and half a mask/shift).
+template <int D, int G>
+__device__ __forceinline__ void cc_group2(Lane<D> &st, const Consts &c, uint32_t tab2, uint32_t &cnt) {
+  static_assert(G % 2 == 0, "nodes per group must be even");
+  if constexpr (D >= 3) {
+    uint32_t h = tab2 + 16u * st.rho;
+    uint32_t A = st.A;
+    const uint32_t kk = st.k;
+    uint32_t n = cnt;
+#pragma unroll
+    for (int v = 0; v < G / 2; ++v) {
+      uint32_t w0, w1, w2, w3;
+      asm("ld.shared.v4.u32 {%0, %1, %2, %3}, [%4];" : "=r"(w0), "=r"(w1), "=r"(w2), "=r"(w3) : "r"(h));
+      (void)w3;
+      h = w0 & ((1u << kCAdvShift) - 1u);
+      int32_t x1 = (int32_t)(A + w1), x2 = (int32_t)(A + w2);
+      x1 = x1 > 0 ? x1 : 0;
+      x2 = x2 > 0 ? x2 : 0;
+      A += w0 >> kCAdvShift;
+      asm("{\n\t.reg .pred p;\n\tsetp.lt.u32 p, %2, %3;\n\t@p mad.hi.u32 %0, %1, %4, %0;\n\t}"
+          : "+r"(n)
+          : "r"((uint32_t)x1), "r"((uint32_t)(2 * v)), "r"(kk), "r"(c.mhi));
+      asm("{\n\t.reg .pred p;\n\tsetp.lt.u32 p, %2, %3;\n\t@p mad.hi.u32 %0, %1, %4, %0;\n\t}"
+          : "+r"(n)
+          : "r"((uint32_t)x2), "r"((uint32_t)(2 * v + 1)), "r"(kk), "r"(c.mhi));
+    }
+    cnt = n;
+    st.rho = (h - tab2) >> 4;
+    st.A = A;
+    st.k = kk > (uint32_t)G ? kk - (uint32_t)G : 0u;
+  }
+}
+
 // Length histogram with the closed tail, group form (Consts::cadv_off set for a histogram
 // plan): per node one shared load gives the next entry's address, the quotient increment,
 // s - k0 and ad0 - k0 (packed into one word when both fit 16 bits), so the node's first-row
@@ -694,10 +730,15 @@ __global__ void __launch_bounds__(kBlock, (CONS == kConsRowsAny || CONS == FS_CO
   uint32_t t2a = t2base, q2 = 0;  // count: ascend-table entry of r = R_{L-1} mod g_L, Q = R_{L-1} / g_L
   for (uint32_t i = threadIdx.x; i < c.ktab_len; i += blockDim.x) {
     uint32_t v = c.ktab[i];
-    if ((cfast || hfast) && i >= c.cadv_off && (i - c.cadv_off) % c.cadv_words == 0u &&
-        (c.t2_off == 0u || i < c.t2_off))
+    // link words (byte offsets of table entries) get the table's shared-memory base
+    if ((cfast || hfast) && i >= c.cadv_off && i < c.cadv_off + c.cadv_words * c.gA &&
+        (i - c.cadv_off) % c.cadv_words == 0u)
       v += ktab_base;
-    if (cfast && c.t2_off != 0u && i >= c.t2_off && ((i - c.t2_off) & 3u) == 0u) v += ktab_base;
+    if (cfast && c.t2_off != 0u && D >= 4 && i >= c.t2_off && i < c.t2_off + 4u * c.g[D >= 4 ? D - 3 : 0] &&
+        ((i - c.t2_off) & 3u) == 0u)
+      v += ktab_base;
+    if (cfast && c.cadv2_off != 0u && i >= c.cadv2_off && i < c.cadv2_off + 4u * c.gA && ((i - c.cadv2_off) & 3u) == 0u)
+      v += ktab_base;
     ktab_s[i] = v;
   }
   if (HISTLIKE) {
@@ -832,7 +873,9 @@ __global__ void __launch_bounds__(kBlock, (CONS == kConsRowsAny || CONS == FS_CO
       const bool had = budget != 0;
       // UNROLL branch-free fast steps, then one (warp-uniform) check for lanes parked on an
       // ascend; the rare slow lanes run the generic successor step together.
-      if (cfast) {
+      if (cfast && c.cadv2_off != 0u && (UNROLL % 2) == 0) {
+        cc_group2<D, (UNROLL % 2) == 0 ? UNROLL : 2>(st, c, ktab_base + 4u * c.cadv2_off, e_count.n);
+      } else if (cfast) {
         cc_group<D, UNROLL>(st, c, ktab_base + 4u * c.cadv_off, e_count.n);
       } else if (CONS == kConsAnyClosed) {
 #pragma unroll
