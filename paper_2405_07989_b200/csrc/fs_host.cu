@@ -256,6 +256,36 @@ int fs_validate_and_build(fs_plan *p, uint64_t n, const uint32_t *gens, int d, i
             ent[2] = rows0;
           }
           c.t2_off = t2o;
+          // Count: two-level ascend table over r3 = R_{L-2} mod g_{L-1} (L >= 3), for a lane
+          // whose a_L and a_{L-1} are both 0: a_{L-2} -= 1, R_{L-2} += g_{L-2} moves r3 to
+          // r3' = (r3 + g_{L-2}) mod g_{L-1} and Q3 = floor(R_{L-2} / g_{L-1}) (the new a_{L-1})
+          // up by dQ3; then a_L = floor(r3' / g_L), r2 = r3' mod g_L, and the new run's entry
+          // node (A0, rho0, rows0) -- all functions of r3.  Entry
+          // {rel(r3') | dQ3 << 16, rho0 | A0 << 16, rows0 | r3' << 16, r2 | a_L << 16}.
+          const uint32_t gL2 = L >= 3 ? gens[L - 3] : 0u;
+          const uint32_t t3o = ((uint32_t)p->ktab.size() + 3u) & ~3u;
+          if (L >= 3 && gL1 <= 2048u && gL2 / gL1 + 1u < 65536u && gL1 < 65536u && gL < 65536u &&
+              4ull * t3o + 16ull * gL1 + 16384ull <= (1ull << fs::kCAdvShift)) {
+            bool fits = true;
+            std::vector<uint32_t> t3(4u * gL1, 0u);
+            for (uint32_t r = 0; r < gL1 && fits; ++r) {
+              const uint32_t R3 = r + gL2, dQ3 = R3 / gL1, r3 = R3 % gL1;
+              const uint32_t aL = r3 / gL, r2 = r3 % gL;
+              const uint32_t A0 = r2 / c.gA, rho0 = r2 % c.gA, k0 = fs::k0_arith(rho0, c);
+              const uint32_t rows0 = (k0 == fs::kNone || k0 > A0) ? 0u : (A0 - k0) / c.s + 1u;
+              if (rows0 >= 65536u || aL >= 65536u) fits = false;
+              uint32_t *ent = &t3[4u * r];
+              ent[0] = (4u * t3o + 16u * r3) | (dQ3 << 16);
+              ent[1] = rho0 | (A0 << 16);
+              ent[2] = rows0 | (r3 << 16);
+              ent[3] = r2 | (aL << 16);
+            }
+            if (fits) {
+              p->ktab.resize(t3o, 0u);
+              p->ktab.insert(p->ktab.end(), t3.begin(), t3.end());
+              c.t3_off = t3o;
+            }
+          }
         }
         // Count: the closed-tail table for TWO node advances per entry (4 words per rho):
         // {rel(next^2(rho)) | (inc1 + inc2) << 16, inc1 + s - k0(next(rho)),
@@ -263,18 +293,24 @@ int fs_validate_and_build(fs_plan *p, uint64_t n, const uint32_t *gens, int d, i
         // of the two advances; k0 = none -> INT32_MIN (no rows).  With A the quotient before
         // the pair, the two nodes' rows are umulhi(max(A + w, 0), ceil(2^32 / s)) and the
         // quotient after it is A + (inc1 + inc2): one 16 B shared load serves two nodes.
+        // The table is stored in 8 interleaved copies, entry (rho, j) at 16 (8 rho + j) bytes,
+        // each copy's links pointing into the same copy: lane l reads copy l mod 8, so the 8
+        // lanes of a quarter-warp always hit 8 distinct 16 B bank groups (one wavefront per
+        // quarter; a single copy of a small table gave 1.8e9 bank conflicts on C3).
         const uint32_t c2o = ((uint32_t)p->ktab.size() + 3u) & ~3u;
         if (consumer == FS_CONSUMER_COUNT && 2u * (c.q + 1u) < (1u << 15) &&
-            4ull * c2o + 16ull * c.gA + 16384ull <= (1ull << fs::kCAdvShift)) {
-          p->ktab.resize(c2o + 4u * c.gA, 0u);
+            4ull * c2o + 128ull * c.gA + 16384ull <= (1ull << fs::kCAdvShift)) {
+          p->ktab.resize(c2o + 32u * c.gA, 0u);
           for (uint32_t rho = 0; rho < c.gA; ++rho) {
             const fs::Adv w1 = ar.step(rho, c);
             const fs::Adv w2 = ar.step(w1.next, c);
-            uint32_t *ent = &p->ktab[c2o + 4u * rho];
-            ent[0] = (4u * c2o + 16u * w2.next) | ((w1.inc + w2.inc) << fs::kCAdvShift);
-            ent[1] = w1.k0 == fs::kNone ? 0x80000000u : (uint32_t)((int32_t)(w1.inc + c.s) - (int32_t)w1.k0);
-            ent[2] = w2.k0 == fs::kNone ? 0x80000000u
-                                        : (uint32_t)((int32_t)(w1.inc + w2.inc + c.s) - (int32_t)w2.k0);
+            for (uint32_t j = 0; j < 8u; ++j) {
+              uint32_t *ent = &p->ktab[c2o + 4u * (8u * rho + j)];
+              ent[0] = (4u * c2o + 16u * (8u * w2.next + j)) | ((w1.inc + w2.inc) << fs::kCAdvShift);
+              ent[1] = w1.k0 == fs::kNone ? 0x80000000u : (uint32_t)((int32_t)(w1.inc + c.s) - (int32_t)w1.k0);
+              ent[2] = w2.k0 == fs::kNone ? 0x80000000u
+                                          : (uint32_t)((int32_t)(w1.inc + w2.inc + c.s) - (int32_t)w2.k0);
+            }
           }
           c.cadv2_off = c2o;
         }

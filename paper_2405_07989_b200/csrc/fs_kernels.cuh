@@ -540,6 +540,52 @@ __device__ __forceinline__ void t2_ascend(Lane<D> &st, const Consts &c, uint32_t
   }
 }
 
+// Count: the two-level ascend (a_L = a_{L-1} = 0: a_{L-2} -= 1, re-solve a_{L-1} and a_L,
+// enter the new run) as one LDS.128 of the t3 table (Consts::t3_off, fs_host.cu) instead of
+// the generic ascend's rightmost-nonzero search and four magic divisions.  t3a/q3 track
+// r3 = R_{L-2} mod g_{L-1} and Q3 = floor(R_{L-2} / g_{L-1}); the t2 state follows from the
+// entry.  (0-based: a[L-3] is a_{L-2}.)
+template <int D>
+__device__ __forceinline__ bool t3_can_ascend(const Lane<D> &st) {
+  if constexpr (D >= 5)
+    return st.a[D - 4] == 0u && st.a[D - 5] > 0u;
+  else
+    return false;
+}
+template <int D>
+__device__ __forceinline__ void t3_sync(const Lane<D> &st, const Consts &c, uint32_t t3base, uint32_t &t3a,
+                                        uint32_t &q3) {
+  if constexpr (D >= 5) {
+    constexpr int L = D - 2;
+    const uint32_t R3 = st.R[L - 3];
+    q3 = divq(R3, c.dv[L - 2]);
+    t3a = t3base + 16u * (R3 - q3 * c.g[L - 2]);
+  }
+}
+template <int D>
+__device__ __forceinline__ void t3_ascend(Lane<D> &st, const Consts &c, uint32_t &t3a, uint32_t &q3, uint32_t t2base,
+                                          uint32_t &t2a, uint32_t &q2, uint32_t &cnt) {
+  if constexpr (D >= 5) {
+    constexpr int L = D - 2;
+    const uint4 w = lds128(t3a);
+    t3a = w.x & ((1u << kCAdvShift) - 1u);
+    q3 += w.x >> 16;
+    st.a[L - 3] -= 1u;
+    st.R[L - 3] += c.g[L - 3];
+    st.a[L - 2] = q3;
+    st.R[L - 2] = w.z >> 16;
+    const uint32_t aL = w.w >> 16;
+    st.a[L - 1] = aL;
+    st.lsum = st.lsum - 1u + q3 + aL;
+    st.rho = w.y & 0xffffu;
+    st.A = w.y >> 16;
+    st.cur = -1;  // the entry node's rows are taken here
+    cnt += w.z & 0xffffu;
+    q2 = aL;
+    t2a = t2base + 16u * (w.w & 0xffffu);
+  }
+}
+
 template <int D, int G>
 __device__ __forceinline__ void cc_group(Lane<D> &st, const Consts &c, uint32_t tab, uint32_t &cnt) {
   if constexpr (D >= 3) {
@@ -575,7 +621,7 @@ template <int D, int G>
 __device__ __forceinline__ void cc_group2(Lane<D> &st, const Consts &c, uint32_t tab2, uint32_t &cnt) {
   static_assert(G % 2 == 0, "nodes per group must be even");
   if constexpr (D >= 3) {
-    uint32_t h = tab2 + 16u * st.rho;
+    uint32_t h = tab2 + 16u * (8u * st.rho + (threadIdx.x & 7u));  // the lane's copy (bank group)
     uint32_t A = st.A;
     const uint32_t kk = st.k;
     uint32_t n = cnt;
@@ -597,7 +643,7 @@ __device__ __forceinline__ void cc_group2(Lane<D> &st, const Consts &c, uint32_t
           : "r"((uint32_t)x2), "r"((uint32_t)(2 * v + 1)), "r"(kk), "r"(c.mhi));
     }
     cnt = n;
-    st.rho = (h - tab2) >> 4;
+    st.rho = (h - tab2) >> 7;
     st.A = A;
     st.k = kk > (uint32_t)G ? kk - (uint32_t)G : 0u;
   }
@@ -728,6 +774,9 @@ __global__ void __launch_bounds__(kBlock, (CONS == kConsRowsAny || CONS == FS_CO
   const bool t2fast = cfast && D >= 4 && c.t2_off != 0;
   const uint32_t t2base = ktab_base + 4u * c.t2_off;
   uint32_t t2a = t2base, q2 = 0;  // count: ascend-table entry of r = R_{L-1} mod g_L, Q = R_{L-1} / g_L
+  const bool t3fast = t2fast && D >= 5 && c.t3_off != 0;
+  const uint32_t t3base = ktab_base + 4u * c.t3_off;
+  uint32_t t3a = t3base, q3 = 0;  // count: two-level ascend entry of r3 = R_{L-2} mod g_{L-1}, Q3
   for (uint32_t i = threadIdx.x; i < c.ktab_len; i += blockDim.x) {
     uint32_t v = c.ktab[i];
     // link words (byte offsets of table entries) get the table's shared-memory base
@@ -737,7 +786,10 @@ __global__ void __launch_bounds__(kBlock, (CONS == kConsRowsAny || CONS == FS_CO
     if (cfast && c.t2_off != 0u && D >= 4 && i >= c.t2_off && i < c.t2_off + 4u * c.g[D >= 4 ? D - 3 : 0] &&
         ((i - c.t2_off) & 3u) == 0u)
       v += ktab_base;
-    if (cfast && c.cadv2_off != 0u && i >= c.cadv2_off && i < c.cadv2_off + 4u * c.gA && ((i - c.cadv2_off) & 3u) == 0u)
+    if (cfast && c.cadv2_off != 0u && i >= c.cadv2_off && i < c.cadv2_off + 32u * c.gA && ((i - c.cadv2_off) & 3u) == 0u)
+      v += ktab_base;
+    if (cfast && c.t3_off != 0u && D >= 5 && i >= c.t3_off && i < c.t3_off + 4u * c.g[D >= 5 ? D - 4 : 0] &&
+        ((i - c.t3_off) & 3u) == 0u)
       v += ktab_base;
     ktab_s[i] = v;
   }
@@ -850,6 +902,7 @@ __global__ void __launch_bounds__(kBlock, (CONS == kConsRowsAny || CONS == FS_CO
             if (CONS == FS_CONSUMER_ROWS) e_rows.start((u - P.unit0) * (uint64_t)EmitRows<D, B>::kRB);
             if (cfast) e_count.n += take_entry_rows<D>(st, c);
             if (t2fast) t2_sync<D>(st, c, t2base, t2a, q2);
+            if (t3fast) t3_sync<D>(st, c, t3base, t3a, q3);
             if (hfast) take_entry_hist<D>(st, c, e_hcl);
           }
         }
@@ -926,12 +979,17 @@ __global__ void __launch_bounds__(kBlock, (CONS == kConsRowsAny || CONS == FS_CO
             t2_ascend<D>(st, c, t2a, q2, e_count.n);
             budget -= 1u;
             sync_k<D, ALPHA>(st, budget);
+          } else if (t3fast && t3_can_ascend<D>(st)) {  // two-level ascend by table (count)
+            t3_ascend<D>(st, c, t3a, q3, t2base, t2a, q2, e_count.n);
+            budget -= 1u;
+            sync_k<D, ALPHA>(st, budget);
           } else {
           slow_step<D, NEED_AD, ALPHA>(st, c, kt, budget);
           if (CAND) enter_candidates<D>(st, c);
           sync_k<D, ALPHA>(st, budget);
           if (cfast) e_count.n += take_entry_rows<D>(st, c);
           if (t2fast) t2_sync<D>(st, c, t2base, t2a, q2);
+          if (t3fast) t3_sync<D>(st, c, t3base, t3a, q3);
           }
           if (hfast) take_entry_hist<D>(st, c, e_hcl);
           if (CONS == FS_CONSUMER_ROWS && budget == 0) rows_slice_done(P, e_rows, fin, fin_soff, fin_goff, fin_len);
