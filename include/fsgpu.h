@@ -89,7 +89,10 @@ enum {
  *   order       materialise layout: FS_ORDER_CANONICAL (0, default) writes every row at its
  *               exact canonical offset; FS_ORDER_ANY (1) compacts rows per warp with
  *               warp-aggregated atomics into an arbitrary order (the same multiset of rows;
- *               requires cap >= the rank's rows, else FS_ERANGE).
+ *               requires cap >= the rank's rows, else FS_ERANGE); FS_ORDER_INCREASING (2)
+ *               writes the rows in increasing lex order ("could readily be
+ *               modified to proceed in increasing order"): the first cap rows of that order,
+ *               and the _ex offset is the block's position in it (total - row_end).
  *   tail        count / histogram / any: FS_TAIL_ROWS (0, default) steps through every valid
  *               factorization of a node (one modulo-skip step per row); FS_TAIL_CLOSED (1)
  *               takes a node's rows at once (the closed form of the
@@ -127,7 +130,7 @@ typedef struct {
     int reserved[4];
 } fs_exec_t;
 
-enum { FS_ORDER_CANONICAL = 0, FS_ORDER_ANY = 1 };
+enum { FS_ORDER_CANONICAL = 0, FS_ORDER_ANY = 1, FS_ORDER_INCREASING = 2 };
 enum { FS_TAIL_ROWS = 0, FS_TAIL_CLOSED = 1, FS_TAIL_SKIP_OFF = 2, FS_TAIL_SKIP_PAPER = 3 };
 enum { FS_GENORDER_GIVEN = 0, FS_GENORDER_AUTO = 1 };
 enum { FS_ROWS_BATCH = 0, FS_ROWS_STAGED = 1 };

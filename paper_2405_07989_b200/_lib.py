@@ -15,7 +15,7 @@ FS_OK, FS_EINVAL, FS_ERANGE, FS_ECUDA, FS_ENOMEM, FS_ENODEV = 0, -1, -2, -3, -4,
 FS_PRED_LEN_LE, FS_PRED_LEN_GE, FS_PRED_LEN_EQ, FS_PRED_COORD_GE = 1, 2, 3, 4
 FS_CONSUMER_COUNT, FS_CONSUMER_HIST, FS_CONSUMER_ANY, FS_CONSUMER_ROWS = 0, 1, 2, 3
 FS_MAX_D = 16
-FS_ORDER_CANONICAL, FS_ORDER_ANY = 0, 1
+FS_ORDER_CANONICAL, FS_ORDER_ANY, FS_ORDER_INCREASING = 0, 1, 2
 FS_TAIL_ROWS, FS_TAIL_CLOSED, FS_TAIL_SKIP_OFF, FS_TAIL_SKIP_PAPER = 0, 1, 2, 3
 FS_GENORDER_GIVEN, FS_GENORDER_AUTO = 0, 1
 FS_ROWS_BATCH, FS_ROWS_STAGED = 0, 1

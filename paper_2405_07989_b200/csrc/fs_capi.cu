@@ -222,7 +222,13 @@ int fs_plan_enumerate_async(fs_plan *p, int B, void *out_dev, uint64_t cap) {
   const uint64_t take = cap < span ? cap : span;
   if (take == 0) return finish(p, FS_OK);
   if (!out_dev) return FS_EINVAL;
+  const bool incr = p->ex.order == FS_ORDER_INCREASING;
+  if (p->ex.order != FS_ORDER_CANONICAL && p->ex.order != FS_ORDER_ANY && !incr) return FS_EINVAL;
   kp.unit1 = p->unit_begin + take;
+  if (incr) {  // the first `take` rows in increasing order = the last `take` canonical rows
+    kp.unit0 = p->unit_end - take;
+    kp.unit1 = p->unit_end;
+  }
   kp.num_slices = (take + p->T - 1) / p->T;
   kp.num_claims = kp.num_slices;
   kp.rows_out = reinterpret_cast<unsigned char *>(out_dev);
@@ -241,7 +247,8 @@ int fs_plan_enumerate_async(fs_plan *p, int B, void *out_dev, uint64_t cap) {
     }
     int launches = 0;
     uint32_t grid = 0;
-    rc = fs_dispatch_rows_batch(p, B, p->ex.order == FS_ORDER_ANY, kp, p->stream, false, &grid, &launches);
+    rc = fs_dispatch_rows_batch(p, B, p->ex.order == FS_ORDER_ANY ? 1 : incr ? 2 : 0, kp, p->stream, false, &grid,
+                                &launches);
     if (rc != FS_OK) return rc;
     p->grid = grid;
     g_fs_total_launches += (unsigned long long)launches;
@@ -256,6 +263,14 @@ int fs_plan_enumerate_async(fs_plan *p, int B, void *out_dev, uint64_t cap) {
     kp.back = reinterpret_cast<unsigned long long *>(base + kOffBack);
     kp.rank_rows = span;
     return finish(p, fs_launch(p, fs::kConsRowsAny, B, kp, p->stream));
+  }
+  if (incr) {  // staged kernel in canonical order, then the rows reversed in place
+    rc = fs_launch(p, FS_CONSUMER_ROWS, B, kp, p->stream);
+    if (rc != FS_OK) return rc;
+    rc = fs_launch_rows_reverse(kp.rows_out, take, kp.row_bytes, p->stream);
+    if (rc != FS_OK) return rc;
+    p->last_launches = 2;
+    return FS_OK;
   }
   return finish(p, fs_launch(p, FS_CONSUMER_ROWS, B, kp, p->stream));
 }
@@ -368,7 +383,8 @@ int64_t fs_enumerate_ex(uint64_t n, const uint32_t *gens, int d, int B, void *ou
         return FS_ECUDA;
     }
   }
-  if (global_row_offset_out) *global_row_offset_out = h.p->row_begin;
+  if (global_row_offset_out)  // the block's first row in the requested order
+    *global_row_offset_out = h.p->ex.order == FS_ORDER_INCREASING ? h.p->total_rows - h.p->row_end : h.p->row_begin;
   return (int64_t)(h.p->row_end - h.p->row_begin);
 }
 

@@ -123,6 +123,8 @@ int fs_launch_hist_finalize(const fs::KParams &kp, cudaStream_t stream);
 extern unsigned long long g_fs_total_launches;
 // lockstep batch materialise kernel (fs_k_rowsb.cu)
 bool fs_rows_batch_supported(const fs_plan *p, int B);
-bool fs_rows_batch_shape_ok(int d);  // some B in {16, 32} has a batch kernel for d coordinates
-int fs_dispatch_rows_batch(fs_plan *p, int B, bool any, const fs::KParams &kp, cudaStream_t s, bool query_only,
+bool fs_rows_batch_shape_ok(int d);
+int fs_launch_rows_reverse(unsigned char *out, uint64_t rows, uint32_t rb, cudaStream_t stream);  // some B in {16, 32} has a batch kernel for d coordinates
+// mode: 0 canonical (M1), 1 order any (M2), 2 increasing lex order (mirrored M1)
+int fs_dispatch_rows_batch(fs_plan *p, int B, int mode, const fs::KParams &kp, cudaStream_t s, bool query_only,
                            uint32_t *grid_out, int *launches);

@@ -15,6 +15,12 @@
 //   any (M2):       the warp reserves 32 * NBUF * NB rows on the front cursor with one
 //                   atomicAdd and writes its whole staging area as ONE contiguous block.
 // The rank's ragged last slice (< T rows) is written by fs_rows_tail_kernel.
+// MODE 2 (increasing lex order, "could readily be modified to proceed in increasing
+// order"): the same stream written mirrored -- output row p holds canonical row E-1-p of the
+// enumerated range [0, E); slices are anchored at the output side (slice j = output rows
+// [jT, jT + T) = canonical rows [E - jT - T, E - jT)), rows inside a batch and batches inside
+// a group are placed in reverse, so every group is still one aligned 16 B-multiple segment;
+// the ragged slice (canonical rows [0, E - nfull T)) goes to the tail kernel.
 #pragma once
 
 #include "fs_kernels.cuh"
@@ -184,9 +190,10 @@ __device__ __forceinline__ void rb_ensure_row(Lane<D> &st, uint32_t &ad, typenam
   }
 }
 
-template <int D, int B, bool ANY, bool KTAB>
+template <int D, int B, int MODE, bool KTAB>
 __global__ void __launch_bounds__(kRbBlock, 1) fs_rows_batch_kernel(const KParams P) {
   using G = RowsBatchGeom<D, B>;
+  constexpr bool ANY = MODE == 1, REV = MODE == 2;
   constexpr int L = D - 2;
   extern __shared__ __align__(16) unsigned char smem[];
   const Consts &c = P.c;
@@ -245,7 +252,8 @@ __global__ void __launch_bounds__(kRbBlock, 1) fs_rows_batch_kernel(const KParam
     const uint64_t rem = P.num_slices - base;
     const uint32_t nlive = rem < 32u ? (uint32_t)rem : 32u;
     if (live) {
-      const uint64_t u = P.unit0 + idx * P.T;
+      // REV: slice idx = output rows [idx T, idx T + T) = canonical rows E - idx T - T ..
+      const uint64_t u = REV ? P.unit1 - (idx + 1) * P.T : P.unit0 + idx * P.T;
       const uint64_t off = unrank<D, true>(st, c, kt, u);
       st.cur -= (int32_t)((uint32_t)off * s);  // row units: skip to row `off` of the node
       ad = rb_solve_ad<D>(st, c);
@@ -273,6 +281,8 @@ __global__ void __launch_bounds__(kRbBlock, 1) fs_rows_batch_kernel(const KParam
       for (int b = 0; b < G::NBUF; ++b) {
         uint32_t wd[G::BW];
 #pragma unroll
+        for (int i = 0; i < G::BW; ++i) wd[i] = 0u;  // halves are OR-ed in (REV fills odd halves first)
+#pragma unroll
         for (int u = 0; u < G::NB; ++u) {
           rb_ensure_row<D>(st, ad, wn, c, rc, kt, ra);
           uint32_t v[D];
@@ -280,24 +290,23 @@ __global__ void __launch_bounds__(kRbBlock, 1) fs_rows_batch_kernel(const KParam
           for (int j = 0; j < L; ++j) v[j] = st.a[j];
           v[D - 2] = (uint32_t)st.cur;
           v[D - 1] = ad;
+          const int us = REV ? G::NB - 1 - u : u;  // the row's slot in the batch
 #pragma unroll
           for (int j = 0; j < D; ++j) {
             if (B == 32) {
-              wd[u * D + j] = v[j];
+              wd[us * D + j] = v[j];
             } else {
-              const int h = u * D + j;
-              if (h & 1)
-                wd[h >> 1] |= v[j] << 16;
-              else
-                wd[h >> 1] = v[j];
+              const int h = us * D + j;
+              wd[h >> 1] |= (h & 1) ? v[j] << 16 : v[j];
             }
           }
           st.cur -= (int32_t)s;
           ad += t;
         }
+        const uint32_t bs = REV ? (uint32_t)(G::NBUF - 1 - b) : (uint32_t)b;  // the batch's slot
 #pragma unroll
         for (int i = 0; i < G::BW / 4; ++i)
-          sts128(myslot + (uint32_t)b * G::BB + 16u * i, wd[4 * i], wd[4 * i + 1], wd[4 * i + 2], wd[4 * i + 3]);
+          sts128(myslot + bs * G::BB + 16u * i, wd[4 * i], wd[4 * i + 1], wd[4 * i + 2], wd[4 * i + 3]);
       }
       __syncwarp();
       if (ANY) {
@@ -309,7 +318,9 @@ __global__ void __launch_bounds__(kRbBlock, 1) fs_rows_batch_kernel(const KParam
           if (l < nlive) __stcs(dst + q, lds128_nv(wstage + l * G::STRIDE + part * 16u));
         }
       } else {
-        unsigned char *dst = dst0 + (uint64_t)grp * G::FG;
+        // REV: group grp of slice j = output rows [jT + T - (grp+1) GR, jT + T - grp GR)
+        unsigned char *dst = dst0 + (REV ? (P.T - (uint64_t)(grp + 1) * G::GR) * (uint64_t)G::RB
+                                         : (uint64_t)grp * G::FG);
 #pragma unroll 4
         for (int it = 0; it < G::C; ++it) {
           const uint32_t q = (uint32_t)it * 32u + (uint32_t)lane;
@@ -323,14 +334,15 @@ __global__ void __launch_bounds__(kRbBlock, 1) fs_rows_batch_kernel(const KParam
   }
 }
 
-// The rank's ragged last slice: rows [unit0 + first, unit1) (fewer than T), split across the
-// threads of one CTA; each thread unranks its first row and stores its rows coordinate by
-// coordinate (M1: at their canonical offsets; M2: at the back of the rank's block, where the
-// back cursor grows down from rank_rows).
-template <int D, int B, bool ANY>
-__global__ void fs_rows_tail_kernel(const KParams P, uint64_t first) {
+// The rank's ragged slice: canonical rows [unit0 + first, unit0 + first + rows) (fewer than
+// T), split across the threads of one CTA; each thread unranks its first row and stores its
+// rows coordinate by coordinate (M1: at their canonical offsets; M2: at the back of the rank's
+// block, where the back cursor grows down from rank_rows; REV: mirrored).
+template <int D, int B, int MODE>
+__global__ void fs_rows_tail_kernel(const KParams P, uint64_t first, uint64_t rows) {
+  constexpr bool ANY = MODE == 1, REV = MODE == 2;
   const Consts &c = P.c;
-  const uint64_t rows = P.unit1 - (P.unit0 + first);
+  const uint64_t E = P.unit1 - P.unit0;
   const uint64_t per = (rows + blockDim.x - 1) / blockDim.x;
   const uint64_t r0 = (uint64_t)threadIdx.x * per;
   if (ANY && threadIdx.x == 0) atomicAdd(P.back, (unsigned long long)rows);
@@ -344,8 +356,9 @@ __global__ void fs_rows_tail_kernel(const KParams P, uint64_t first) {
   st.cur -= (int32_t)((uint32_t)off * c.s);
   uint32_t ad = rb_solve_ad<D>(st, c);
   RAdvArith::Ent wn = ra.load(st.rho, c);
-  const uint64_t out_row = ANY ? (P.rank_rows - rows + r0) : (first + r0);
+  const uint64_t out_row = ANY ? (P.rank_rows - rows + r0) : REV ? E - 1 - (first + r0) : (first + r0);
   unsigned char *q = P.rows_out + out_row * (uint64_t)(D * (B / 8));
+  const int64_t step = REV ? -(int64_t)(D * (B / 8)) : (int64_t)(D * (B / 8));
   for (uint64_t r = r0; r < r1; ++r) {
     rb_slow<D>(st, ad, wn, c, c, kt, ra);  // per thread (threads diverge here)
     uint32_t v[D];
@@ -360,7 +373,7 @@ __global__ void fs_rows_tail_kernel(const KParams P, uint64_t first) {
       else
         reinterpret_cast<uint32_t *>(q)[j] = v[j];
     }
-    q += D * (B / 8);
+    q += step;
     st.cur -= (int32_t)c.s;
     ad += c.t;
   }

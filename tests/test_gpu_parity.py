@@ -261,9 +261,19 @@ def test_rows_impls(oracle_mod, inst, impl):
         if B == 16 and max(n // x for x in g) > 65535:
             continue
         want = oracle.rows(n, g, B=B)
+        rb = len(g) * B // 8
+        rev = b"".join(want[i:i + rb] for i in range(len(want) - rb, -1, -rb)) if want else b""
         for T in (64, 192, 0):
             rows, off, t = api.fs_enumerate_ex(n, g, B=B, slice_units=T, rows_impl=impl)
             assert rows_bytes(t) == want
+            # increasing lex order: the canonical rows reversed; cap = the smallest rows
+            rows, off, t = api.fs_enumerate_ex(n, g, B=B, slice_units=T, rows_impl=impl,
+                                               order=L.FS_ORDER_INCREASING)
+            assert rows_bytes(t) == rev and off == 0
+            cap = len(want) // rb // 3
+            rows, off, t = api.fs_enumerate_ex(n, g, B=B, slice_units=T, rows_impl=impl, cap=cap,
+                                               order=L.FS_ORDER_INCREASING)
+            assert rows_bytes(t) == rev[: cap * rb]
             rows, off, t = api.fs_enumerate_ex(n, g, B=B, slice_units=T, rows_impl=impl, order=L.FS_ORDER_ANY)
             assert rows_bytes(api.sort_rows_desc(t)) == want
 
@@ -276,15 +286,21 @@ def test_rows_impls_c2(oracle_mod, impl):
     for B in (16, 32):
         want = oracle.rows(n, g, B=B)
         for world in (1, 3):
-            blob, blob_any = b"", []
+            blob, blob_any, inc = b"", [], {}
             for r in range(world):
                 rows, off, t = api.fs_enumerate_ex(n, g, B=B, rank=r, world=world, rows_impl=impl)
                 blob += rows_bytes(t)
+                rows, off, t = api.fs_enumerate_ex(n, g, B=B, rank=r, world=world, rows_impl=impl,
+                                                   order=L.FS_ORDER_INCREASING)
+                inc[off] = rows_bytes(t)
                 rows, off, t = api.fs_enumerate_ex(n, g, B=B, rank=r, world=world, rows_impl=impl,
                                                    order=L.FS_ORDER_ANY)
                 blob_any.append(rows_bytes(api.sort_rows_desc(t)))
             assert blob == want
             assert b"".join(blob_any) == want
+            rb = 5 * B // 8
+            assert b"".join(inc[k] for k in sorted(inc)) == b"".join(
+                want[i:i + rb] for i in range(len(want) - rb, -1, -rb))
 
 
 def test_rows_order_any_c2(oracle_mod):
