@@ -443,6 +443,7 @@ def extras(args, world, rank, local, dev, stream, peaks, peaks_kind, barrier, ma
     # batch kernel (default, lockstep register batches) and the round-1 staged kernels
     for order, key, go, impl in ((L.FS_ORDER_CANONICAL, "store", 0, L.FS_ROWS_BATCH),
                                  (L.FS_ORDER_ANY, "store_any", 0, L.FS_ROWS_BATCH),
+                                 (L.FS_ORDER_INCREASING, "store_increasing", 0, L.FS_ROWS_BATCH),
                                  (L.FS_ORDER_CANONICAL, "store_staged", 0, L.FS_ROWS_STAGED),
                                  (L.FS_ORDER_ANY, "store_any_staged_auto_order", L.FS_GENORDER_AUTO,
                                   L.FS_ROWS_STAGED)):
@@ -461,7 +462,8 @@ def extras(args, world, rank, local, dev, stream, peaks, peaks_kind, barrier, ma
         gbs_all = bytes_ / (ms / 1e3) / 1e9
         peak = peaks["hbm_gbs"] * world
         ex[key] = {"workload": "C2XL: Z(16000, (11,13,17,19,23)) materialise u16 rows, %s order%s"
-                               % ("canonical (exact offsets)" if order == 0 else "any (warp compaction)",
+                               % ({0: "canonical (exact offsets)", 1: "any (warp compaction)",
+                                   2: "increasing lex (mirrored exact offsets)"}[order],
                                   ", NEXT-2 generator order" if go else ""),
                    "kernel": "batch (lockstep register batches)" if impl == L.FS_ROWS_BATCH
                    else "staged (round-1 per-step emission)",
