@@ -288,8 +288,8 @@ int fs_validate_and_build(fs_plan *p, uint64_t n, const uint32_t *gens, int d, i
           }
         }
         // Count: the closed-tail table for TWO node advances per entry (4 words per rho):
-        // {rel(next^2(rho)) | (inc1 + inc2) << 16, inc1 + s - k0(next(rho)),
-        //  inc1 + inc2 + s - k0(next^2(rho)), 0}, where inc1/inc2 are the quotient increments
+        // {rel(next^2(rho)), inc1 + s - k0(next(rho)), inc1 + inc2 + s - k0(next^2(rho)),
+        //  inc1 + inc2}, where inc1/inc2 are the quotient increments
         // of the two advances; k0 = none -> INT32_MIN (no rows).  With A the quotient before
         // the pair, the two nodes' rows are umulhi(max(A + w, 0), ceil(2^32 / s)) and the
         // quotient after it is A + (inc1 + inc2): one 16 B shared load serves two nodes.
@@ -306,10 +306,11 @@ int fs_validate_and_build(fs_plan *p, uint64_t n, const uint32_t *gens, int d, i
             const fs::Adv w2 = ar.step(w1.next, c);
             for (uint32_t j = 0; j < 8u; ++j) {
               uint32_t *ent = &p->ktab[c2o + 4u * (8u * rho + j)];
-              ent[0] = (4u * c2o + 16u * (8u * w2.next + j)) | ((w1.inc + w2.inc) << fs::kCAdvShift);
+              ent[0] = 4u * c2o + 16u * (8u * w2.next + j);
               ent[1] = w1.k0 == fs::kNone ? 0x80000000u : (uint32_t)((int32_t)(w1.inc + c.s) - (int32_t)w1.k0);
               ent[2] = w2.k0 == fs::kNone ? 0x80000000u
                                           : (uint32_t)((int32_t)(w1.inc + w2.inc + c.s) - (int32_t)w2.k0);
+              ent[3] = w1.inc + w2.inc;
             }
           }
           c.cadv2_off = c2o;

@@ -615,8 +615,10 @@ __device__ __forceinline__ void cc_group(Lane<D> &st, const Consts &c, uint32_t 
 
 // The same group over the paired table (Consts::cadv2_off): one LDS.128 per TWO nodes gives
 // the link two advances ahead, both nodes' row-count numerators relative to the quotient
-// before the pair, and the pair's quotient increment -- per node: half a shared load, one
-// add-max, one predicated umulhi-accumulate (and half a mask/shift).
+// before the pair, and the pair's quotient increment -- per node: half a shared load, half an
+// add, one add-max, one predicated umulhi-accumulate.  (The predicated mad.hi's register moves
+// run on the FMA pipe; a select-masked form with fewer instructions loads the ALU pipe, which
+// is the busier one, and measured 5 % slower.)
 template <int D, int G>
 __device__ __forceinline__ void cc_group2(Lane<D> &st, const Consts &c, uint32_t tab2, uint32_t &cnt) {
   static_assert(G % 2 == 0, "nodes per group must be even");
@@ -629,12 +631,11 @@ __device__ __forceinline__ void cc_group2(Lane<D> &st, const Consts &c, uint32_t
     for (int v = 0; v < G / 2; ++v) {
       uint32_t w0, w1, w2, w3;
       asm("ld.shared.v4.u32 {%0, %1, %2, %3}, [%4];" : "=r"(w0), "=r"(w1), "=r"(w2), "=r"(w3) : "r"(h));
-      (void)w3;
-      h = w0 & ((1u << kCAdvShift) - 1u);
+      h = w0;  // the link alone (no mask): the ALU pipe is the busy one
       int32_t x1 = (int32_t)(A + w1), x2 = (int32_t)(A + w2);
       x1 = x1 > 0 ? x1 : 0;
       x2 = x2 > 0 ? x2 : 0;
-      A += w0 >> kCAdvShift;
+      A += w3;
       asm("{\n\t.reg .pred p;\n\tsetp.lt.u32 p, %2, %3;\n\t@p mad.hi.u32 %0, %1, %4, %0;\n\t}"
           : "+r"(n)
           : "r"((uint32_t)x1), "r"((uint32_t)(2 * v)), "r"(kk), "r"(c.mhi));
