@@ -52,6 +52,11 @@ struct RowsBatchGeom {
   static constexpr int C = FG / 16;                   // 16 B chunks per lane per group
   static constexpr int STRIDE = (C & 1) ? FG : FG + 16;  // odd number of 16 B units
   static constexpr size_t kWarpStage = 32u * STRIDE;
+  // group copy: chunk q = 32 it + lane -> slot l = q / C, part = q % C.  (32 it) mod C cycles
+  // with period NPH, so per lane the NPH (slot delta, part) offsets are precomputed once and a
+  // chunk's addresses are one add each (when NPH is small enough to keep them in registers)
+  static constexpr int NPH = C / cgcd(32, C);
+  static constexpr bool kPhase = NPH <= 8;
   static constexpr size_t smem_stage(int warps) { return (size_t)warps * kWarpStage; }
 };
 
@@ -275,6 +280,17 @@ __global__ void __launch_bounds__(kRbBlock, 1) fs_rows_batch_kernel(const KParam
       dst0 = P.rows_out + base * P.T * (uint64_t)G::RB;
     }
     const uint64_t SS = P.T * (uint64_t)G::RB;  // M1: bytes per slice
+    // per-lane copy offsets for the NPH phases of q = 32 it + lane (see RowsBatchGeom)
+    uint32_t so[G::kPhase ? G::NPH : 1], go[G::kPhase ? G::NPH : 1];
+    if constexpr (G::kPhase) {
+#pragma unroll
+      for (int ph = 0; ph < G::NPH; ++ph) {
+        const uint32_t x = (uint32_t)((32 * ph) % G::C) + (uint32_t)lane;
+        const uint32_t dl = x / (uint32_t)G::C, part = x - dl * (uint32_t)G::C;
+        so[ph] = dl * G::STRIDE + 16u * part;
+        go[ph] = (uint32_t)(dl * SS) + 16u * part;  // M1 (a slice is far below 4 GB)
+      }
+    }
     __syncwarp();
     for (uint32_t grp = 0; grp < groups; ++grp) {
 #pragma unroll 1
@@ -309,7 +325,27 @@ __global__ void __launch_bounds__(kRbBlock, 1) fs_rows_batch_kernel(const KParam
           sts128(myslot + bs * G::BB + 16u * i, wd[4 * i], wd[4 * i + 1], wd[4 * i + 2], wd[4 * i + 3]);
       }
       __syncwarp();
-      if (ANY) {
+      if (G::kPhase && nlive == 32u) {  // every slot live: addresses by phase, no checks
+        unsigned char *gdst = dst0 + (ANY ? (uint64_t)grp * 32u * G::FG
+                                          : REV ? (P.T - (uint64_t)(grp + 1) * G::GR) * (uint64_t)G::RB
+                                                : (uint64_t)grp * G::FG);
+        if (ANY) gdst += 16u * (uint32_t)lane;
+        // it = blk NPH + ph: slot base b = blk (32 NPH / C) + (32 ph) / C (32 NPH is a multiple
+        // of C); the phase loop is unrolled, the block loop is not (loads stay few in flight)
+        constexpr uint32_t kBStep = (uint32_t)(32 * G::NPH / G::C);
+#pragma unroll 1
+        for (uint32_t blk = 0; blk < (uint32_t)(G::C / G::NPH); ++blk) {
+#pragma unroll
+          for (int ph = 0; ph < G::NPH; ++ph) {
+            const uint32_t b = blk * kBStep + (uint32_t)((32 * ph) / G::C);
+            const uint4 v = lds128_nv(wstage + b * G::STRIDE + so[G::kPhase ? ph : 0]);
+            if (ANY)
+              __stcs(reinterpret_cast<uint4 *>(gdst + 512u * (blk * G::NPH + (uint32_t)ph)), v);
+            else
+              __stcs(reinterpret_cast<uint4 *>(gdst + b * SS + go[G::kPhase ? ph : 0]), v);
+          }
+        }
+      } else if (ANY) {
         uint4 *dst = reinterpret_cast<uint4 *>(dst0 + (uint64_t)grp * nlive * G::FG);
 #pragma unroll 4
         for (int it = 0; it < G::C; ++it) {
