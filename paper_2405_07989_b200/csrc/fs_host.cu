@@ -550,6 +550,117 @@ struct HostNodeSink {
   }
 };
 
+// The kernels' count-only closed tail with the tables (fs_kernels.cuh cc_group2, t2_ascend,
+// t3_ascend) replayed on the host for one lane, reading the same host table words: the link
+// words hold byte offsets from the table start (the kernels add their shared-memory base), and
+// the lane's copy of the paired table is j = lane mod 8.  Returns the slice's rows.
+template <int D, class KT>
+uint64_t host_count_tables_slice(const fs_plan *p, const KT &ktab, fs::Lane<D> &st, uint32_t &budget, uint32_t j) {
+  const fs::Consts &c = p->c;
+  const uint32_t *W = p->ktab.data();
+  constexpr int L = D - 2;
+  constexpr uint32_t G = FS_CC_GROUP;
+  uint64_t n = 0;
+  auto take_entry = [&]() {
+    const int32_t x = st.cur + (int32_t)c.s;
+    st.cur = -1;
+    n += fs::divq((uint32_t)(x > 0 ? x : 0), c.dvS);
+  };
+  uint32_t t2w = 0, q2 = 0, t3w = 0, q3 = 0;  // word indices of the t2 / t3 entries
+  auto t2_sync = [&]() {
+    if constexpr (D >= 4) {
+      if (!c.t2_off) return;
+      const uint32_t R1 = st.R[L - 2];
+      q2 = fs::divq(R1, c.dv[L - 1]);
+      t2w = c.t2_off + 4u * (R1 - q2 * c.g[L - 1]);
+    }
+  };
+  auto t3_sync = [&]() {
+    if constexpr (D >= 5) {
+      if (!c.t3_off) return;
+      const uint32_t R3 = st.R[L - 3];
+      q3 = fs::divq(R3, c.dv[L - 2]);
+      t3w = c.t3_off + 4u * (R3 - q3 * c.g[L - 2]);
+    }
+  };
+  take_entry();
+  t2_sync();
+  t3_sync();
+  while (!fs::needs_refill<D, 1>(st, budget)) {
+    if constexpr (D >= 3) {  // cc_group2: G nodes, two per paired-table entry
+      uint32_t h = c.cadv2_off + 4u * (8u * st.rho + j);
+      uint32_t A = st.A;
+      const uint32_t kk = st.k;
+      for (uint32_t v = 0; v < G / 2; ++v) {
+        const uint32_t *w = W + h;
+        h = w[0] / 4u;
+        int32_t x1 = (int32_t)(A + w[1]), x2 = (int32_t)(A + w[2]);
+        x1 = x1 > 0 ? x1 : 0;
+        x2 = x2 > 0 ? x2 : 0;
+        A += w[3];
+        if (2u * v < kk) n += (uint32_t)(((uint64_t)(uint32_t)x1 * c.mhi) >> 32);
+        if (2u * v + 1u < kk) n += (uint32_t)(((uint64_t)(uint32_t)x2 * c.mhi) >> 32);
+      }
+      st.rho = (h - c.cadv2_off) / 32u;
+      st.A = A;
+      st.k = kk > G ? kk - G : 0u;
+    }
+    fs::sync_k<D, 1>(st, budget);
+    if (fs::needs_slow<D>(st, budget)) {
+      bool done = false;
+      if constexpr (D >= 4) {
+        if (c.t2_off && st.a[L - 2] > 0u) {  // t2_ascend
+          const uint32_t *w = W + t2w;
+          t2w = (w[0] & 0xffffu) / 4u;
+          q2 += w[0] >> 16;
+          st.a[L - 2] -= 1u;
+          st.R[L - 2] += c.g[L - 2];
+          st.a[L - 1] = q2;
+          st.lsum = st.lsum - 1u + q2;
+          st.rho = w[1] & 0xffffu;
+          st.A = w[1] >> 16;
+          st.cur = -1;
+          n += w[2];
+          budget -= 1u;
+          fs::sync_k<D, 1>(st, budget);
+          done = true;
+        }
+      }
+      if constexpr (D >= 5) {
+        if (!done && c.t3_off && st.a[L - 2] == 0u && st.a[L - 3] > 0u) {  // t3_ascend
+          const uint32_t *w = W + t3w;
+          t3w = (w[0] & 0xffffu) / 4u;
+          q3 += w[0] >> 16;
+          st.a[L - 3] -= 1u;
+          st.R[L - 3] += c.g[L - 3];
+          st.a[L - 2] = q3;
+          st.R[L - 2] = w[2] >> 16;
+          const uint32_t aL = w[3] >> 16;
+          st.a[L - 1] = aL;
+          st.lsum = st.lsum - 1u + q3 + aL;
+          st.rho = w[1] & 0xffffu;
+          st.A = w[1] >> 16;
+          st.cur = -1;
+          n += w[2] & 0xffffu;
+          q2 = aL;
+          t2w = c.t2_off + 4u * (w[3] & 0xffffu);
+          budget -= 1u;
+          fs::sync_k<D, 1>(st, budget);
+          done = true;
+        }
+      }
+      if (!done) {
+        fs::slow_step<D, true, 1>(st, c, ktab, budget);
+        fs::sync_k<D, 1>(st, budget);
+        take_entry();
+        t2_sync();
+        t3_sync();
+      }
+    }
+  }
+  return n;
+}
+
 template <int D, int ALPHA, class KT>
 void host_model_d(const fs_plan *p, const KT &ktab, HostSink &sink, uint64_t *slice_counts, uint32_t *slice_first) {
   const Consts &c = p->c;
@@ -588,6 +699,11 @@ void host_model_d(const fs_plan *p, const KT &ktab, HostSink &sink, uint64_t *sl
                p->ex.tail == FS_TAIL_CLOSED) {
       HostNodeSink ns{p, &sink, 0};
       const bool count_only = p->consumer == FS_CONSUMER_COUNT && !sink.pred;
+      if (count_only && p->c.cadv2_off != 0) {  // the kernel's table-driven group form
+        ns.n += host_count_tables_slice<D>(p, ktab, st, budget, (uint32_t)(sl & 7u));
+        budget = 0;
+        st.cur = -1;
+      }
       while (!fs::needs_refill<D, ALPHA>(st, budget)) {
         if (count_only) {  // the kernels' count-only closed step
           uint32_t cnt = 0;
