@@ -661,6 +661,43 @@ uint64_t host_count_tables_slice(const fs_plan *p, const KT &ktab, fs::Lane<D> &
   return n;
 }
 
+// The batch materialise kernel's row stream (fs_rows_batch.cuh rb_ensure_row) replayed on the
+// host for one full row slice: table advances from the radv entry of the current residue
+// (next residue, quotient increment, k0 and a_d of the next node's first row), generic ascend
+// otherwise; one row per step.  Pins the radv table against the oracle on the CPU.
+template <int D, class KT>
+void host_rows_batch_slice(const fs_plan *p, const KT &ktab, fs::Lane<D> &st, uint32_t rows, HostSink &sink) {
+  const fs::Consts &c = p->c;
+  const uint32_t *W = p->ktab.data();
+  constexpr int L = D - 2;
+  uint32_t ad = fs::divq((st.A - (uint32_t)st.cur) * c.gA + st.rho, c.dvB);
+  for (uint32_t r = 0; r < rows; ++r) {
+    if constexpr (L >= 1) {
+      while (st.cur < 0) {
+        if (st.a[L - 1] > 0) {
+          const uint32_t *w = W + c.radv_off + 4u * st.rho;
+          st.a[L - 1] -= 1u;
+          st.rho = w[0] & ((1u << fs::kAdvBits) - 1u);
+          st.A += w[0] >> fs::kAdvBits;
+          st.cur = (int32_t)st.A - (int32_t)w[1];
+          ad = w[2];
+        } else {
+          if (!fs::ascend<D>(st, c)) return;  // end of stream (not inside a full slice)
+          st.cur = (int32_t)st.A - (int32_t)ktab(st.rho, c);
+          ad = fs::divq((st.A - (uint32_t)st.cur) * c.gA + st.rho, c.dvB);
+        }
+      }
+    }
+    uint32_t v[FS_MAX_D];
+    for (int q = 0; q < L; ++q) v[q] = st.a[q];
+    v[D - 2] = (uint32_t)st.cur;
+    v[D - 1] = ad;
+    sink.put(v);
+    st.cur -= (int32_t)c.s;
+    ad += c.t;
+  }
+}
+
 template <int D, int ALPHA, class KT>
 void host_model_d(const fs_plan *p, const KT &ktab, HostSink &sink, uint64_t *slice_counts, uint32_t *slice_first) {
   const Consts &c = p->c;
@@ -720,6 +757,9 @@ void host_model_d(const fs_plan *p, const KT &ktab, HostSink &sink, uint64_t *sl
       }
       sink.count += ns.n;
       sink.slice_rows = ns.n;
+    } else if (!ALPHA && p->c.radv_off != 0 && p->ex.rows_impl == FS_ROWS_BATCH && !p->c.permuted) {
+      // the batch kernel's stream (its own row-unit slices: st is at row `off` of the node)
+      host_rows_batch_slice<D>(p, ktab, st, budget, sink);
     } else {
       while (!fs::needs_refill<D, ALPHA>(st, budget)) {
         fs::fast_step<D, true, ALPHA>(st, c, ktab, budget, emit);
