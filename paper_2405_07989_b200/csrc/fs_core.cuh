@@ -77,6 +77,7 @@ struct Consts {
   uint32_t t2_off;       // word offset of the count's one-level ascend table (0: none; fs_host.cu)
   uint32_t cadv2_off;    // word offset of the count's paired closed-tail table (0: none; fs_host.cu)
   uint32_t t3_off;       // word offset of the count's two-level ascend table (0: none; fs_host.cu)
+  uint32_t hadv_off;     // word offset of the histogram's 8-copy closed-tail table (0: none; fs_host.cu)
   uint32_t radv_off;     // word offset of the materialise advance table (0: none; fs_host.cu):
                          //   4 words per rho {next | inc << 11, k0(next), ad0(next), 0}
   int32_t dl;            // t - s: change of a row's length from one valid a_{d-1} to the next

@@ -231,6 +231,30 @@ int fs_validate_and_build(fs_plan *p, uint64_t n, const uint32_t *gens, int d, i
             ent[2] = w.k0 == fs::kNone ? 0u : ad0 - w.k0;
           }
         }
+        // Histogram: the same transition with its fields in separate words, in 8 interleaved
+        // copies (entry (rho, j) at 16 (8 rho + j) bytes; lane l reads copy l mod 8, so a
+        // quarter-warp's 16 B loads hit 8 distinct bank groups):
+        // {rel(next copy-j entry), q + carry, s - k0(next) (INT32_MIN: none), ad0 - k0}.
+        if (want_hist) {
+          const uint32_t ho = ((uint32_t)p->ktab.size() + 3u) & ~3u;
+          if (c.gA <= 128u) {  // <= 16 KB: the table shares shared memory with the bins
+            std::vector<uint32_t> hv(32u * c.gA, 0u);
+            for (uint32_t rho = 0; rho < c.gA; ++rho) {
+              const fs::Adv w = ar.step(rho, c);
+              const uint32_t ad0 = w.k0 == fs::kNone ? 0u : (uint32_t)(((uint64_t)w.k0 * c.gA + w.next) / c.gB);
+              for (uint32_t j = 0; j < 8u; ++j) {
+                uint32_t *ent = &hv[4u * (8u * rho + j)];
+                ent[0] = 4u * ho + 16u * (8u * w.next + j);
+                ent[1] = w.inc;
+                ent[2] = w.k0 == fs::kNone ? 0x80000000u : (uint32_t)((int32_t)c.s - (int32_t)w.k0);
+                ent[3] = w.k0 == fs::kNone ? 0u : ad0 - w.k0;
+              }
+            }
+            c.hadv_off = ho;
+            p->ktab.resize(ho, 0u);
+            p->ktab.insert(p->ktab.end(), hv.begin(), hv.end());
+          }
+        }
         c.cadv_off = cadv_off;
         c.cadv_words = cw;
         c.cadv_packed = packed ? 1u : 0u;

@@ -727,6 +727,49 @@ __device__ __forceinline__ void hc_group(Lane<D> &st, const Consts &c, uint32_t 
   }
 }
 
+// The histogram group over the 8-copy table (Consts::hadv_off): fields in separate words
+// (no unpacking on the ALU pipe) and a bank-group-private copy per quarter-warp lane.
+template <int D, int G, int DLS>
+__device__ __forceinline__ void hc_group8(Lane<D> &st, const Consts &c, uint32_t tab, const HcConsts &k,
+                                          uint32_t &nrows) {
+  if constexpr (D >= 3) {
+    uint32_t h = tab + 16u * (8u * st.rho + (threadIdx.x & 7u));
+    uint32_t A = st.A;
+    const uint32_t kk = st.k;
+    // address of index l0 is base0 + dstr * (A + w3 - u): l0 = lsum0 - 1 - u + A + (ad0 - k0)
+    const uint32_t bofs = st.lsum - 1u + (DLS < 0 ? (uint32_t)(-c.dl) : 0u);
+    const uint32_t base0 = k.dbase + k.dstr * bofs;
+    uint32_t n = nrows;
+#pragma unroll
+    for (int u = 0; u < G; ++u) {
+      uint32_t w0, w1, w2, w3;
+      asm("ld.shared.v4.u32 {%0, %1, %2, %3}, [%4];" : "=r"(w0), "=r"(w1), "=r"(w2), "=r"(w3) : "r"(h));
+      h = w0;
+      A += w1;
+      const int32_t y = (int32_t)(A + w2);
+      const uint32_t rows = __umulhi((uint32_t)(y > 0 ? y : 0), c.mhi);
+      if ((uint32_t)u < kk && rows != 0u) {  // valid step with rows: both updates
+        n += rows;
+        const uint32_t a0 = base0 + k.dstr * (A + w3 - (uint32_t)u);  // l0 (t < s: l0 + s - t)
+        if (DLS > 0) {
+          asm volatile("red.shared.add.u32 [%0], %1;" ::"r"(a0), "r"(1u) : "memory");
+          asm volatile("red.shared.add.u32 [%0], %1;" ::"r"(a0 + rows * k.sstr), "r"(0xffffffffu) : "memory");
+        } else if (DLS < 0) {
+          asm volatile("red.shared.add.u32 [%0], %1;" ::"r"(a0 - rows * k.sstr), "r"(1u) : "memory");
+          asm volatile("red.shared.add.u32 [%0], %1;" ::"r"(a0), "r"(0xffffffffu) : "memory");
+        } else {
+          asm volatile("red.shared.add.u32 [%0], %1;" ::"r"(a0), "r"(rows) : "memory");
+          asm volatile("red.shared.add.u32 [%0], %1;" ::"r"(a0 + k.dstr), "r"(0u - rows) : "memory");
+        }
+      }
+    }
+    nrows = n;
+    st.rho = (h - tab) >> 7;
+    st.A = A;
+    st.k = kk > (uint32_t)G ? kk - (uint32_t)G : 0u;
+  }
+}
+
 template <int D, int G, bool PACKED>
 __device__ __forceinline__ void hc_group_dl(Lane<D> &st, const Consts &c, uint32_t tab, const HcConsts &k,
                                             uint32_t &nrows) {
@@ -788,6 +831,8 @@ __global__ void __launch_bounds__(kBlock, (CONS == kConsRowsAny || CONS == FS_CO
         ((i - c.t2_off) & 3u) == 0u)
       v += ktab_base;
     if (cfast && c.cadv2_off != 0u && i >= c.cadv2_off && i < c.cadv2_off + 32u * c.gA && ((i - c.cadv2_off) & 3u) == 0u)
+      v += ktab_base;
+    if (hfast && c.hadv_off != 0u && i >= c.hadv_off && i < c.hadv_off + 32u * c.gA && ((i - c.hadv_off) & 3u) == 0u)
       v += ktab_base;
     if (cfast && c.t3_off != 0u && D >= 5 && i >= c.t3_off && i < c.t3_off + 4u * c.g[D >= 5 ? D - 4 : 0] &&
         ((i - c.t3_off) & 3u) == 0u)
@@ -934,6 +979,14 @@ __global__ void __launch_bounds__(kBlock, (CONS == kConsRowsAny || CONS == FS_CO
       } else if (CONS == kConsAnyClosed) {
 #pragma unroll
         for (int u = 0; u < UNROLL; ++u) fast_step_closed<D>(st, c, kt, budget, e_any);
+      } else if (hfast && c.hadv_off != 0u) {
+        const uint32_t htab = ktab_base + 4u * c.hadv_off;
+        if (c.dl > 0)
+          hc_group8<D, UNROLL, 1>(st, c, htab, hck, e_hcl.n);
+        else if (c.dl < 0)
+          hc_group8<D, UNROLL, -1>(st, c, htab, hck, e_hcl.n);
+        else
+          hc_group8<D, UNROLL, 0>(st, c, htab, hck, e_hcl.n);
       } else if (hfast) {
         if (c.cadv_packed)
           hc_group_dl<D, UNROLL, true>(st, c, ktab_base + 4u * c.cadv_off, hck, e_hcl.n);
