@@ -17,7 +17,10 @@ constexpr int kBlock = 256;          // threads per persistent CTA
 #define FS_CC_GROUP 16  // steps per group of the closed-tail count (cc_group)
 #endif
 #ifndef FS_CC_MINB
-#define FS_CC_MINB 1  // __launch_bounds__ min blocks per SM of the closed-tail count kernel
+// __launch_bounds__ min blocks per SM of the closed-tail count kernel (d <= 9): 5 CTAs of 256
+// threads (<= 48 registers, no spills) hide more of the table walk's latency than 4 (C3:
+// 14.7 -> 13.8 ms); 6 spills.  Larger d keep the compiler's choice (no spills).
+#define FS_CC_MINB 5
 #endif
 // Materialise (M1) per-lane staging: two 64 B halves + room for one row spilling past them
 // (rows are <= 64 B); lane stride 196 B = 49 words (odd) so lanes at equal positions hit

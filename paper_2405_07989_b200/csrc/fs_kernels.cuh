@@ -783,7 +783,7 @@ __device__ __forceinline__ void hc_group_dl(Lane<D> &st, const Consts &c, uint32
 
 template <int D, int CONS, int B, bool KTAB>
 __global__ void __launch_bounds__(kBlock, (CONS == kConsRowsAny || CONS == FS_CONSUMER_ROWS ? 4
-                                           : CONS == kConsCountClosed              ? FS_CC_MINB
+                                           : CONS == kConsCountClosed              ? (D <= 9 ? FS_CC_MINB : 1)
                                                                                    : 1))
     fs_enum_kernel(const KParams P) {
   constexpr bool CAND = CONS == kConsCountSkipOff || CONS == kConsCountSkipPaper;
