@@ -473,6 +473,24 @@ def extras(args, world, rank, local, dev, stream, peaks, peaks_kind, barrier, ma
                                 "peak_source": "MEASURED_PEAKS.json hbm_gbs x %d (%s, copy r+w)" % (world, peaks_kind),
                                 "frac_of_write_microbench": (gbs_all / world / mb["hbm_write_gbs"]) if mb else None}}
         del out
+    # filtered materialise (NEXT-4): rows of one length class, two passes (count, write) through
+    # the synchronous C-ABI call -- timed with CUDA events around the whole call (plan creation
+    # on the host and both passes included)
+    try:
+        X = 1056  # a populated length class of C2-XL (lengths 688..1454)
+        m_cnt, _ = api.fs_enumerate_filtered(inst.n, inst.gens, L.FS_PRED_LEN_EQ, X, B=16, cap=0, device=local,
+                                             rank=rank, world=world)
+        fout = store_out[:max(1, m_cnt)]
+        def filt():
+            api.fs_enumerate_filtered(inst.n, inst.gens, L.FS_PRED_LEN_EQ, X, B=16, cap=m_cnt, out=fout,
+                                      device=local, rank=rank, world=world)
+        ms = _time_ms(filt, stream, 3, barrier, max_over_ranks)
+        ex["store_filtered"] = {"workload": "C2XL: rows of Z(16000, (11,13,17,19,23)) with a_1+..+a_5 = %d, u16, "
+                                            "any order (count pass + write pass)" % X,
+                                "matching_rows": m_cnt, "scanned_rows": info["total_rows"], "ms": ms,
+                                "value": info["total_rows"] / (ms / 1e3), "unit": "scanned factorizations/s"}
+    except Exception as e:  # an extra: report, do not fail the bench line
+        ex["store_filtered"] = {"error": repr(e)}
     del store_out
     torch.cuda.empty_cache()
 
