@@ -45,6 +45,7 @@ fs::KParams base_params(const fs_plan *p) {
   kp.queue = p->scratch_dev;
   kp.hist_len = (uint32_t)p->hist_len;
   kp.hist_smem = p->hist_len <= fs::kHistSmemMax ? 1u : 0u;
+  kp.starts = p->starts_dev;
   return kp;
 }
 

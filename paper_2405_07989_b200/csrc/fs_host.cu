@@ -427,7 +427,9 @@ void fs_plan_free_device(fs_plan *p) {
   if (p->ktab_dev) cudaFree(p->ktab_dev);
   if (p->scratch_dev) cudaFree(p->scratch_dev);
   if (p->diff_dev) cudaFree(p->diff_dev);
+  if (p->starts_dev) cudaFree(p->starts_dev);
   p->diff_dev = nullptr;
+  p->starts_dev = nullptr;
   p->U_dev = nullptr;
   p->ktab_dev = nullptr;
   p->scratch_dev = nullptr;
@@ -464,7 +466,7 @@ int fs_plan_upload_impl(fs_plan *p) {
   }
   if (cudaMalloc(&p->scratch_dev, fs::kScratchBytes) != cudaSuccess) return FS_ENOMEM;
   p->uploaded = true;
-  return FS_OK;
+  return fs_build_slice_starts(p);
 }
 
 // ------------------------------------------------------------------ host model (tests only)

@@ -74,11 +74,15 @@ struct KParams {
   unsigned long long *diff_out;
   uint32_t diff_len;
   uint32_t hist_rep;  // closed-tail histogram: 32 = one difference-array copy per lane (bank-private), else 1
+  // node-unit plans: the prefix a_1..a_L of every slice's first node (num_slices x L words,
+  // built once per plan by fs_build_slice_starts), so a refill is L independent loads instead
+  // of the unrank's O(L log n) dependent ones; nullptr = unrank
   // filtered materialise (M2 staged kernel): only rows satisfying
   // filt_pred(filt_arg) are compacted; count_only = pass 1 (count them into *front)
   int filt_pred;
   uint64_t filt_arg;
   int count_only;
+  const uint32_t *starts;
 };
 
 }  // namespace fs
@@ -107,6 +111,7 @@ struct fs_plan {
   uint32_t *ktab_dev = nullptr;
   unsigned long long *scratch_dev = nullptr;  // [0] queue head, [1..] spare
   unsigned long long *diff_dev = nullptr;     // closed-tail histogram difference array
+  uint32_t *starts_dev = nullptr;             // slice-start table (node-unit plans), or nullptr
   bool uploaded = false;
   uint32_t grid = 0, block = fs::kBlock;
   int last_launches = 0;
@@ -123,6 +128,8 @@ fs::Div fs_make_div(uint32_t g);
 int fs_launch(fs_plan *p, int consumer, int B, const fs::KParams &kp_template, cudaStream_t stream);
 int fs_occupancy_grid(fs_plan *p, int consumer, int B, uint32_t *grid_out);
 int fs_launch_hist_finalize(const fs::KParams &kp, cudaStream_t stream);
+// builds p->starts_dev on p->stream (node-unit plans with L >= 1; skipped when too large)
+int fs_build_slice_starts(fs_plan *p);
 extern unsigned long long g_fs_total_launches;
 // lockstep batch materialise kernel (fs_k_rowsb.cu)
 bool fs_rows_batch_supported(const fs_plan *p, int B);

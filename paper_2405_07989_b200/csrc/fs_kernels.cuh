@@ -37,6 +37,44 @@ struct KTabSmem {
 
 constexpr unsigned kFull = 0xffffffffu;
 
+// Node-unit slice entry from the precomputed slice-start table: the first node's prefix
+// a_1..a_L (independent loads), the residuals re-derived -- the state unrank() would produce
+// (node-unit slices start at a node's entry unit, so the offset is 0).
+template <int D, bool NEED_AD, class KT>
+__device__ __forceinline__ uint64_t start_from_table(Lane<D> &st, const Consts &c, const KT &kt, const uint32_t *p) {
+  constexpr int L = D - 2;
+  uint32_t R = c.n, lsum = 0;
+#pragma unroll
+  for (int k = 0; k < L; ++k) {
+    const uint32_t a = __ldg(p + k);
+    st.a[k] = a;
+    R -= a * c.g[k];
+    st.R[k] = R;
+    lsum += a;
+  }
+  const uint32_t A = divq(R, c.dvA);
+  st.A = A;
+  st.rho = R - A * c.gA;
+  st.lsum = lsum;
+  st.k = st.kb = 0;
+  entry<D, NEED_AD>(st, c, kt);
+  return 0;
+}
+
+// One thread per slice: unrank the slice's first unit and store the node prefix (plan setup).
+template <int D>
+__global__ void fs_slice_starts_kernel(const KParams P, uint32_t *out) {
+  constexpr int L = D - 2;
+  for (uint64_t sl = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; sl < P.num_slices;
+       sl += (uint64_t)gridDim.x * blockDim.x) {
+    Lane<D> st;
+    KTabArith kt;
+    unrank<D, false>(st, P.c, kt, P.unit0 + sl * P.T);
+#pragma unroll
+    for (int k = 0; k < L; ++k) out[sl * L + k] = st.a[k];
+  }
+}
+
 template <int CONS>
 struct Inner {
   static constexpr int value = 64;
@@ -941,7 +979,8 @@ __global__ void __launch_bounds__(kBlock, (CONS == kConsRowsAny || CONS == FS_CO
             const uint64_t u = P.unit0 + sl * P.T;
             const uint64_t e = u + P.T < P.unit1 ? u + P.T : P.unit1;
             budget = (uint32_t)(e - u);
-            const uint64_t off = unrank<D, NEED_AD>(st, c, kt, u);
+            const uint64_t off = P.starts ? start_from_table<D, NEED_AD>(st, c, kt, P.starts + sl * (uint64_t)(D - 2))
+                                          : unrank<D, NEED_AD>(st, c, kt, u);
             budget -= position_in_node<D, NEED_AD>(st, c, off);
             if (CAND) enter_candidates<D>(st, c);
             sync_k<D, ALPHA>(st, budget);
