@@ -62,7 +62,10 @@ static uint64_t ceil_div_u64(uint64_t a, uint64_t b) { return a / b + (a % b ? 1
 // target number of resident lanes used to size slices when the caller does not (a B200
 // holds 148 SMs x 2048 threads; the persistent grid uses about half that at ~64 regs)
 static const uint64_t kTargetLanes = 148ull * 1024ull;
-static const uint64_t kSlicesPerLane = 16;
+#ifndef FS_SLICES_PER_LANE
+#define FS_SLICES_PER_LANE 16
+#endif
+static const uint64_t kSlicesPerLane = FS_SLICES_PER_LANE;
 
 int fs_validate_and_build(fs_plan *p, uint64_t n, const uint32_t *gens, int d, int consumer,
                           const fs_exec_t *ex) {
