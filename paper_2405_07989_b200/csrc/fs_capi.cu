@@ -168,7 +168,8 @@ int fs_plan_hist_async(fs_plan *p, uint64_t *hist_dev, uint64_t hist_cap) {
     kp.hist_smem = kp.diff_len <= fs::kHistSmemMax ? 1u : 0u;
     // group-form kernels spread the shared updates over 32 lane-private copies (one bank
     // each: no bank conflicts) when they fit
-    kp.hist_rep = (kp.hist_smem && p->c.cadv_off && (size_t)(kp.diff_len + 1) * 32 * 4 <= fs::kHistRepBytes) ? 32u : 1u;
+    kp.hist_rep = (kp.hist_smem && p->c.cadv_off && (size_t)(kp.diff_len + 1) * FS_HIST_REP * 4 <= fs::kHistRepBytes)
+                      ? (uint32_t)FS_HIST_REP : 1u;
     if (!p->diff_dev && cudaMalloc(&p->diff_dev, (size_t)kp.diff_len * 8) != cudaSuccess) return FS_ENOMEM;
     if (cudaMemsetAsync(p->diff_dev, 0, (size_t)kp.diff_len * 8, p->stream) != cudaSuccess) return FS_ECUDA;
     kp.diff_out = p->diff_dev;

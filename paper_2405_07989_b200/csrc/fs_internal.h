@@ -31,6 +31,12 @@ constexpr uint32_t kLaneStride = kStageBytes + 4;
 constexpr uint32_t kKtabMax = 2048;  // node tables in shared memory if g_{d-1} <= this (<= 24 KB)
 constexpr uint32_t kHistSmemMax = 24576;  // u32 histogram bins kept in shared memory
 constexpr uint32_t kHistRepBytes = 49152; // lane-private difference-array copies if they fit in this
+#ifndef FS_HIST_REP
+#define FS_HIST_REP 32  // difference-array copies per CTA (lane l uses copy l mod FS_HIST_REP)
+#endif
+#ifndef FS_HC_MINB
+#define FS_HC_MINB 1  // __launch_bounds__ min blocks per SM of the closed-tail histogram kernel (d <= 9)
+#endif
 constexpr int kConsRowsAny = 4;           // internal consumer: materialise, order = any (M2)
 #ifndef FS_WARPBUF
 #define FS_WARPBUF 6144

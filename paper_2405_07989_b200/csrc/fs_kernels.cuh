@@ -705,7 +705,7 @@ struct HcConsts {
 };
 __device__ __forceinline__ HcConsts hc_consts(const Consts &c, uint32_t diff, uint32_t rep) {
   HcConsts k;
-  k.dbase = diff + (rep > 1u ? 4u * (threadIdx.x & 31u) : 0u);
+  k.dbase = diff + (rep > 1u ? 4u * (threadIdx.x & (rep - 1u)) : 0u);
   k.dstr = 4u * rep;
   k.sstr = k.dstr * (uint32_t)(c.dl < 0 ? -c.dl : c.dl);
   return k;
@@ -822,6 +822,7 @@ __device__ __forceinline__ void hc_group_dl(Lane<D> &st, const Consts &c, uint32
 template <int D, int CONS, int B, bool KTAB>
 __global__ void __launch_bounds__(kBlock, (CONS == kConsRowsAny || CONS == FS_CONSUMER_ROWS ? 4
                                            : CONS == kConsCountClosed              ? (D <= 9 ? FS_CC_MINB : 1)
+                                           : CONS == kConsHistClosed               ? (D <= 9 ? FS_HC_MINB : 1)
                                                                                    : 1))
     fs_enum_kernel(const KParams P) {
   constexpr bool CAND = CONS == kConsCountSkipOff || CONS == kConsCountSkipPaper;
@@ -911,7 +912,7 @@ __global__ void __launch_bounds__(kBlock, (CONS == kConsRowsAny || CONS == FS_CO
   EmitCount<D> e_count{0};
   EmitHist<D> e_hist{hist_s, P.hist_out, P.hist_smem, 0};
   const uint32_t hrep = CONS == kConsHistClosed && P.hist_rep > 1u ? P.hist_rep : 1u;
-  EmitHistClosed<D> e_hcl{hist_s + (hrep > 1u ? (threadIdx.x & 31u) : 0u), P.diff_out, P.hist_smem, hrep, 0};
+  EmitHistClosed<D> e_hcl{hist_s + (hrep > 1u ? (threadIdx.x & (hrep - 1u)) : 0u), P.diff_out, P.hist_smem, hrep, 0};
   const HcConsts hck = hc_consts(c, (uint32_t)__cvta_generic_to_shared(hist_s), hrep);
   EmitAny<D> e_any{P.pred, P.pred_arg, P.found, P.witness, false};
   EmitRows<D, B> e_rows;
