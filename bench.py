@@ -473,6 +473,25 @@ def extras(args, world, rank, local, dev, stream, peaks, peaks_kind, barrier, ma
                                 "peak_source": "MEASURED_PEAKS.json hbm_gbs x %d (%s, copy r+w)" % (world, peaks_kind),
                                 "frac_of_write_microbench": (gbs_all / world / mb["hbm_write_gbs"]) if mb else None}}
         del out
+    # common-divisor skip (NEXT-3): a non-coprime last pair; the batch kernel jumps over the
+    # level-L nodes without factorizations, the staged kernel steps through them
+    try:
+        icd = W.C2CD
+        for key, impl in (("store_cd", L.FS_ROWS_BATCH), ("store_cd_staged", L.FS_ROWS_STAGED)):
+            p = api.Plan(icd.n, icd.gens, L.FS_CONSUMER_ROWS, rows_impl=impl, **kw)
+            inf = p.info
+            rows = inf["row_end"] - inf["row_begin"]
+            out = store_out.view(-1)[: rows * icd.d].view(rows, icd.d)
+            p.enumerate_async(16, out, rows)
+            ms = _time_ms(lambda: p.enumerate_async(16, out, rows), stream, 3, barrier, max_over_ranks)
+            gbs = inf["total_rows"] * icd.d * 2 / (ms / 1e3) / 1e9
+            ex[key] = {"workload": "C2CD: Z(12000, (11,13,17,18,24)) materialise u16 rows, canonical order, %s kernel"
+                                   % ("batch (dead-node skip)" if impl == L.FS_ROWS_BATCH else "staged"),
+                       "rows": inf["total_rows"], "ms": ms, "value": inf["total_rows"] / (ms / 1e3), "unit": UNIT,
+                       "roofline": {"bound": "hbm", "achieved": gbs, "peak": peaks["hbm_gbs"] * world, "unit": "GB/s",
+                                    "frac": gbs / (peaks["hbm_gbs"] * world)}}
+    except Exception as e:
+        ex["store_cd"] = {"error": repr(e)}
     # filtered materialise (NEXT-4): rows of one length class, two passes (count, write) through
     # the synchronous C-ABI call -- timed with CUDA events around the whole call (plan creation
     # on the host and both passes included)

@@ -178,21 +178,45 @@ int fs_validate_and_build(fs_plan *p, uint64_t n, const uint32_t *gens, int d, i
         p->ktab[adv_off + 2 * rho + 1] = w.k0;
       }
       c.adv_off = adv_off;
-      // Materialise (batch kernel): the advance transition extended by ad0(next) =
-      // (k0(next) g_{d-1} + next) / g_d, a_d of the next node's first row (a function of the
+      // Materialise (batch kernel): the advance transition to the next LIVE node, extended by
+      // ad0 = (k0 g_{d-1} + rho') / g_d, a_d of that node's first row (a function of the
       // residue alone: R_L - (A - k0) g_{d-1} = k0 g_{d-1} + rho), so a node entry needs no
-      // division.  One 16 B shared load per advance.
+      // division.  Nodes whose residual gcd(g_{d-1}, g_d) does not divide have no rows (the
+      // paper's common-divisor skip for the last two generators):
+      // the entry jumps over them -- `steps` advances at once, summed quotient increments;
+      // steps = 0xFFFFFFFF when no residue of the cycle is live.  One 16 B load per advance.
       if (consumer == FS_CONSUMER_ROWS && c.gA <= 1024u) {
         const uint32_t radv_off = ((uint32_t)p->ktab.size() + 3u) & ~3u;
-        p->ktab.resize(radv_off + 4u * c.gA, 0u);
-        for (uint32_t rho = 0; rho < c.gA; ++rho) {
-          const fs::Adv w = ar.step(rho, c);
-          uint32_t *ent = &p->ktab[radv_off + 4u * rho];
-          ent[0] = fs::adv_pack(w.next, w.inc);
-          ent[1] = w.k0;
-          ent[2] = w.k0 == fs::kNone ? 0u : (uint32_t)(((uint64_t)w.k0 * c.gA + w.next) / c.gB);
+        std::vector<uint32_t> rv(4u * c.gA, 0u);
+        bool fits = true;
+        for (uint32_t rho = 0; rho < c.gA && fits; ++rho) {
+          uint32_t r = rho, steps = 0, k0n = fs::kNone;
+          uint64_t inc = 0;
+          do {
+            const fs::Adv w = ar.step(r, c);
+            inc += w.inc;
+            ++steps;
+            r = w.next;
+            k0n = w.k0;
+          } while (k0n == fs::kNone && steps <= c.gA);
+          uint32_t *ent = &rv[4u * rho];
+          if (k0n == fs::kNone) {  // the whole residue cycle is dead
+            ent[0] = 0u;
+            ent[1] = fs::kNone;
+            ent[3] = 0xFFFFFFFFu;
+          } else {
+            if (inc >= (1ull << (32 - fs::kAdvBits))) fits = false;
+            ent[0] = fs::adv_pack(r, (uint32_t)inc);
+            ent[1] = k0n;
+            ent[2] = (uint32_t)(((uint64_t)k0n * c.gA + r) / c.gB);
+            ent[3] = steps;
+          }
         }
-        c.radv_off = radv_off;
+        if (fits) {
+          p->ktab.resize(radv_off, 0u);
+          p->ktab.insert(p->ktab.end(), rv.begin(), rv.end());
+          c.radv_off = radv_off;
+        }
       }
       // Closed-tail group tables (count or histogram + tail=closed): per residue rho the entry
       // {rel | (q + carry) << kCAdvShift, s - k0(next)} (count, 8 B), followed for the
@@ -753,14 +777,16 @@ void host_rows_batch_slice(const fs_plan *p, const KT &ktab, fs::Lane<D> &st, ui
   for (uint32_t r = 0; r < rows; ++r) {
     if constexpr (L >= 1) {
       while (st.cur < 0) {
-        if (st.a[L - 1] > 0) {
-          const uint32_t *w = W + c.radv_off + 4u * st.rho;
-          st.a[L - 1] -= 1u;
+        const uint32_t *w = W + c.radv_off + 4u * st.rho;
+        if (st.a[L - 1] >= w[3]) {  // to the next live node, w[3] advances at once
+          st.a[L - 1] -= w[3];
           st.rho = w[0] & ((1u << fs::kAdvBits) - 1u);
           st.A += w[0] >> fs::kAdvBits;
           st.cur = (int32_t)st.A - (int32_t)w[1];
           ad = w[2];
-        } else {
+        } else {  // the rest of the run is dead (or empty): ascend
+          st.lsum -= st.a[L - 1];
+          st.a[L - 1] = 0u;
           if (!fs::ascend<D>(st, c)) return;  // end of stream (not inside a full slice)
           st.cur = (int32_t)st.A - (int32_t)ktab(st.rho, c);
           ad = fs::divq((st.A - (uint32_t)st.cur) * c.gA + st.rho, c.dvB);

@@ -81,19 +81,30 @@ struct RAdvSmem {
   __device__ __forceinline__ static uint32_t inc(const Ent &e) { return e.x >> kAdvBits; }
   __device__ __forceinline__ static uint32_t k0(const Ent &e) { return e.y; }
   __device__ __forceinline__ static uint32_t ad0(const Ent &e) { return e.z; }
+  __device__ __forceinline__ static uint32_t steps(const Ent &e) { return e.w; }
 };
 struct RAdvArith {
   struct Ent {
-    uint32_t nx, in, k, a;
+    uint32_t nx, in, k, a, st;
   };
+  // the same transition by arithmetic: advance until a live residue (at most g_{d-1} steps)
   __device__ __forceinline__ Ent load(uint32_t rho, const Consts &c) const {
-    const Adv w = KTabArith{}.step(rho, c);
-    return Ent{w.next, w.inc, w.k0, divq(w.k0 * c.gA + w.next, c.dvB)};  // a: garbage when k0 = none
+    uint32_t r = rho, inc = 0, steps = 0;
+    Adv w;
+    do {
+      w = KTabArith{}.step(r, c);
+      inc += w.inc;
+      ++steps;
+      r = w.next;
+    } while (w.k0 == kNone && steps <= c.gA);
+    if (w.k0 == kNone) steps = 0xFFFFFFFFu;
+    return Ent{r, inc, w.k0, divq(w.k0 * c.gA + r, c.dvB), steps};  // a: garbage when k0 = none
   }
   __device__ __forceinline__ static uint32_t next(const Ent &e) { return e.nx; }
   __device__ __forceinline__ static uint32_t inc(const Ent &e) { return e.in; }
   __device__ __forceinline__ static uint32_t k0(const Ent &e) { return e.k; }
   __device__ __forceinline__ static uint32_t ad0(const Ent &e) { return e.a; }
+  __device__ __forceinline__ static uint32_t steps(const Ent &e) { return e.st; }
 };
 
 // Register copy of the constants the row step and ascend() read.  They are staged through
@@ -155,13 +166,15 @@ __device__ __forceinline__ void rb_slow(Lane<D> &st, uint32_t &ad, typename RA::
   if constexpr (L >= 1) {
     if (st.cur >= 0) return;
     while (st.cur < 0) {
-      if (st.a[L - 1] > 0) {
-        st.a[L - 1] -= 1u;
+      if (st.a[L - 1] >= RA::steps(wn)) {  // to the next live node (NEXT-3 skip of dead ones)
+        st.a[L - 1] -= RA::steps(wn);
         st.rho = RA::next(wn);
         st.A += RA::inc(wn);
         st.cur = (int32_t)st.A - (int32_t)RA::k0(wn);
         ad = RA::ad0(wn);
-      } else {
+      } else {  // the rest of the run is dead (or empty): ascend
+        st.lsum -= st.a[L - 1];
+        st.a[L - 1] = 0u;
         if (!ascend<D>(st, rc)) {  // end of stream: impossible inside a full slice
           st.cur = 0x3fffffff;
           break;
@@ -183,8 +196,8 @@ __device__ __forceinline__ void rb_ensure_row(Lane<D> &st, uint32_t &ad, typenam
                                               const CC &rc, const KT &kt, const RA &ra) {
   constexpr int L = D - 2;
   if constexpr (L >= 1) {
-    if (st.cur < 0 && st.a[L - 1] != 0u) {
-      st.a[L - 1] -= 1u;
+    if (st.cur < 0 && st.a[L - 1] >= RA::steps(wn)) {
+      st.a[L - 1] -= RA::steps(wn);
       st.rho = RA::next(wn);
       st.A += RA::inc(wn);
       st.cur = (int32_t)st.A - (int32_t)RA::k0(wn);

@@ -44,6 +44,9 @@ C3 = Instance("C3", 4275, c3_generators())
 C4 = Instance("C4", 4275, c3_generators())
 C5 = Instance("C5", 20000, (1, 1, 2, 997, 1000))
 C5Q = Instance("C5Q", 10000, (1, 1, 2, 997, 1000))  # quick variant
+# C2's shape with a non-coprime last pair (gcd(18, 24) = 6: 5 of 6 level-L nodes have no
+# factorization) -- exercises the common-divisor skip of the materialise kernel (NEXT-3)
+C2CD = Instance("C2CD", 12000, (11, 13, 17, 18, 24))
 
 CONFIGS = {i.name: i for i in (C1, C2, C2L, C2XL, C3, C4, C5, C5Q)}
 
