@@ -530,6 +530,10 @@ def extras(args, world, rank, local, dev, stream, peaks, peaks_kind, barrier, ma
         ("count_auto_order_closed", W.C3, L.FS_CONSUMER_COUNT, {"gen_order": AUTO, "tail": 1},
          "C3 count, NEXT-1 + NEXT-2", 3),
         ("c5_count", W.C5, L.FS_CONSUMER_COUNT, {}, "C5 count, given order", 1),
+        ("c2cd_count_closed", W.C2CD, L.FS_CONSUMER_COUNT, {"tail": 1},
+         "C2CD count, given order (gcd(18, 24) = 6: the closed tail walks live nodes only, NEXT-3)", 3),
+        ("c2cd_count_rows", W.C2CD, L.FS_CONSUMER_COUNT, {},
+         "C2CD count, given order, one step per row (no skip)", 3),
         # E2 (Table 1 modulo on/off) re-run on B200: the index-(d-1) loop variants
         ("c2l_skip_off", W.C2L, L.FS_CONSUMER_COUNT, {"tail": 2}, "C2-L count, Skip=off (every candidate)", 2),
         ("c2l_skip_paper", W.C2L, L.FS_CONSUMER_COUNT, {"tail": 3}, "C2-L count, Skip=paper (P:170-176)", 2),

@@ -76,6 +76,7 @@ struct Consts {
   uint32_t mhi;          // ceil(2^32 / s) for the group table's umulhi division
   uint32_t t2_off;       // word offset of the count's one-level ascend table (0: none; fs_host.cu)
   uint32_t cadv2_off;    // word offset of the count's paired closed-tail table (0: none; fs_host.cu)
+  uint32_t cadv2_skip;   // 1: that table walks live nodes only (8 words per entry; NEXT-3)
   uint32_t t3_off;       // word offset of the count's two-level ascend table (0: none; fs_host.cu)
   uint32_t hadv_off;     // word offset of the histogram's 8-copy closed-tail table (0: none; fs_host.cu)
   uint32_t radv_off;     // word offset of the materialise advance table (0: none; fs_host.cu):

@@ -366,6 +366,48 @@ int fs_validate_and_build(fs_plan *p, uint64_t n, const uint32_t *gens, int d, i
           }
           c.cadv2_off = c2o;
         }
+        // gcd(g_{d-1}, g_d) = h > 1: a level-L node whose residual h does not divide has no
+        // factorization (the paper's common-divisor skip for the last two generators, P:174,
+        // SURVEY 8(f) NEXT-3).  The paired table then walks LIVE nodes only: 8 words per entry
+        // {link, inc1 + s - k0_1, inc1 + inc2 + s - k0_2, inc1 + inc2, st1, st1 + st2, 0, 0},
+        // where each of the two steps jumps st advances to the next live node (inc = summed
+        // quotient increments); the advances still count as node units, so the group masks by
+        // the cumulative advance count instead of the node index.  8 copies as above.
+        if (c.cadv2_off != 0 && c.h > 1u && c.gA <= 64u &&
+            4ull * ((((uint32_t)p->ktab.size() + 7u) & ~7u) + 64u * c.gA) + 16384ull <= (1ull << fs::kCAdvShift)) {
+          struct Live {
+            uint32_t next, steps, inc, k0;
+          };
+          auto live_after = [&](uint32_t rho) {
+            uint32_t r = rho, steps = 0, inc = 0, k0 = fs::kNone;
+            do {
+              const fs::Adv w = ar.step(r, c);
+              inc += w.inc;
+              ++steps;
+              r = w.next;
+              k0 = w.k0;
+            } while (k0 == fs::kNone && steps <= c.gA);
+            if (k0 == fs::kNone) steps = 0x3FFFFFFFu;  // no live residue in the cycle
+            return Live{r, steps, inc, k0};
+          };
+          const uint32_t cso = ((uint32_t)p->ktab.size() + 7u) & ~7u;
+          p->ktab.resize(cso + 64u * c.gA, 0u);
+          for (uint32_t rho = 0; rho < c.gA; ++rho) {
+            const Live l1 = live_after(rho), l2 = live_after(l1.next);
+            for (uint32_t j = 0; j < 8u; ++j) {
+              uint32_t *ent = &p->ktab[cso + 8u * (8u * rho + j)];
+              ent[0] = 4u * cso + 32u * (8u * l2.next + j);
+              ent[1] = l1.k0 == fs::kNone ? 0x80000000u : (uint32_t)((int32_t)(l1.inc + c.s) - (int32_t)l1.k0);
+              ent[2] = l2.k0 == fs::kNone ? 0x80000000u
+                                          : (uint32_t)((int32_t)(l1.inc + l2.inc + c.s) - (int32_t)l2.k0);
+              ent[3] = l1.inc + l2.inc;
+              ent[4] = l1.steps;
+              ent[5] = std::min<uint32_t>(l1.steps + l2.steps, 0x3FFFFFFFu);
+            }
+          }
+          c.cadv2_off = cso;
+          c.cadv2_skip = 1u;
+        }
       }
       c.ktab_len = (uint32_t)p->ktab.size();
       c.ktab = p->ktab.data();
@@ -691,9 +733,12 @@ uint64_t host_count_tables_slice(const fs_plan *p, const KT &ktab, fs::Lane<D> &
   t3_sync();
   while (!fs::needs_refill<D, 1>(st, budget)) {
     if constexpr (D >= 3) {  // cc_group2: G nodes, two per paired-table entry
-      uint32_t h = c.cadv2_off + 4u * (8u * st.rho + j);
+      const bool skip = c.cadv2_skip != 0;
+      const uint32_t ew = skip ? 8u : 4u;  // words per entry
+      uint32_t h = c.cadv2_off + ew * (8u * st.rho + j);
       uint32_t A = st.A;
       const uint32_t kk = st.k;
+      uint32_t cum = 0;  // advances taken (skip form), else 2 per pair
       for (uint32_t v = 0; v < G / 2; ++v) {
         const uint32_t *w = W + h;
         h = w[0] / 4u;
@@ -701,12 +746,14 @@ uint64_t host_count_tables_slice(const fs_plan *p, const KT &ktab, fs::Lane<D> &
         x1 = x1 > 0 ? x1 : 0;
         x2 = x2 > 0 ? x2 : 0;
         A += w[3];
-        if (2u * v < kk) n += (uint32_t)(((uint64_t)(uint32_t)x1 * c.mhi) >> 32);
-        if (2u * v + 1u < kk) n += (uint32_t)(((uint64_t)(uint32_t)x2 * c.mhi) >> 32);
+        const uint32_t c1 = skip ? cum + w[4] : 2u * v + 1u, c2 = skip ? cum + w[5] : 2u * v + 2u;
+        if (c1 <= kk) n += (uint32_t)(((uint64_t)(uint32_t)x1 * c.mhi) >> 32);
+        if (c2 <= kk) n += (uint32_t)(((uint64_t)(uint32_t)x2 * c.mhi) >> 32);
+        cum = c2;
       }
-      st.rho = (h - c.cadv2_off) / 32u;
+      st.rho = (h - c.cadv2_off) / (8u * ew);
       st.A = A;
-      st.k = kk > G ? kk - G : 0u;
+      st.k = kk > cum ? kk - cum : 0u;
     }
     fs::sync_k<D, 1>(st, budget);
     if (fs::needs_slow<D>(st, budget)) {

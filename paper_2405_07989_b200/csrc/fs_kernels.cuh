@@ -657,6 +657,40 @@ __device__ __forceinline__ void cc_group(Lane<D> &st, const Consts &c, uint32_t 
 // add, one add-max, one predicated umulhi-accumulate.  (The predicated mad.hi's register moves
 // run on the FMA pipe; a select-masked form with fewer instructions loads the ALU pipe, which
 // is the busier one, and measured 5 % slower.)
+// The paired group over the live-node table (Consts::cadv2_skip, gcd(g_{d-1}, g_d) > 1): each
+// step jumps to the next live node; the validity mask compares the cumulative advance count
+// (node units) with kk.
+template <int D, int G>
+__device__ __forceinline__ void cc_group2_skip(Lane<D> &st, const Consts &c, uint32_t tab2, uint32_t &cnt) {
+  if constexpr (D >= 3) {
+    uint32_t h = tab2 + 32u * (8u * st.rho + (threadIdx.x & 7u));
+    uint32_t A = st.A;
+    const uint32_t kk = st.k;
+    uint32_t n = cnt, cum = 0;
+#pragma unroll
+    for (int v = 0; v < G / 2; ++v) {
+      uint32_t w0, w1, w2, w3, w4, w5, w6, w7;
+      asm("ld.shared.v4.u32 {%0, %1, %2, %3}, [%4];" : "=r"(w0), "=r"(w1), "=r"(w2), "=r"(w3) : "r"(h));
+      asm("ld.shared.v4.u32 {%0, %1, %2, %3}, [%4];" : "=r"(w4), "=r"(w5), "=r"(w6), "=r"(w7) : "r"(h + 16u));
+      (void)w6;
+      (void)w7;
+      h = w0;
+      int32_t x1 = (int32_t)(A + w1), x2 = (int32_t)(A + w2);
+      x1 = x1 > 0 ? x1 : 0;
+      x2 = x2 > 0 ? x2 : 0;
+      A += w3;
+      const uint32_t c1 = cum + w4, c2 = cum + w5;
+      if (c1 <= kk) n += __umulhi((uint32_t)x1, c.mhi);
+      if (c2 <= kk) n += __umulhi((uint32_t)x2, c.mhi);
+      cum = c2;
+    }
+    cnt = n;
+    st.rho = (h - tab2) >> 8;
+    st.A = A;
+    st.k = kk > cum ? kk - cum : 0u;
+  }
+}
+
 template <int D, int G>
 __device__ __forceinline__ void cc_group2(Lane<D> &st, const Consts &c, uint32_t tab2, uint32_t &cnt) {
   static_assert(G % 2 == 0, "nodes per group must be even");
@@ -869,7 +903,9 @@ __global__ void __launch_bounds__(kBlock, (CONS == kConsRowsAny || CONS == FS_CO
     if (cfast && c.t2_off != 0u && D >= 4 && i >= c.t2_off && i < c.t2_off + 4u * c.g[D >= 4 ? D - 3 : 0] &&
         ((i - c.t2_off) & 3u) == 0u)
       v += ktab_base;
-    if (cfast && c.cadv2_off != 0u && i >= c.cadv2_off && i < c.cadv2_off + 32u * c.gA && ((i - c.cadv2_off) & 3u) == 0u)
+    if (cfast && c.cadv2_off != 0u &&
+        (c.cadv2_skip ? (i >= c.cadv2_off && i < c.cadv2_off + 64u * c.gA && ((i - c.cadv2_off) & 7u) == 0u)
+                      : (i >= c.cadv2_off && i < c.cadv2_off + 32u * c.gA && ((i - c.cadv2_off) & 3u) == 0u)))
       v += ktab_base;
     if (hfast && c.hadv_off != 0u && i >= c.hadv_off && i < c.hadv_off + 32u * c.gA && ((i - c.hadv_off) & 3u) == 0u)
       v += ktab_base;
@@ -1012,7 +1048,11 @@ __global__ void __launch_bounds__(kBlock, (CONS == kConsRowsAny || CONS == FS_CO
       const bool had = budget != 0;
       // UNROLL branch-free fast steps, then one (warp-uniform) check for lanes parked on an
       // ascend; the rare slow lanes run the generic successor step together.
-      if (cfast && c.cadv2_off != 0u && (UNROLL % 2) == 0) {
+      if (CONS == kConsCountClosed && B == 32 && cfast && c.cadv2_off != 0u && (UNROLL % 2) == 0) {
+        // (the count ignores B: its B = 32 instantiation is the live-node walk, Consts::cadv2_skip,
+        // so the common kernel carries none of that code)
+        cc_group2_skip<D, (UNROLL % 2) == 0 ? UNROLL : 2>(st, c, ktab_base + 4u * c.cadv2_off, e_count.n);
+      } else if (cfast && c.cadv2_off != 0u && (UNROLL % 2) == 0) {
         cc_group2<D, (UNROLL % 2) == 0 ? UNROLL : 2>(st, c, ktab_base + 4u * c.cadv2_off, e_count.n);
       } else if (cfast) {
         cc_group<D, UNROLL>(st, c, ktab_base + 4u * c.cadv_off, e_count.n);
