@@ -230,7 +230,12 @@ int fs_plan_enumerate_async(fs_plan *p, int B, void *out_dev, uint64_t cap) {
   if (incr) {  // the first `take` rows in increasing order = the last `take` canonical rows
     kp.unit0 = p->unit_end - take;
     kp.unit1 = p->unit_end;
+    kp.starts = nullptr;  // the table holds the canonical slicing from unit_begin
   }
+  // canonical order (M1): no table -- its 80 MB stream through L2 (512-row slices) disturbs
+  // the L2 merging of M1's scattered 320 B segments (C2-XL 4.78 -> 4.97 ms with it), while
+  // M2 (whole-warp blocks) gains (4.06 -> 3.93 ms)
+  if (p->ex.order == FS_ORDER_CANONICAL) kp.starts = nullptr;
   kp.num_slices = (take + p->T - 1) / p->T;
   kp.num_claims = kp.num_slices;
   kp.rows_out = reinterpret_cast<unsigned char *>(out_dev);

@@ -23,13 +23,14 @@ int fs_dispatch_count(fs_plan *p, int B, const fs::KParams &kp, cudaStream_t s, 
   (void)B; return fs::dispatch_kt<FS_CONSUMER_COUNT, 16>(p, kp, s, q, g);
 }
 
-// Slice-start table of a node-unit plan (count / histogram / any): launched once per plan at
-// upload; refills then read L words instead of unranking (16 dependent-load binary searches
+// Slice-start table of a plan (node units: the first node's prefix; row units: also the row
+// offset in it): launched once per plan at upload; refills then read L (+1) words instead of
+// unranking (16 dependent-load binary searches
 // per slice otherwise cost ~0.9 ms of latency per launch on C3, which dominates small shards).
 int fs_build_slice_starts(fs_plan *p) {
   const int L = p->d - 2;
-  if (L < 1 || p->c.alpha != 1u || p->num_slices == 0) return FS_OK;
-  const uint64_t words = p->num_slices * (uint64_t)L;
+  if (L < 1 || p->num_slices == 0) return FS_OK;
+  const uint64_t words = p->num_slices * (uint64_t)(L + (p->c.alpha ? 0 : 1));  // row units: + offset
   if (words * 4u > (256ull << 20)) return FS_OK;  // the unrank path instead
   if (cudaMalloc(&p->starts_dev, words * 4u) != cudaSuccess) {
     cudaGetLastError();

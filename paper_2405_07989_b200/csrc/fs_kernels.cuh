@@ -37,9 +37,14 @@ struct KTabSmem {
 
 constexpr unsigned kFull = 0xffffffffu;
 
-// Node-unit slice entry from the precomputed slice-start table: the first node's prefix
-// a_1..a_L (independent loads), the residuals re-derived -- the state unrank() would produce
-// (node-unit slices start at a node's entry unit, so the offset is 0).
+// Slice entry from the precomputed slice-start table (stride L words for node-unit plans, L + 1
+// for row-unit plans): the first node's prefix a_1..a_L (independent loads) and, for row
+// units, the row offset inside the node; the residuals are re-derived -- the state unrank()
+// would produce.  Returns the offset (node units: 0, the slice starts at a node's entry).
+template <int D>
+__device__ __forceinline__ uint32_t starts_stride(const Consts &c) {
+  return (uint32_t)(D - 2) + (c.alpha ? 0u : 1u);
+}
 template <int D, bool NEED_AD, class KT>
 __device__ __forceinline__ uint64_t start_from_table(Lane<D> &st, const Consts &c, const KT &kt, const uint32_t *p) {
   constexpr int L = D - 2;
@@ -58,20 +63,22 @@ __device__ __forceinline__ uint64_t start_from_table(Lane<D> &st, const Consts &
   st.lsum = lsum;
   st.k = st.kb = 0;
   entry<D, NEED_AD>(st, c, kt);
-  return 0;
+  return c.alpha ? 0u : __ldg(p + L);
 }
 
 // One thread per slice: unrank the slice's first unit and store the node prefix (plan setup).
 template <int D>
 __global__ void fs_slice_starts_kernel(const KParams P, uint32_t *out) {
   constexpr int L = D - 2;
+  const uint32_t stride = starts_stride<D>(P.c);
   for (uint64_t sl = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; sl < P.num_slices;
        sl += (uint64_t)gridDim.x * blockDim.x) {
     Lane<D> st;
     KTabArith kt;
-    unrank<D, false>(st, P.c, kt, P.unit0 + sl * P.T);
+    const uint64_t off = unrank<D, false>(st, P.c, kt, P.unit0 + sl * P.T);
 #pragma unroll
-    for (int k = 0; k < L; ++k) out[sl * L + k] = st.a[k];
+    for (int k = 0; k < L; ++k) out[sl * stride + k] = st.a[k];
+    if (!P.c.alpha) out[sl * stride + L] = (uint32_t)off;
   }
 }
 
@@ -1016,7 +1023,7 @@ __global__ void __launch_bounds__(kBlock, (CONS == kConsRowsAny || CONS == FS_CO
             const uint64_t u = P.unit0 + sl * P.T;
             const uint64_t e = u + P.T < P.unit1 ? u + P.T : P.unit1;
             budget = (uint32_t)(e - u);
-            const uint64_t off = P.starts ? start_from_table<D, NEED_AD>(st, c, kt, P.starts + sl * (uint64_t)(D - 2))
+            const uint64_t off = P.starts ? start_from_table<D, NEED_AD>(st, c, kt, P.starts + sl * (uint64_t)starts_stride<D>(c))
                                           : unrank<D, NEED_AD>(st, c, kt, u);
             budget -= position_in_node<D, NEED_AD>(st, c, off);
             if (CAND) enter_candidates<D>(st, c);
