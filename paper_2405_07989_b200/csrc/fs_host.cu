@@ -294,8 +294,10 @@ int fs_validate_and_build(fs_plan *p, uint64_t n, const uint32_t *gens, int d, i
         const uint32_t gL = L >= 2 ? gens[L - 1] : 0u, gL1 = L >= 2 ? gens[L - 2] : 0u;
         const uint32_t t2_off = (uint32_t)p->ktab.size();  // multiple of 2 words; padded to 4 below
         const uint32_t t2o = (t2_off + 3u) & ~3u;
-        if (consumer == FS_CONSUMER_COUNT && L >= 2 && gL <= 2048u && gL1 / gL + 1u < 65536u && c.gA < 65536u &&
-            4ull * t2o + 16ull * gL + 16384ull <= (1ull << fs::kCAdvShift)) {
+        // (histogram: the same table with word 2 = a*0 = A0 - k0(rho0) of the entry node,
+        // INT32_MIN when k0 = none; the kernel takes the node's length progression from it)
+        if ((consumer == FS_CONSUMER_COUNT || want_hist) && L >= 2 && gL <= 2048u && gL1 / gL + 1u < 65536u &&
+            c.gA < 65536u && 4ull * t2o + 16ull * gL + 16384ull <= (1ull << fs::kCAdvShift)) {
           p->ktab.resize(t2o + 4u * gL, 0u);
           for (uint32_t r = 0; r < gL; ++r) {
             const uint32_t R2 = r + gL1, dQ = R2 / gL, r2 = R2 % gL;
@@ -304,7 +306,7 @@ int fs_validate_and_build(fs_plan *p, uint64_t n, const uint32_t *gens, int d, i
             uint32_t *ent = &p->ktab[t2o + 4u * r];
             ent[0] = (4u * t2o + 16u * r2) | (dQ << 16);
             ent[1] = rho0 | (A0 << 16);
-            ent[2] = rows0;
+            ent[2] = want_hist ? (k0 == fs::kNone ? 0x80000000u : (uint32_t)((int32_t)A0 - (int32_t)k0)) : rows0;
           }
           c.t2_off = t2o;
           // Count: two-level ascend table over r3 = R_{L-2} mod g_{L-1} (L >= 3), for a lane
@@ -315,7 +317,7 @@ int fs_validate_and_build(fs_plan *p, uint64_t n, const uint32_t *gens, int d, i
           // {rel(r3') | dQ3 << 16, rho0 | A0 << 16, rows0 | r3' << 16, r2 | a_L << 16}.
           const uint32_t gL2 = L >= 3 ? gens[L - 3] : 0u;
           const uint32_t t3o = ((uint32_t)p->ktab.size() + 3u) & ~3u;
-          if (L >= 3 && gL1 <= 2048u && gL2 / gL1 + 1u < 65536u && gL1 < 65536u && gL < 65536u &&
+          if (consumer == FS_CONSUMER_COUNT && L >= 3 && gL1 <= 2048u && gL2 / gL1 + 1u < 65536u && gL1 < 65536u && gL < 65536u &&
               4ull * t3o + 16ull * gL1 + 16384ull <= (1ull << fs::kCAdvShift)) {
             bool fits = true;
             std::vector<uint32_t> t3(4u * gL1, 0u);

@@ -631,6 +631,25 @@ __device__ __forceinline__ void t3_ascend(Lane<D> &st, const Consts &c, uint32_t
   }
 }
 
+// Histogram: the one-level ascend by the same table (word 2 = a*0 of the new run's entry
+// node); the entry's length progression is then taken by take_entry_hist.
+template <int D>
+__device__ __forceinline__ void t2_ascend_hist(Lane<D> &st, const Consts &c, uint32_t &t2a, uint32_t &q2) {
+  if constexpr (D >= 4) {
+    constexpr int L = D - 2;
+    const uint4 w = lds128(t2a);
+    t2a = w.x & ((1u << kCAdvShift) - 1u);
+    q2 += w.x >> 16;
+    st.a[L - 2] -= 1u;
+    st.R[L - 2] += c.g[L - 2];
+    st.a[L - 1] = q2;
+    st.lsum = st.lsum - 1u + q2;
+    st.rho = w.y & 0xffffu;
+    st.A = w.y >> 16;
+    st.cur = (int32_t)w.z;
+  }
+}
+
 template <int D, int G>
 __device__ __forceinline__ void cc_group(Lane<D> &st, const Consts &c, uint32_t tab, uint32_t &cnt) {
   if constexpr (D >= 3) {
@@ -896,6 +915,7 @@ __global__ void __launch_bounds__(kBlock, (CONS == kConsRowsAny || CONS == FS_CO
   const bool cfast = KTAB && CONS == kConsCountClosed && c.cadv_off != 0 && ktab_base < 16384u;
   const bool hfast = KTAB && CONS == kConsHistClosed && c.cadv_off != 0 && P.hist_smem && ktab_base < 16384u;
   const bool t2fast = cfast && D >= 4 && c.t2_off != 0;
+  const bool t2h = hfast && D >= 4 && c.t2_off != 0;  // histogram: one-level ascend by table
   const uint32_t t2base = ktab_base + 4u * c.t2_off;
   uint32_t t2a = t2base, q2 = 0;  // count: ascend-table entry of r = R_{L-1} mod g_L, Q = R_{L-1} / g_L
   const bool t3fast = t2fast && D >= 5 && c.t3_off != 0;
@@ -907,7 +927,7 @@ __global__ void __launch_bounds__(kBlock, (CONS == kConsRowsAny || CONS == FS_CO
     if ((cfast || hfast) && i >= c.cadv_off && i < c.cadv_off + c.cadv_words * c.gA &&
         (i - c.cadv_off) % c.cadv_words == 0u)
       v += ktab_base;
-    if (cfast && c.t2_off != 0u && D >= 4 && i >= c.t2_off && i < c.t2_off + 4u * c.g[D >= 4 ? D - 3 : 0] &&
+    if ((cfast || hfast) && c.t2_off != 0u && D >= 4 && i >= c.t2_off && i < c.t2_off + 4u * c.g[D >= 4 ? D - 3 : 0] &&
         ((i - c.t2_off) & 3u) == 0u)
       v += ktab_base;
     if (cfast && c.cadv2_off != 0u &&
@@ -1030,7 +1050,7 @@ __global__ void __launch_bounds__(kBlock, (CONS == kConsRowsAny || CONS == FS_CO
             sync_k<D, ALPHA>(st, budget);
             if (CONS == FS_CONSUMER_ROWS) e_rows.start((u - P.unit0) * (uint64_t)EmitRows<D, B>::kRB);
             if (cfast) e_count.n += take_entry_rows<D>(st, c);
-            if (t2fast) t2_sync<D>(st, c, t2base, t2a, q2);
+            if (t2fast || t2h) t2_sync<D>(st, c, t2base, t2a, q2);
             if (t3fast) t3_sync<D>(st, c, t3base, t3a, q3);
             if (hfast) take_entry_hist<D>(st, c, e_hcl);
           }
@@ -1120,6 +1140,10 @@ __global__ void __launch_bounds__(kBlock, (CONS == kConsRowsAny || CONS == FS_CO
             t2_ascend<D>(st, c, t2a, q2, e_count.n);
             budget -= 1u;
             sync_k<D, ALPHA>(st, budget);
+          } else if (t2h && t2_can_ascend<D>(st)) {  // one-level ascend by table (histogram)
+            t2_ascend_hist<D>(st, c, t2a, q2);
+            budget -= 1u;
+            sync_k<D, ALPHA>(st, budget);
           } else if (t3fast && t3_can_ascend<D>(st)) {  // two-level ascend by table (count)
             t3_ascend<D>(st, c, t3a, q3, t2base, t2a, q2, e_count.n);
             budget -= 1u;
@@ -1129,7 +1153,7 @@ __global__ void __launch_bounds__(kBlock, (CONS == kConsRowsAny || CONS == FS_CO
           if (CAND) enter_candidates<D>(st, c);
           sync_k<D, ALPHA>(st, budget);
           if (cfast) e_count.n += take_entry_rows<D>(st, c);
-          if (t2fast) t2_sync<D>(st, c, t2base, t2a, q2);
+          if (t2fast || t2h) t2_sync<D>(st, c, t2base, t2a, q2);
           if (t3fast) t3_sync<D>(st, c, t3base, t3a, q3);
           }
           if (hfast) take_entry_hist<D>(st, c, e_hcl);
