@@ -548,7 +548,12 @@ void fs_plan_free_device(fs_plan *p) {
   if (p->ktab_dev) cudaFree(p->ktab_dev);
   if (p->scratch_dev) cudaFree(p->scratch_dev);
   if (p->diff_dev) cudaFree(p->diff_dev);
-  if (p->starts_dev) cudaFree(p->starts_dev);
+  if (p->starts_dev) {
+    if (p->starts_async)
+      cudaFreeAsync(p->starts_dev, p->stream);  // back to the pool, stream-ordered after the plan's work
+    else
+      cudaFree(p->starts_dev);
+  }
   p->diff_dev = nullptr;
   p->starts_dev = nullptr;
   p->U_dev = nullptr;

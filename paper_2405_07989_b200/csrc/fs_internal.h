@@ -117,7 +117,8 @@ struct fs_plan {
   uint32_t *ktab_dev = nullptr;
   unsigned long long *scratch_dev = nullptr;  // [0] queue head, [1..] spare
   unsigned long long *diff_dev = nullptr;     // closed-tail histogram difference array
-  uint32_t *starts_dev = nullptr;             // slice-start table (node-unit plans), or nullptr
+  uint32_t *starts_dev = nullptr;             // slice-start table, or nullptr
+  bool starts_async = false;                  // starts_dev came from cudaMallocAsync (pool)
   bool uploaded = false;
   uint32_t grid = 0, block = fs::kBlock;
   int last_launches = 0;

@@ -32,11 +32,24 @@ int fs_build_slice_starts(fs_plan *p) {
   if (L < 1 || p->num_slices == 0) return FS_OK;
   const uint64_t words = p->num_slices * (uint64_t)(L + (p->c.alpha ? 0 : 1));  // row units: + offset
   if (words * 4u > (256ull << 20)) return FS_OK;  // the unrank path instead
-  if (cudaMalloc(&p->starts_dev, words * 4u) != cudaSuccess) {
+  // stream-ordered allocation from the device's memory pool (kept across plans: a one-shot
+  // fs_count would otherwise pay a synchronous cudaMalloc/cudaFree of tens of MB per call)
+  static bool pool_set[64] = {false};
+  if (p->device >= 0 && p->device < 64 && !pool_set[p->device]) {
+    cudaMemPool_t pool;
+    if (cudaDeviceGetDefaultMemPool(&pool, p->device) == cudaSuccess) {
+      uint64_t keep = 1ull << 30;
+      cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &keep);
+    }
+    cudaGetLastError();
+    pool_set[p->device] = true;
+  }
+  if (cudaMallocAsync(reinterpret_cast<void **>(&p->starts_dev), words * 4u, p->stream) != cudaSuccess) {
     cudaGetLastError();
     p->starts_dev = nullptr;
     return FS_OK;
   }
+  p->starts_async = true;
   fs::KParams kp;
   memset(&kp, 0, sizeof(kp));
   kp.c = p->c;
