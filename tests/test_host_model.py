@@ -269,3 +269,20 @@ def test_validation_errors():
     Plan(2 ** 31 - 21, (20, 3))  # n + max g = 2^31 - 1: accepted (d = 2, no tables)
     with pytest.raises(ValueError):
         Plan(10, (2, 3), rank=2, world=2)
+
+
+def test_filtered_and_order_argument_checks():
+    """fs_enumerate_filtered_ex rejects a bad width / predicate / misaligned buffer before any
+    GPU work (FS_EINVAL on any machine); the exec struct carries the rows_impl field."""
+    import ctypes
+
+    g = (ctypes.c_uint32 * 3)(6, 9, 20)
+    fn = L.lib().fs_enumerate_filtered_ex
+    ex = L.ExecT()
+    ex.device, ex.world = -1, 1
+    assert fn(1000, g, 3, 8, L.FS_PRED_LEN_EQ, 100, None, 0, ctypes.byref(ex)) == L.FS_EINVAL  # B
+    assert fn(1000, g, 3, 16, 0, 100, None, 0, ctypes.byref(ex)) == L.FS_EINVAL  # predicate
+    assert fn(1000, g, 3, 16, 9, 100, None, 0, ctypes.byref(ex)) == L.FS_EINVAL
+    assert fn(1000, g, 3, 16, L.FS_PRED_LEN_EQ, 100, ctypes.c_void_p(8), 10, ctypes.byref(ex)) == L.FS_EINVAL
+    names = [f for f, _ in L.ExecT._fields_]
+    assert "rows_impl" in names and names.index("rows_impl") == names.index("gen_order") + 1
