@@ -127,15 +127,69 @@ def microbench():
 OPS_NODE_CLOSED = 8  # node entry (5) + closed-form row count floor(a*/s) + 1: max, mulhi, add (NEXT-1)
 
 
-def ops_model(info, closed: bool = False) -> float:
+OPS_NODE_HIST_CLOSED = 12  # closed-tail histogram: node entry (5) + rows (3) + first-row length (2) + two
+#                            difference-array updates (2)
+OPS_NODE_ANY_CLOSED = 14   # closed-tail any: node entry (5) + rows (3) + a_d of the first row (2) + the
+#                            progression's extreme length (2) + compare/flag (2)
+
+
+def ops_model(info, closed: bool = False, hist: bool = False, any_: bool = False) -> float:
     """algorithmic integer ops of the stream the kernel runs: per node
     entry, per row (per-row tail) or per node (closed tail), per deeper node."""
     nodes = info["nodes_per_level"]
     L = info["level"]
     deep = sum(nodes[1:L]) if L >= 2 else 0
     if closed:
-        return OPS_NODE_CLOSED * nodes[L] + OPS_DEEP * deep
+        per = OPS_NODE_HIST_CLOSED if hist else OPS_NODE_ANY_CLOSED if any_ else OPS_NODE_CLOSED
+        return per * nodes[L] + OPS_DEEP * deep
     return OPS_NODE * nodes[L] + OPS_ROW * info["total_rows"] + OPS_DEEP * deep
+
+
+OPS_CAND = 5  # one candidate of the paper's index-(d-1) loop: residue add, conditional subtract,
+#              zero test, accumulate, loop (SURVEY 8(d) c_step)
+OPS_MODEL_DOC = ("closed tail: 8 int ops per level-L node (entry 5 + closed-form row count 3) + 12 per "
+                 "deeper node; per-row tail: 5 per node + 4 per row + 12 per deeper node; Skip ablations: "
+                 "5 per candidate + 5 per node + 12 per deeper node (DESIGN.md section 6)")
+
+
+def paper_candidates(inst, skip_paper: bool, gens=None) -> int:
+    """Exact number of candidates the paper's stream (Alg. 3.1) visits on the
+    instance, with or without its modulo skip: Skip=off visits
+    sum_{k<d} #{prefixes of length k with phi < n}; with the skip, a level-(d-2)
+    node of residual R > 0 visits c - j (s - 1) index-(d-1) candidates instead of
+    c = ceil(R / g_{d-1}), where a* is its largest valid a_{d-1} and j = floor(a* / s) the jumps
+    (none without a valid a*).  Reproduces SURVEY's 9,576 / 3,629 (C1)."""
+    from math import gcd
+
+    n = inst.n
+    g = list(gens or inst.gens)
+    d = len(g)
+    if d < 2:
+        return 1
+    F = [0] * (n + 1)
+    F[0] = 1
+    tot = 1 if n > 0 else 0  # the empty prefix
+    for k in range(d - 2):
+        for r in range(g[k], n + 1):
+            F[r] += F[r - g[k]]
+        tot += sum(F[:n])  # prefixes of length k + 1 with phi < n
+    gA, gB = g[d - 2], g[d - 1]
+    s = gB // gcd(gA, gB)
+    for phi in range(n):
+        m = F[phi]
+        if not m:
+            continue
+        R = n - phi
+        c = -(-R // gA)
+        cnt = c
+        if skip_paper:
+            a = R // gA
+            while a >= 0 and (R - a * gA) % gB:
+                a -= 1
+            if a >= 0:
+                cnt = c - (a // s) * (s - 1)
+        tot += m * cnt
+    return tot
 
 
 # ------------------------------------------------------------------ CPU oracle (baseline arm)
@@ -190,10 +244,49 @@ def oracle_sample(inst, seconds: float, seed: int = 0):
     return (num / den if den else 0.0), rows_tot, secs_tot, boxes
 
 
-def base_config(inst, total: int) -> dict:
-    """The workload keys both arms report (fsgpu and --impl reference)."""
+def cpu_info() -> dict:
+    """Host CPU model and core count (the oracle baseline runs on one pinned core)."""
+    model = None
+    try:
+        with open("/proc/cpuinfo") as f:
+            for ln in f:
+                if ln.startswith("model name"):
+                    model = ln.split(":", 1)[1].strip()
+                    break
+    except OSError:
+        pass
+    return {"cpu_model": model, "nproc": os.cpu_count()}
+
+
+class pinned_core:
+    """Run the oracle on ONE host core (`taskset -c 0` equivalent); restores the
+    previous affinity afterwards."""
+
+    def __init__(self, core: int = 0):
+        self.core = core
+        self.prev = None
+
+    def __enter__(self):
+        try:
+            self.prev = os.sched_getaffinity(0)
+            core = self.core if self.core in self.prev else min(self.prev)
+            os.sched_setaffinity(0, {core})
+            self.core = core
+        except (AttributeError, OSError):
+            self.prev = None
+        return self
+
+    def __exit__(self, *exc):
+        if self.prev is not None:
+            os.sched_setaffinity(0, self.prev)
+
+
+def base_config(inst, total: int, world: int) -> dict:
+    """The workload keys both arms report (fsgpu and --impl reference), identical in both."""
     return {"workload": "%s: Z(%d, %s) count, |Z| = %d" % (inst.name, inst.n, list(inst.gens), total),
-            "instance": inst.name, "n": inst.n, "gens": list(inst.gens), "consumer": "count"}
+            "instance": inst.name, "n": inst.n, "gens": list(inst.gens), "consumer": "count",
+            "parallelism": "lex-slice dp%d" % world,
+            "l2": "flushed between steps (256 MB write)"}
 
 
 def run_reference(args, inst):
@@ -201,22 +294,24 @@ def run_reference(args, inst):
     if rank != 0:
         return 0
     per_step = max(1.0, float(os.environ.get("FS_REF_STEP_SECONDS", "6")))
-    for _ in range(args.warmup):
-        oracle_sample(inst, min(per_step, 2.0), seed=1)
     vals = []
     tot_rows, tot_s = 0, 0.0
-    for k in range(args.steps):
-        rate, rows, secs, boxes = oracle_sample(inst, per_step, seed=100 + k)
-        vals.append(rate)
-        tot_rows += rows
-        tot_s += secs
+    with pinned_core(0) as pc:
+        for _ in range(args.warmup):
+            oracle_sample(inst, min(per_step, 2.0), seed=1)
+        for k in range(args.steps):
+            rate, rows, secs, boxes = oracle_sample(inst, per_step, seed=100 + k)
+            vals.append(rate)
+            tot_rows += rows
+            tot_s += secs
     value = statistics.mean(vals)
     line = {
         "impl": "reference", "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": args.gpus,
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1000.0 * tot_s / args.steps,
         "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "u64",
-        "data": "synthetic", "config": base_config(inst, __import__("oracle").gf.count(inst.n, inst.gens)),
-        "cpu_baseline": {"value": value, "unit": UNIT, "cores": 1, "kind": "oracle",
+        "data": "synthetic", "config": base_config(inst, __import__("oracle").gf.count(inst.n, inst.gens), args.gpus),
+        "cpu_baseline": {"value": value, "unit": UNIT, "cores": 1, "kind": "oracle", "pinned_core": pc.core,
+                         **cpu_info(),
                          "sample": "work-weighted prefix boxes of %s, seeds 100..%d, %.0f s per step, "
                                    "%d rows total, ratio estimator" % (inst.name, 99 + args.steps, per_step,
                                                                         tot_rows)},
@@ -260,9 +355,15 @@ def main():
     dev = torch.device("cuda", local)
     if world > 1:
         if backend == "nccl":
+            # the communicator's init line (rank / nranks) goes to stderr, so the rank count of
+            # the run can be checked from the log
+            os.environ.setdefault("NCCL_DEBUG", "INFO")
+            os.environ.setdefault("NCCL_DEBUG_SUBSYS", "INIT")
             dist.init_process_group("nccl", device_id=dev)
         else:
             dist.init_process_group(backend)
+        print("[bench] rank %d/%d backend=%s device=cuda:%d" % (rank, world, dist.get_backend(), local),
+              file=sys.stderr, flush=True)
     stream = torch.cuda.current_stream()
     peaks, peaks_kind = load_peaks()
 
@@ -275,7 +376,7 @@ def main():
         if world == 1:
             return x
         t = torch.tensor([x], dtype=torch.float64, device=dev)
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        fsdist.combine_max(t)
         return float(t.item())
 
     # ---- plan: constants + DP tables resident in HBM before the timed region
@@ -290,8 +391,7 @@ def main():
 
     def step():
         plan.count_async(out)
-        if world > 1:
-            dist.all_reduce(out, op=dist.ReduceOp.SUM)
+        fsdist.combine_sum(out)
 
     for _ in range(args.warmup):
         step()
@@ -311,8 +411,7 @@ def main():
         kev[k][0].record(stream)
         plan.count_async(out)
         kev[k][1].record(stream)
-        if world > 1:
-            dist.all_reduce(out, op=dist.ReduceOp.SUM)
+        fsdist.combine_sum(out)  # NCCL all_reduce on the stream (gloo: staged through the host)
         ev[k][1].record(stream)
     barrier()
     clocks = sampler.stop()
@@ -338,28 +437,36 @@ def main():
     achieved = ops / (ms_kern / 1e3) / 1e12
     traffic = _traffic(args.workload)
 
+    rank_units = [[info["unit_begin"], info["unit_end"]]]
+    if world > 1:
+        allr = [None] * world
+        dist.all_gather_object(allr, rank_units[0])
+        rank_units = allr
+    cands = paper_candidates(inst, skip_paper=True)
     line = {
         "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
         "warmup": args.warmup, "ms_per_step": ms_step, "higher_is_better": True, "scaling": "strong",
         "vs_baseline": None, "dtype": "u32", "data": "synthetic",
-        "config": {**base_config(inst, total),
-                   "method": "Alg. 3.1 stream over the generators largest-first (gen_order=auto, NEXT-2), "
-                             "modulo skip at run entry, closed-form row count per node (tail=closed, NEXT-1)",
-                   "nodes": info["nodes_per_level"][-1],
-                   "parallelism": "lex-slice dp%d" % world, "l2": "flushed between steps (256 MB write)",
-                   "dist_backend": backend if world > 1 else None,
-                   "slice_units": info["slice_units"], "num_slices": info["num_slices"],
-                   "grid": plan.info["grid"], "block": info["block"]},
+        "config": base_config(inst, total, world),
+        "plan": {"method": "Alg. 3.1 stream over the generators largest-first (gen_order=auto, NEXT-2), "
+                           "modulo skip at run entry, closed-form row count per node (tail=closed, NEXT-1)",
+                 "nodes": info["nodes_per_level"][-1], "nodes_per_level": info["nodes_per_level"],
+                 "dist_backend": (dist.get_backend() if world > 1 else None),
+                 "slice_units": info["slice_units"], "num_slices": info["num_slices"],
+                 "grid": plan.info["grid"], "block": info["block"], "rank_units": rank_units},
         "roofline": {"bound": "alu", "achieved": achieved, "peak": peak_tops, "unit": "Tops/s (int32 lane-ops)",
                      "frac": achieved / peak_tops, "traffic": traffic,
                      "peak_source": ("measured: best INT32 microbenchmark (fs_micro.cu)" if measured_tops else
                                      "derived: 128 int lane-ops/clk/SM x 148 SMs x %.0f MHz" % sm_max),
                      "derived_issue_peak": derived_tops, "frac_of_derived": achieved / derived_tops,
-                     "ops_per_launch": ops, "kernel_ms": ms_kern},
+                     "ops_per_launch": ops, "ops_model": OPS_MODEL_DOC, "kernel_ms": ms_kern},
         "gpu_launches": int(launches),
         "microbench": mb,
         "clocks": clocks,
-        "cand_per_s": None,
+        # the paper's own stream (Alg. 3.1 with its modulo skip) visits
+        # `cands` candidates on this instance (exact DP count); the kernel skips most of them
+        "cand_per_s": {"value": cands / (ms_step / 1e3), "candidates": cands,
+                       "stream": "Alg. 3.1 with the paper's modulo skip (Skip=paper), exact DP count"},
     }
 
     # ---- e2e: through the public API with host buffers (DP + H2D + kernel + D2H per step)
@@ -378,17 +485,26 @@ def main():
     line["e2e"] = {"value": total / e2e_s, "unit": UNIT, "h2d_bytes_per_step": int(info["table_bytes"]),
                    "d2h_bytes_per_step": 8, "seconds": e2e_s}
 
-    # ---- extras (same run): store (materialise C2-XL) and C4 length histogram
+    # ---- extras (same run): store (materialise C2-XL) and C4 length histogram; the rooflines
+    # of the other consumers' kernels are nested in `roofline` (hist, any, store, store_any, ..)
     if not args.no_extra:
-        line["extra"] = extras(args, world, rank, local, dev, stream, peaks, peaks_kind, barrier, max_over_ranks,
-                               mb)
+        ex = extras(args, world, rank, local, dev, stream, peaks, peaks_kind, barrier, max_over_ranks, mb)
+        line["extra"] = ex
+        for rk, ek in (("hist", "hist_auto_order_closed"), ("any", "c5_any_P_none_auto_order_closed"),
+                       ("store", "store"), ("store_any", "store_any"), ("store_increasing", "store_increasing")):
+            if ek in ex and isinstance(ex[ek], dict) and "roofline" in ex[ek]:
+                line["roofline"][rk] = {**ex[ek]["roofline"], "ms": ex[ek].get("ms"),
+                                        "workload": ex[ek].get("workload"), "extra_key": ek}
 
     # ---- CPU oracle beside it (rank 0, N = 1 only)
-    if world == 1:
-        rate, rows, secs, boxes = oracle_sample(inst, args.cpu_seconds)
-        line["cpu_baseline"] = {"value": rate, "unit": UNIT, "cores": 1, "kind": "oracle",
+    if world == 1 and args.cpu_seconds > 0:
+        with pinned_core(0) as pc:
+            rate, rows, secs, boxes = oracle_sample(inst, args.cpu_seconds)
+        line["cpu_baseline"] = {"value": rate, "unit": UNIT, "cores": 1, "kind": "oracle", "pinned_core": pc.core,
+                                **cpu_info(),
                                 "sample": "%d work-weighted prefix boxes of %s (seed 0): %d rows in %.1f s, "
-                                          "1 thread, ratio estimator" % (boxes, inst.name, rows, secs)}
+                                          "1 thread pinned to one core, ratio estimator" % (boxes, inst.name, rows,
+                                                                                          secs)}
     if rank == 0:
         print(json.dumps(line), flush=True)
     if world > 1:
@@ -456,7 +572,9 @@ def extras(args, world, rank, local, dev, stream, peaks, peaks_kind, barrier, ma
             store_out = torch.empty((rows, inst.d), dtype=torch.uint16, device=dev)
         out = store_out[:rows]
         p.enumerate_async(16, out, rows)
+        p.rows_check()  # order = any: the M2 cursors met exactly (every row written once)
         ms = _time_ms(lambda: p.enumerate_async(16, out, rows), stream, 5, barrier, max_over_ranks)
+        p.rows_check()
         total_rows = info["total_rows"]
         bytes_ = total_rows * inst.d * 2
         gbs_all = bytes_ / (ms / 1e3) / 1e9
@@ -560,13 +678,25 @@ def extras(args, world, rank, local, dev, stream, peaks, peaks_kind, barrier, ma
         ex[key] = {"workload": "%s: Z(%d, %s)" % (label, inst.n, list(inst.gens)), "rows": total, "ms": ms,
                    "value": total / (ms / 1e3), "unit": UNIT,
                    "nodes": p.info["nodes_per_level"][-1]}
-        if cons == L.FS_CONSUMER_COUNT and mb:
-            pi = p.info
-            sh = (pi["unit_end"] - pi["unit_begin"]) / max(1, pi["total_units"])
-            ach = ops_model(pi, closed=pk.get("tail", 0) == 1) * sh / (ms / 1e3) / 1e12
+        pi = p.info
+        sh = (pi["unit_end"] - pi["unit_begin"]) / max(1, pi["total_units"])
+        tail = pk.get("tail", 0)
+        if tail in (L.FS_TAIL_SKIP_OFF, L.FS_TAIL_SKIP_PAPER):  # the paper's candidate loop
+            cands = paper_candidates(inst, tail == L.FS_TAIL_SKIP_PAPER)
+            ex[key]["candidates"] = cands
+            ex[key]["cand_per_s"] = cands * sh / (ms / 1e3)
+        if mb and cons in (L.FS_CONSUMER_COUNT, L.FS_CONSUMER_HIST):
+            if tail in (L.FS_TAIL_SKIP_OFF, L.FS_TAIL_SKIP_PAPER):
+                ops = OPS_CAND * ex[key]["candidates"] + ops_model(pi, closed=True) - 3 * pi["nodes_per_level"][-1]
+            elif cons == L.FS_CONSUMER_HIST:
+                ops = ops_model(pi, closed=tail == 1, hist=True)
+            else:
+                ops = ops_model(pi, closed=tail == 1)
+            ach = ops * sh / (ms / 1e3) / 1e12
             pk_tops = max(v["tops"] for v in mb.values() if isinstance(v, dict))
-            ex[key]["roofline"] = {"bound": "alu", "achieved": ach, "peak": pk_tops, "unit": "Tops/s",
-                                   "frac": ach / pk_tops}
+            ex[key]["roofline"] = {"bound": "alu", "achieved": ach, "peak": pk_tops, "unit": "Tops/s (int32 lane-ops)",
+                                   "frac": ach / pk_tops, "ops_per_launch": ops * sh,
+                                   "traffic": _traffic(key)}
     for order_name, pk in (("", {}), ("_auto_order", {"gen_order": AUTO}),
                            ("_auto_order_closed", {"gen_order": AUTO, "tail": L.FS_TAIL_CLOSED})):
         pa = api.Plan(W.C5.n, W.C5.gens, L.FS_CONSUMER_ANY, **pk, **kw)
@@ -577,7 +707,19 @@ def extras(args, world, rank, local, dev, stream, peaks, peaks_kind, barrier, ma
                 allreduce(f, dist.ReduceOp.MAX if world > 1 else None)
 
             ms = _time_ms(any_step, stream, 3, barrier, max_over_ranks)
-            ex["c5_any_%s%s" % (name, order_name)] = {"pred": [pred, arg], "found": bool(f.item()), "ms": ms}
+            ek = "c5_any_%s%s" % (name, order_name)
+            ex[ek] = {"pred": [pred, arg], "found": bool(f.item()), "ms": ms}
+            if name == "P_none" and pk.get("tail") == L.FS_TAIL_CLOSED and mb:
+                # no witness: the whole stream is scanned, one closed-form test per node
+                pi = pa.info
+                sh = (pi["unit_end"] - pi["unit_begin"]) / max(1, pi["total_units"])
+                ops = ops_model(pi, closed=True, any_=True) * sh
+                pk_tops = max(v["tops"] for v in mb.values() if isinstance(v, dict))
+                ach = ops / (ms / 1e3) / 1e12
+                ex[ek]["workload"] = "C5 any-predicate sum(a) <= 19 (no witness: full scan), NEXT-1 + NEXT-2"
+                ex[ek]["roofline"] = {"bound": "alu", "achieved": ach, "peak": pk_tops, "unit": "Tops/s (int32 lane-ops)",
+                                      "frac": ach / pk_tops, "ops_per_launch": ops, "nodes": pi["nodes_per_level"][-1],
+                                      "traffic": _traffic(ek)}
     return ex
 
 

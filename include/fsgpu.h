@@ -232,6 +232,13 @@ int fs_plan_hist_async(fs_plan *plan, uint64_t *hist_dev, uint64_t hist_cap);
 int fs_plan_any_async(fs_plan *plan, int pred, uint64_t pred_arg, int *found_dev, uint32_t *witness_dev);
 /* writes min(cap, rank rows) rows of the rank's block to out_dev (16-byte aligned). */
 int fs_plan_enumerate_async(fs_plan *plan, int B, void *out_dev, uint64_t cap);
+/* ROWS plans, after fs_plan_enumerate_async: waits for the plan's stream, then checks the
+ * order = any (M2) exactness invariant -- the front cursor (8-row blocks growing up) and the
+ * back cursor (each warp's final < 8 rows, growing down from the rank's row count) must meet
+ * exactly, so every row was written exactly once (every bound
+ * factorization is saved exactly once).  FS_OK (also for other orders, and before any run),
+ * FS_ECUDA if the cursors did not meet or the copy failed, FS_EINVAL for a non-ROWS plan. */
+int fs_plan_rows_check(fs_plan *plan);
 /* number of kernel launches the last *_async call enqueued (for launch accounting) */
 int fs_plan_last_launches(const fs_plan *plan);
 void fs_plan_destroy(fs_plan *plan);

@@ -150,3 +150,30 @@ def work_tables(n: int, gens: Sequence[int]) -> List[List[int]]:
             pref[r] = acc
         out[k] = pref
     return out
+
+
+def count_pair(n: int, a: int, b: int) -> int:
+    """|Z(n, (a, b))| = #{(x, y) >= 0 : a x + b y = n}, solved as a linear congruence (the
+    definition of Z, PAPER.md:29-31, for d = 2): with h = gcd(a, b), no solution unless h | n;
+    else x must satisfy (a/h) x = n/h (mod b/h), i.e. x = x0 + k b/h with
+    x0 = (n/h) (a/h)^{-1} mod (b/h), and 0 <= x <= floor(n / a)."""
+    from math import gcd
+
+    if n < 0:
+        return 0
+    h = gcd(a, b)
+    if n % h:
+        return 0
+    a1, b1, n1 = a // h, b // h, n // h
+    x0 = (n1 * pow(a1, -1, b1)) % b1 if b1 > 1 else 0
+    top = n1 // a1
+    return 0 if x0 > top else (top - x0) // b1 + 1
+
+
+def count_d3(n: int, gens: Sequence[int]) -> int:
+    """|Z(n, (g1, g2, g3))| as the sum over a_1 of the two-generator counts of the residual
+    (Z(n, g) is the disjoint union over a_1 of {a_1} x Z(n - a_1 g_1, (g_2, g_3))).  O(n / g_1)
+    Python steps: usable for d = 3 instances with n near 2^31 when g_1 is large, where the
+    coin-change DP (count) would need O(n) memory and time."""
+    g1, g2, g3 = (int(x) for x in gens)
+    return sum(count_pair(n - x * g1, g2, g3) for x in range(n // g1 + 1))

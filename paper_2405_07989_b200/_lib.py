@@ -86,6 +86,7 @@ EXPORTS = {
     "fs_plan_any_async": (ctypes.c_int, [vp, ctypes.c_int, u64, vp, vp]),
     "fs_plan_enumerate_async": (ctypes.c_int, [vp, ctypes.c_int, vp, u64]),
     "fs_plan_last_launches": (ctypes.c_int, [vp]),
+    "fs_plan_rows_check": (ctypes.c_int, [vp]),
     "fs_plan_destroy": (None, [vp]),
     "fs_strerror": (ctypes.c_char_p, [ctypes.c_int]),
     "fs_version": (ctypes.c_int, []),

@@ -228,6 +228,10 @@ class Plan:
         return L.check(L.lib().fs_plan_enumerate_async(self._h, int(B), ctypes.c_void_p(out.data_ptr()), int(cap)),
                        "enumerate_async")
 
+    def rows_check(self) -> None:
+        """Wait for the plan's stream and check the order=any (M2) cursor invariant (raises)."""
+        L.check(L.lib().fs_plan_rows_check(self._h), "fs_plan_rows_check")
+
     def last_launches(self) -> int:
         return int(L.lib().fs_plan_last_launches(self._h))
 

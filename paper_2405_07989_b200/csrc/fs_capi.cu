@@ -163,22 +163,30 @@ int fs_plan_hist_async(fs_plan *p, uint64_t *hist_dev, uint64_t hist_cap) {
   fs::KParams kp = base_params(p);
   kp.hist_out = reinterpret_cast<unsigned long long *>(hist_dev);
   if (p->ex.tail == FS_TAIL_CLOSED && p->d >= 2) {
-    // closed tail: strided difference array + finalize (two launches)
+    // closed tail: strided difference array + finalize (two or four launches)
     kp.diff_len = (uint32_t)(p->hist_len + p->c.dstride);
-    kp.hist_smem = kp.diff_len <= fs::kHistSmemMax ? 1u : 0u;
+    // 32-bit shared difference bins only while one inner-loop iteration of a CTA (256 lanes x
+    // FS_CC_GROUP nodes, <= 2^29 at < 2^17 rows per node) changes a bin by less than the
+    // kernel's 2^30 drain guard, so a bin stays below 2^31; else 64-bit global atomics
+    const uint64_t max_node_rows = (p->n / p->c.gA) / p->c.s + 1;
+    kp.hist_smem = kp.diff_len <= fs::kHistSmemMax && max_node_rows < (1ull << 17) ? 1u : 0u;
     // group-form kernels spread the shared updates over 32 lane-private copies (one bank
     // each: no bank conflicts) when they fit
     kp.hist_rep = (kp.hist_smem && p->c.cadv_off && (size_t)(kp.diff_len + 1) * FS_HIST_REP * 4 <= fs::kHistRepBytes)
                       ? (uint32_t)FS_HIST_REP : 1u;
-    if (!p->diff_dev && cudaMalloc(&p->diff_dev, (size_t)kp.diff_len * 8) != cudaSuccess) return FS_ENOMEM;
+    const uint64_t scratch = fs_hist_finalize_scratch(p->hist_len, p->c.dstride);
+    if (!p->diff_dev && cudaMalloc(&p->diff_dev, ((size_t)kp.diff_len + scratch) * 8) != cudaSuccess) return FS_ENOMEM;
     if (cudaMemsetAsync(p->diff_dev, 0, (size_t)kp.diff_len * 8, p->stream) != cudaSuccess) return FS_ECUDA;
     kp.diff_out = p->diff_dev;
     rc = fs_launch(p, fs::kConsHistClosed, 16, kp, p->stream);
     if (rc != FS_OK) return rc;
-    rc = fs_launch_hist_finalize(kp, p->stream);
-    if (rc == FS_OK) p->last_launches = 2;
+    int fl = 0;
+    rc = fs_launch_hist_finalize(kp, scratch ? p->diff_dev + kp.diff_len : nullptr, p->stream, &fl);
+    if (rc == FS_OK) p->last_launches = 1 + fl;
     return rc;
   }
+  // per-row histogram: one inner-loop iteration adds at most 4 rows per lane, far below the
+  // drain guard's 2^30, whatever the instance
   return finish(p, fs_launch(p, FS_CONSUMER_HIST, 16, kp, p->stream));
 }
 
@@ -282,6 +290,20 @@ int fs_plan_enumerate_async(fs_plan *p, int B, void *out_dev, uint64_t cap) {
   return finish(p, fs_launch(p, FS_CONSUMER_ROWS, B, kp, p->stream));
 }
 
+int fs_plan_rows_check(fs_plan *p) {
+  if (!p || p->c.alpha != 0) return FS_EINVAL;
+  if (!p->uploaded || p->ex.order != FS_ORDER_ANY || p->row_end == p->row_begin) return FS_OK;
+  DeviceGuard g(p->device);
+  if (sync_plan(p) != FS_OK) return FS_ECUDA;
+  // M2 exactness check: the front and back cursors must meet at the rank's row count
+  unsigned long long fr = 0, bk = 0;
+  char *base = reinterpret_cast<char *>(p->scratch_dev);
+  if (cudaMemcpy(&fr, base + kOffFront, 8, cudaMemcpyDeviceToHost) != cudaSuccess ||
+      cudaMemcpy(&bk, base + kOffBack, 8, cudaMemcpyDeviceToHost) != cudaSuccess)
+    return FS_ECUDA;
+  return fr + bk == p->row_end - p->row_begin ? FS_OK : FS_ECUDA;
+}
+
 // ------------------------------------------------------------------ synchronous entry points
 int fs_count_ex(uint64_t n, const uint32_t *gens, int d, const fs_exec_t *ex, uint64_t *count_out) {
   if (!count_out) return FS_EINVAL;
@@ -379,16 +401,8 @@ int64_t fs_enumerate_ex(uint64_t n, const uint32_t *gens, int d, int B, void *ou
     DeviceGuard g(h.p->device);
     rc = sync_plan(h.p);
     if (rc != FS_OK) return rc;
-    if (h.p->ex.order == FS_ORDER_ANY && h.p->row_end > h.p->row_begin) {
-      // M2 exactness check: the front and back cursors must meet at the rank's row count
-      unsigned long long fr = 0, bk = 0;
-      char *base = reinterpret_cast<char *>(h.p->scratch_dev);
-      if (cudaMemcpy(&fr, base + kOffFront, 8, cudaMemcpyDeviceToHost) != cudaSuccess ||
-          cudaMemcpy(&bk, base + kOffBack, 8, cudaMemcpyDeviceToHost) != cudaSuccess)
-        return FS_ECUDA;
-      if (fr + bk != h.p->row_end - h.p->row_begin)
-        return FS_ECUDA;
-    }
+    rc = fs_plan_rows_check(h.p);  // order = any: the M2 cursors met exactly
+    if (rc != FS_OK) return rc;
   }
   if (global_row_offset_out)  // the block's first row in the requested order
     *global_row_offset_out = h.p->ex.order == FS_ORDER_INCREASING ? h.p->total_rows - h.p->row_end : h.p->row_begin;

@@ -85,7 +85,8 @@ struct Consts {
   uint32_t dstride;      // stride of the closed-tail length-difference array (|dl|, or 1 if 0)
   uint8_t perm[FS_MAX_D];  // internal coordinate j is the caller's coordinate perm[j]
   uint32_t permuted;       // perm is not the identity
-  const uint64_t *U;     // DP tables, L rows of (n+1) entries
+  const uint64_t *U;     // DP tables: V0[x] = U[0][n - x g_1] (u0_len entries), then U[1..L-1][0..n]
+  uint32_t u0_len;       // floor(n / g_1) + 1
   // node tables (device or host), for rho in [0, g_{d-1}) (g_{d-1} <= 2048):
   //   ktab[rho]                     = k0(rho)
   //   ktab[adv_off + 2 rho]         = next(rho) | (q + carry(rho)) << 11,
@@ -297,19 +298,20 @@ FS_HD uint64_t unrank(Lane<D> &st, const Consts &c, const KT &kt, uint64_t u) {
   const uint64_t stride = (uint64_t)c.n + 1;
 #pragma unroll
   for (int k = 0; k < L; ++k) {
-    const uint64_t *Uk = c.U + (uint64_t)k * stride;
+    // level 0 is stored compactly (entry x = U[0][n - x g_1]); levels >= 1 in full
+    const uint64_t *Uk = k == 0 ? c.U : c.U + c.u0_len + (uint64_t)(k - 1) * stride;
     const uint32_t g = c.g[k];
     uint32_t top = divq(R, c.dv[k]);
     // cum(x) = U[k][R - x g] = units of the subtrees a_k in [x, top]; nonincreasing in x.
     uint32_t lo = 0, hi = top + 1;
     while (hi - lo > 1) {
       uint32_t mid = (lo + hi) >> 1;
-      if (ldU(Uk + (R - mid * g)) > u)
+      if (ldU(Uk + (k == 0 ? mid : R - mid * g)) > u)
         lo = mid;
       else
         hi = mid;
     }
-    if (lo < top) u -= ldU(Uk + (R - (lo + 1) * g));
+    if (lo < top) u -= ldU(Uk + (k == 0 ? lo + 1 : R - (lo + 1) * g));
     st.a[k] = lo;
     R -= lo * g;
     st.R[k] = R;
@@ -417,9 +419,10 @@ FS_HD void fast_step_closed(Lane<D> &st, const Consts &c, const KT &kt, uint32_t
 
 // Count-only closed step: rows = floor(max(cur + s, 0) / s), which is floor(a*/s) + 1 for a
 // node with rows (cur = a* >= 0) and 0 otherwise (cur < 0), so no compare/select is needed
-// (cur + s <= n + g_d < 2^31 keeps the magic division exact).
+// (cur + s <= n + g_d < 2^31 keeps the magic division exact).  One node can hold up to
+// ~n / (g_{d-1} s) < 2^31 rows, so the count is accumulated in 64 bits here.
 template <int D, class KT>
-FS_HD void fast_step_count_closed(Lane<D> &st, const Consts &c, const KT &kt, uint32_t &cnt) {
+FS_HD void fast_step_count_closed(Lane<D> &st, const Consts &c, const KT &kt, uint64_t &cnt) {
   constexpr int L = D - 2;
   if constexpr (L >= 1) {
     const bool fa = st.cur < 0 && st.k != 0;

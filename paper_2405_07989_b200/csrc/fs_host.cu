@@ -102,10 +102,15 @@ int fs_validate_and_build(fs_plan *p, uint64_t n, const uint32_t *gens, int d, i
   const bool batch_rows = consumer == FS_CONSUMER_ROWS && e.rows_impl == FS_ROWS_BATCH && fs_rows_batch_shape_ok(d);
   const bool may_permute = e.gen_order == FS_GENORDER_AUTO &&
                            (consumer != FS_CONSUMER_ROWS || (e.order == FS_ORDER_ANY && !batch_rows)) && d >= 3;
-  if (may_permute) {
+  // the full-width DP levels (1..L-1, n+1 entries each) must fit FS_MAX_TABLE_BYTES; level 0
+  // is stored compactly (only the residuals n - x g_1 are ever read), so d = 3 instances
+  // reach n + max g = 2^31 - 1
+  const bool tables_fit = d < 4 || (uint64_t)(d - 3) * (n + 1) * 8ull <= FS_MAX_TABLE_BYTES;
+  if (may_permute && tables_fit) {
     std::vector<int> desc(perm);
     std::stable_sort(desc.begin(), desc.end(), [&](int a, int b) { return gens[a] > gens[b]; });
-    auto nodes_L = [&](const std::vector<int> &pm) {
+    auto nodes_L = [&](const std::vector<int> &pm) -> u128 {
+      if (d == 3) return (u128)(n / gens[pm[0]]) + 1;  // level-1 nodes: a_1 = 0 .. floor(n / g_1)
       std::vector<uint64_t> F(n + 1, 0);
       F[0] = 1;
       for (int k = 0; k < d - 2; ++k) {
@@ -240,8 +245,11 @@ int fs_validate_and_build(fs_plan *p, uint64_t n, const uint32_t *gens, int d, i
       }
       const uint32_t cw = want_hist && !packed ? 4u : 2u;  // words per entry
       const uint32_t cadv_off = ((uint32_t)p->ktab.size() + 3u) & ~3u;
+      // (count: a group of FS_CC_GROUP nodes sums its rows in 32 bits before they are folded into
+      // the lane's 64-bit total, so the plan requires FS_CC_GROUP nodes' rows < 2^31)
+      const bool group_fits = consumer != FS_CONSUMER_COUNT || (uint64_t)FS_CC_GROUP * (xmax / c.s + 1) < (1ull << 31);
       if ((consumer == FS_CONSUMER_COUNT || want_hist) && e.tail == FS_TAIL_CLOSED && L >= 1 && c.s >= 2 &&
-          xmax * c.s < (1ull << 32) && c.q + 1u < (1u << (32 - fs::kCAdvShift)) &&
+          group_fits && xmax * c.s < (1ull << 32) && c.q + 1u < (1u << (32 - fs::kCAdvShift)) &&
           4ull * cadv_off + 4ull * cw * c.gA + 16384ull <= (1ull << fs::kCAdvShift)) {
         p->ktab.resize(cadv_off + cw * c.gA, 0u);
         const fs::KTabArith ar{};
@@ -425,41 +433,75 @@ int fs_validate_and_build(fs_plan *p, uint64_t n, const uint32_t *gens, int d, i
       p->total_units = c.alpha + c.beta * nr;
       p->nodes_per_level[0] = 1;
     } else {
-      if ((uint64_t)L * N1 * 8ull > FS_MAX_TABLE_BYTES) return FS_ERANGE;
-      // base: units below a node with residual r; rows-only variant for |Z|.  u64 with an
-      // explicit 2^63 guard (every DP value is a count of an exact subset of the stream).
-      std::vector<uint64_t> arr(N1), rows(N1);
-      for (uint64_t r = 0; r <= n; ++r) {
-        Consts cr = c;
-        cr.alpha = 0;
-        cr.beta = 1;
-        const uint64_t nr = fs::node_units_host((uint32_t)r, cr, p->ktab.empty() ? nullptr : p->ktab.data());
-        rows[r] = nr;
-        arr[r] = c.alpha + c.beta * nr;
-      }
-      p->U.assign((size_t)L * N1, 0);
-      for (int k = L - 1; k >= 0; --k) {
-        const uint64_t gk = gens[k];
-        for (uint64_t r = gk; r <= n; ++r) {
-          arr[r] += arr[r - gk];
-          rows[r] += rows[r - gk];
-          if (arr[r] >= (1ull << 63) || rows[r] >= (1ull << 63)) return FS_ERANGE;
+      // DP tables U[k][r] = units below a level-k prefix with residual r (k = 0..L-1).  Level 0
+      // is only ever read at r = n - x g_1 (the root's children), so it is stored compactly as
+      // V0[x] = U[0][n - x g_1], x = 0..floor(n / g_1); levels 1..L-1 are full (n + 1 entries).
+      // Layout of p->U: V0, then U[1], .., U[L-1].  u64 with an explicit 2^63 guard (every DP
+      // value counts an exact subset of the stream).
+      const uint64_t X0 = n / gens[0] + 1;
+      if (!tables_fit || (X0 + (uint64_t)(L - 1) * N1) * 8ull > FS_MAX_TABLE_BYTES) return FS_ERANGE;
+      c.u0_len = (uint32_t)X0;
+      const uint32_t *kt = p->ktab.empty() ? nullptr : p->ktab.data();
+      // rows of a level-L node with residual r: valid a_{d-1} = a*, a* - s, .. >= 0
+      auto node_rows = [&](uint64_t r) -> uint64_t {
+        const uint32_t A = (uint32_t)(r / c.gA), rho = (uint32_t)(r % c.gA);
+        const uint32_t k = kt ? kt[rho] : fs::k0_arith(rho, c);
+        return (k != fs::kNone && k <= A) ? (uint64_t)((A - k) / c.s) + 1 : 0;
+      };
+      p->U.assign((size_t)X0 + (size_t)(L - 1) * N1, 0);
+      uint64_t *V0 = p->U.data();
+      std::vector<uint64_t> v0rows(X0 + 1, 0);
+      if (L == 1) {  // the base is read at the root's children only
+        uint64_t au = 0, ar = 0;
+        for (uint64_t x = X0; x-- > 0;) {
+          const uint64_t nr = node_rows(n - x * gens[0]);
+          au += c.alpha + c.beta * nr;
+          ar += nr;
+          if (au >= (1ull << 63) || ar >= (1ull << 63)) return FS_ERANGE;
+          V0[x] = au;
+          v0rows[x] = ar;
         }
-        memcpy(&p->U[(size_t)k * N1], arr.data(), N1 * 8);
+      } else {
+        std::vector<uint64_t> arr(N1), rows(N1);
+        for (uint64_t r = 0; r <= n; ++r) {
+          const uint64_t nr = node_rows(r);
+          rows[r] = nr;
+          arr[r] = c.alpha + c.beta * nr;
+        }
+        for (int k = L - 1; k >= 1; --k) {
+          const uint64_t gk = gens[k];
+          for (uint64_t r = gk; r <= n; ++r) {
+            arr[r] += arr[r - gk];
+            rows[r] += rows[r - gk];
+            if (arr[r] >= (1ull << 63) || rows[r] >= (1ull << 63)) return FS_ERANGE;
+          }
+          memcpy(&p->U[(size_t)X0 + (size_t)(k - 1) * N1], arr.data(), N1 * 8);
+        }
+        uint64_t au = 0, ar = 0;
+        for (uint64_t x = X0; x-- > 0;) {
+          au += arr[n - x * gens[0]];
+          ar += rows[n - x * gens[0]];
+          if (au >= (1ull << 63) || ar >= (1ull << 63)) return FS_ERANGE;
+          V0[x] = au;
+          v0rows[x] = ar;
+        }
       }
-      p->total_units = arr[n];
-      p->total_rows = rows[n];
+      p->total_units = V0[0];
+      p->total_rows = v0rows[0];
       c.U = p->U.data();
       // nodes per level: #(a_1..a_k) with sum a_j g_j <= n (forward coin DP, prefix sums)
-      std::vector<uint64_t> F(N1, 0);
-      F[0] = 1;
       p->nodes_per_level[0] = 1;
-      for (int k = 1; k <= L; ++k) {
-        const uint64_t gk = gens[k - 1];
-        for (uint64_t r = gk; r <= n; ++r) F[r] = std::min<uint64_t>(F[r] + F[r - gk], 1ull << 63);
-        u128 s = 0;
-        for (uint64_t r = 0; r <= n; ++r) s += F[r];
-        p->nodes_per_level[k] = s >= ((u128)1 << 64) - 1 ? UINT64_MAX : (uint64_t)s;
+      p->nodes_per_level[1] = X0;
+      if (L >= 2) {
+        std::vector<uint64_t> F(N1, 0);
+        F[0] = 1;
+        for (int k = 1; k <= L; ++k) {
+          const uint64_t gk = gens[k - 1];
+          for (uint64_t r = gk; r <= n; ++r) F[r] = std::min<uint64_t>(F[r] + F[r - gk], 1ull << 63);
+          u128 s = 0;
+          for (uint64_t r = 0; r <= n; ++r) s += F[r];
+          p->nodes_per_level[k] = s >= ((u128)1 << 64) - 1 ? UINT64_MAX : (uint64_t)s;
+        }
       }
     }
   }
@@ -499,7 +541,11 @@ int fs_validate_and_build(fs_plan *p, uint64_t n, const uint32_t *gens, int d, i
         uint64_t R = n, units = 0, rem = target;
         for (int k = 0; k < L - 1; ++k) {
           const uint64_t gk = gens[k], top = R / gk;
-          const uint64_t *Ck = &CW[(size_t)k * N1], *Uk = &p->U[(size_t)k * N1];
+          const uint64_t *Ck = &CW[(size_t)k * N1];
+          // U[k][r] (level 0 compact: r = n - x g_1 is stored at x)
+          auto Uat = [&](uint64_t rr) -> uint64_t {
+            return k == 0 ? p->U[(n - rr) / gens[0]] : p->U[(size_t)c.u0_len + (size_t)(k - 1) * N1 + rr];
+          };
           // cost of the subtrees with a_k >= x is Ck[R - x gk] (nonincreasing in x): the
           // largest x whose subtrees a_k >= x cost more than rem holds the boundary
           uint64_t lo = 0, hi = top + 1;
@@ -509,7 +555,7 @@ int fs_validate_and_build(fs_plan *p, uint64_t n, const uint32_t *gens, int d, i
           }
           if (lo < top) {
             rem -= Ck[R - (lo + 1) * gk];
-            units += Uk[R - (lo + 1) * gk];
+            units += Uat(R - (lo + 1) * gk);
           }
           R -= lo * gk;
         }
@@ -746,6 +792,7 @@ uint64_t host_count_tables_slice(const fs_plan *p, const KT &ktab, fs::Lane<D> &
       uint32_t A = st.A;
       const uint32_t kk = st.k;
       uint32_t cum = 0;  // advances taken (skip form), else 2 per pair
+      uint32_t gsum = 0;  // the kernel's 32-bit group sum (folded into 64 bits per group)
       for (uint32_t v = 0; v < G / 2; ++v) {
         const uint32_t *w = W + h;
         h = w[0] / 4u;
@@ -754,10 +801,11 @@ uint64_t host_count_tables_slice(const fs_plan *p, const KT &ktab, fs::Lane<D> &
         x2 = x2 > 0 ? x2 : 0;
         A += w[3];
         const uint32_t c1 = skip ? cum + w[4] : 2u * v + 1u, c2 = skip ? cum + w[5] : 2u * v + 2u;
-        if (c1 <= kk) n += (uint32_t)(((uint64_t)(uint32_t)x1 * c.mhi) >> 32);
-        if (c2 <= kk) n += (uint32_t)(((uint64_t)(uint32_t)x2 * c.mhi) >> 32);
+        if (c1 <= kk) gsum += (uint32_t)(((uint64_t)(uint32_t)x1 * c.mhi) >> 32);
+        if (c2 <= kk) gsum += (uint32_t)(((uint64_t)(uint32_t)x2 * c.mhi) >> 32);
         cum = c2;
       }
+      n += gsum;
       st.rho = (h - c.cadv2_off) / (8u * ew);
       st.A = A;
       st.k = kk > cum ? kk - cum : 0u;
@@ -874,13 +922,15 @@ void host_model_d(const fs_plan *p, const KT &ktab, HostSink &sink, uint64_t *sl
     if (ALPHA && p->consumer == FS_CONSUMER_COUNT &&
         (p->ex.tail == FS_TAIL_SKIP_OFF || p->ex.tail == FS_TAIL_SKIP_PAPER)) {
       const bool paper = p->ex.tail == FS_TAIL_SKIP_PAPER;
-      uint32_t cnt = 0;
+      uint64_t cnt = 0;
       fs::enter_candidates<D>(st, c);
       while (!fs::needs_refill<D, ALPHA>(st, budget)) {
+        uint32_t step_cnt = 0;  // the kernel's 32-bit per-iteration counter
         if (paper)
-          fs::fast_step_cand<D, true>(st, c, ktab, budget, cnt);
+          fs::fast_step_cand<D, true>(st, c, ktab, budget, step_cnt);
         else
-          fs::fast_step_cand<D, false>(st, c, ktab, budget, cnt);
+          fs::fast_step_cand<D, false>(st, c, ktab, budget, step_cnt);
+        cnt += step_cnt;
         fs::sync_k<D, ALPHA>(st, budget);
         if (fs::needs_slow<D>(st, budget)) {
           fs::slow_step<D, true, ALPHA>(st, c, ktab, budget);
@@ -902,7 +952,7 @@ void host_model_d(const fs_plan *p, const KT &ktab, HostSink &sink, uint64_t *sl
       }
       while (!fs::needs_refill<D, ALPHA>(st, budget)) {
         if (count_only) {  // the kernels' count-only closed step
-          uint32_t cnt = 0;
+          uint64_t cnt = 0;
           fs::fast_step_count_closed<D>(st, c, ktab, cnt);
           ns.n += cnt;
         } else {

@@ -134,7 +134,9 @@ fs::Div fs_make_div(uint32_t g);
 // kernel launchers (fs_kernels.cu); return FS_OK or an error
 int fs_launch(fs_plan *p, int consumer, int B, const fs::KParams &kp_template, cudaStream_t stream);
 int fs_occupancy_grid(fs_plan *p, int consumer, int B, uint32_t *grid_out);
-int fs_launch_hist_finalize(const fs::KParams &kp, cudaStream_t stream);
+// closed-tail histogram finalize (1 or 3 launches); scratch: fs_hist_finalize_scratch() u64s
+int fs_launch_hist_finalize(const fs::KParams &kp, unsigned long long *scratch, cudaStream_t stream, int *launches);
+uint64_t fs_hist_finalize_scratch(uint64_t hist_len, uint32_t dstride);
 // builds p->starts_dev on p->stream (node-unit plans with L >= 1; skipped when too large)
 int fs_build_slice_starts(fs_plan *p);
 extern unsigned long long g_fs_total_launches;

@@ -95,6 +95,11 @@ struct Inner {
 };
 
 // ---------------------------------------------------------------- consumers
+// Per-lane row counter of the count consumers.  32 bits inside one inner-loop iteration only:
+// it is folded into the lane's 64-bit total after every iteration (a per-row step adds at most
+// 1 per step; a closed-tail group at most FS_CC_GROUP nodes' rows, which the plan bounds below
+// 2^31, fs_host.cu; the t2/t3 ascend tables add < 2^16).  Node entries, whose rows are
+// unbounded, go straight to the 64-bit total.
 template <int D>
 struct EmitCount {
   uint32_t n;
@@ -1008,34 +1013,6 @@ __global__ void __launch_bounds__(kBlock, (CONS == kConsRowsAny || CONS == FS_CO
     const bool need = alive && needs_refill<D, ALPHA>(st, budget);
     const unsigned needm = __ballot_sync(kFull, need);
     if (needm) {
-      if (need) {
-        if (COUNTLIKE) {
-          acc += e_count.n;
-          e_count.n = 0;
-        } else if (HISTLIKE) {
-          const uint32_t rows = CONS == kConsHistClosed ? e_hcl.n : e_hist.n;
-          e_hist.n = 0;
-          e_hcl.n = 0;
-          if (P.hist_smem && rows) {
-            // overflow guard: every 2^30 rows added to this CTA, drain the u32 bins (or the
-            // difference array, as sign-extended values) to global memory
-            const uint32_t old = atomicAdd(&hist_guard, rows);
-            if ((old >> 30) != ((old + rows) >> 30)) {
-              if (CONS == kConsHistClosed) {
-                for (uint32_t i = 0; i < P.diff_len * hrep; ++i) {
-                  const int32_t v = (int32_t)atomicExch(&hist_s[i], 0u);
-                  if (v) atomicAdd(&P.diff_out[i / hrep], (unsigned long long)(long long)v);
-                }
-              } else {
-                for (uint32_t i = 0; i < P.hist_len; ++i) {
-                  const uint32_t v = atomicExch(&hist_s[i], 0u);
-                  if (v) atomicAdd(&P.hist_out[i], (unsigned long long)v);
-                }
-              }
-            }
-          }
-        }
-      }
       const int leader = __ffs(needm) - 1;
       unsigned long long base = 0;
       if (lane == leader) base = atomicAdd(P.queue, (unsigned long long)__popc(needm));
@@ -1056,7 +1033,7 @@ __global__ void __launch_bounds__(kBlock, (CONS == kConsRowsAny || CONS == FS_CO
             if (CAND) enter_candidates<D>(st, c);
             sync_k<D, ALPHA>(st, budget);
             if (CONS == FS_CONSUMER_ROWS) e_rows.start((u - P.unit0) * (uint64_t)EmitRows<D, B>::kRB);
-            if (cfast) e_count.n += take_entry_rows<D>(st, c);
+            if (cfast) acc += take_entry_rows<D>(st, c);
             if (t2fast || t2h) t2_sync<D>(st, c, t2base, t2a, q2);
             if (t3fast) t3_sync<D>(st, c, t3base, t3a, q3);
             if (hfast) take_entry_hist<D>(st, c, e_hcl);
@@ -1112,7 +1089,7 @@ __global__ void __launch_bounds__(kBlock, (CONS == kConsRowsAny || CONS == FS_CO
         if (CONS == FS_CONSUMER_COUNT) {
           fast_step<D, NEED_AD, ALPHA>(st, c, kt, budget, e_count);
         } else if (CONS == kConsCountClosed) {
-          fast_step_count_closed<D>(st, c, kt, e_count.n);
+          fast_step_count_closed<D>(st, c, kt, acc);
         } else if (CONS == kConsCountSkipOff) {
           fast_step_cand<D, false>(st, c, kt, budget, e_count.n);
         } else if (CONS == kConsCountSkipPaper) {
@@ -1159,7 +1136,7 @@ __global__ void __launch_bounds__(kBlock, (CONS == kConsRowsAny || CONS == FS_CO
           slow_step<D, NEED_AD, ALPHA>(st, c, kt, budget);
           if (CAND) enter_candidates<D>(st, c);
           sync_k<D, ALPHA>(st, budget);
-          if (cfast) e_count.n += take_entry_rows<D>(st, c);
+          if (cfast) acc += take_entry_rows<D>(st, c);
           if (t2fast || t2h) t2_sync<D>(st, c, t2base, t2a, q2);
           if (t3fast) t3_sync<D>(st, c, t3base, t3a, q3);
           }
@@ -1169,6 +1146,37 @@ __global__ void __launch_bounds__(kBlock, (CONS == kConsRowsAny || CONS == FS_CO
         if (CONS == FS_CONSUMER_ROWS) {
           warp_flush(e_rows.pend, e_rows.pend_soff, e_rows.pend_goff, e_rows.pend_len, warp_stage, P.rows_out, wslot);
           warp_flush(fin, fin_soff, fin_goff, fin_len, warp_stage, P.rows_out, wslot);
+        }
+      }
+      if (COUNTLIKE) {  // fold the iteration's 32-bit count into the lane's 64-bit total
+        acc += e_count.n;
+        e_count.n = 0;
+      }
+      if (HISTLIKE && P.hist_smem) {
+        // overflow guard of the 32-bit shared bins / difference array: the rows added by the
+        // warp this iteration (an upper bound of any bin's change) are summed per CTA, and
+        // every 2^30 of them the bins are drained to global memory (as sign-extended values
+        // for the difference array).  The plan bounds one iteration's rows per CTA far below
+        // 2^30 (fs_capi.cu), so no bin can pass 2^31 between drains.
+        const uint32_t mine = CONS == kConsHistClosed ? e_hcl.n : e_hist.n;
+        e_hist.n = 0;
+        e_hcl.n = 0;
+        const uint32_t wsum = __reduce_add_sync(kFull, mine);
+        if (lane == 0 && wsum) {
+          const uint32_t old = atomicAdd(&hist_guard, wsum);
+          if ((old >> 30) != ((old + wsum) >> 30)) {
+            if (CONS == kConsHistClosed) {
+              for (uint32_t i = 0; i < P.diff_len * hrep; ++i) {
+                const int32_t v = (int32_t)atomicExch(&hist_s[i], 0u);
+                if (v) atomicAdd(&P.diff_out[i / hrep], (unsigned long long)(long long)v);
+              }
+            } else {
+              for (uint32_t i = 0; i < P.hist_len; ++i) {
+                const uint32_t v = atomicExch(&hist_s[i], 0u);
+                if (v) atomicAdd(&P.hist_out[i], (unsigned long long)v);
+              }
+            }
+          }
         }
       }
       if (ANYLIKE && e_any.hit) {

@@ -32,19 +32,33 @@ def _world():
     return 0, 1
 
 
+def _host_staged() -> bool:
+    """gloo (CPU tests, or several ranks sharing one GPU) reduces host tensors: device
+    partials are staged through the host; NCCL reduces them in place on the stream."""
+    dist = _dist()
+    return dist.get_backend() == "gloo"
+
+
+def _all_reduce(t, op):
+    dist = _dist()
+    if not (dist.is_available() and dist.is_initialized() and dist.get_world_size() > 1):
+        return t
+    if t.is_cuda and _host_staged():
+        h = t.cpu()
+        dist.all_reduce(h, op=op)
+        t.copy_(h)
+    else:
+        dist.all_reduce(t, op=op)
+    return t
+
+
 def combine_sum(t):
     """In-place all_reduce(SUM) of a partial count/histogram tensor (int64)."""
-    dist = _dist()
-    if dist.is_available() and dist.is_initialized() and dist.get_world_size() > 1:
-        dist.all_reduce(t, op=dist.ReduceOp.SUM)
-    return t
+    return _all_reduce(t, _dist().ReduceOp.SUM)
 
 
 def combine_max(t):
-    dist = _dist()
-    if dist.is_available() and dist.is_initialized() and dist.get_world_size() > 1:
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
-    return t
+    return _all_reduce(t, _dist().ReduceOp.MAX)
 
 
 def exclusive_offsets(counts: Sequence[int]) -> List[int]:
@@ -62,6 +76,8 @@ def gather_counts(local: int, device) -> List[int]:
     t = torch.tensor([int(local)], dtype=torch.int64, device=device)
     if not (dist.is_available() and dist.is_initialized()) or dist.get_world_size() == 1:
         return [int(local)]
+    if t.is_cuda and _host_staged():
+        t = t.cpu()
     outs = [torch.zeros_like(t) for _ in range(dist.get_world_size())]
     dist.all_gather(outs, t)
     return [int(x.item()) for x in outs]
@@ -87,37 +103,41 @@ def length_set(n: int, gens: Sequence[int], *, slice_units: int = 0):
     rank, world = _world()
     p = Plan(n, gens, L.FS_CONSUMER_HIST, device=torch.cuda.current_device(),
              stream=torch.cuda.current_stream().cuda_stream, rank=rank, world=world, slice_units=slice_units,
-             gen_order=L.FS_GENORDER_AUTO)
+             gen_order=L.FS_GENORDER_AUTO, tail=L.FS_TAIL_CLOSED)  # same configuration as fs_length_set
     h = torch.zeros(hist_len(n, gens), dtype=torch.int64, device="cuda")
     p.hist_async(h)
     return combine_sum(h)
 
 
-def any_pred(n: int, gens: Sequence[int], pred: int, arg: int) -> bool:
+def any_pred(n: int, gens: Sequence[int], pred: int, arg: int, *, slice_units: int = 0) -> bool:
     import torch
 
     rank, world = _world()
     p = Plan(n, gens, L.FS_CONSUMER_ANY, device=torch.cuda.current_device(),
-             stream=torch.cuda.current_stream().cuda_stream, rank=rank, world=world, gen_order=L.FS_GENORDER_AUTO,
-             tail=L.FS_TAIL_CLOSED)  # same configuration as fs_any
+             stream=torch.cuda.current_stream().cuda_stream, rank=rank, world=world, slice_units=slice_units,
+             gen_order=L.FS_GENORDER_AUTO, tail=L.FS_TAIL_CLOSED)  # same configuration as fs_any
     f = torch.zeros(1, dtype=torch.int32, device="cuda")
     p.any_async(pred, arg, f)
     return bool(combine_max(f).item())
 
 
-def enumerate_rows(n: int, gens: Sequence[int], B: int = 16, out=None) -> Tuple[int, int, "object"]:
+def enumerate_rows(n: int, gens: Sequence[int], B: int = 16, out=None, *, slice_units: int = 0,
+                   order: int = L.FS_ORDER_CANONICAL) -> Tuple[int, int, "object"]:
     """This rank's block of canonical rows.  Returns (global_offset, rows, tensor); the
     offsets are exchanged with one all_gather and checked against the DP partition."""
     import torch
 
     rank, world = _world()
     p = Plan(n, gens, L.FS_CONSUMER_ROWS, device=torch.cuda.current_device(),
-             stream=torch.cuda.current_stream().cuda_stream, rank=rank, world=world)
+             stream=torch.cuda.current_stream().cuda_stream, rank=rank, world=world, slice_units=slice_units,
+             order=order)
     info = p.info
     rows = info["row_end"] - info["row_begin"]
     if out is None:
         out = torch.empty((rows, len(gens)), dtype=torch.uint16 if B == 16 else torch.int32, device="cuda")
     p.enumerate_async(B, out, rows)
+    if order == L.FS_ORDER_ANY:
+        p.rows_check()  # the M2 cursors met exactly: every row of the block written once
     counts = gather_counts(rows, out.device)
     offs = exclusive_offsets(counts)
     if offs[rank] != info["row_begin"]:

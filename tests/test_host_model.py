@@ -286,3 +286,31 @@ def test_filtered_and_order_argument_checks():
     assert fn(1000, g, 3, 16, L.FS_PRED_LEN_EQ, 100, ctypes.c_void_p(8), 10, ctypes.byref(ex)) == L.FS_EINVAL
     names = [f for f, _ in L.ExecT._fields_]
     assert "rows_impl" in names and names.index("rows_impl") == names.index("gen_order") + 1
+
+
+def test_range_boundary_d3_plans():
+    """n + max g = 2^31 - 1 at d = 3 (SURVEY 8(c) edge battery): the level-0 DP table is
+    compact (floor(n / g_1) + 1 entries), so the plan exists when g_1 is large; the host model
+    of the closed-tail count (64-bit node counts) matches the oracle's congruence sum.  With
+    g_1 = 1 the level-0 table would need 2^31 entries: FS_ERANGE."""
+    n = 2 ** 31 - 1 - 1000
+    want = gf.count_d3(n, (1000, 1, 1))
+    p = Plan(n, (1, 1, 1000), tail=L.FS_TAIL_CLOSED, gen_order=L.FS_GENORDER_AUTO)
+    assert p.info["total_rows"] == want
+    assert host_model(n, (1, 1, 1000), tail=L.FS_TAIL_CLOSED, gen_order=L.FS_GENORDER_AUTO)["count"] == want
+    with pytest.raises(OverflowError):
+        Plan(n, (1, 1, 1000), gen_order=L.FS_GENORDER_GIVEN)
+    with pytest.raises(OverflowError):
+        Plan(n + 1, (1000, 1, 1))
+
+
+def test_host_model_group_counts_beyond_32_bits():
+    """The table-driven closed-tail count on the host in the kernel's counter widths (32-bit
+    group sums folded into 64 bits): one slice of (1,1,2) at n = 2^22 holds 4.4e12 rows."""
+    n = 2 ** 22
+    want = sum(n - 2 * x + 1 for x in range(n // 2 + 1))
+    assert want > 2 ** 32
+    for T in (0, 1 << 24):
+        r = host_model(n, (1, 1, 2), tail=L.FS_TAIL_CLOSED, slice_units=T)
+        assert r["count"] == want
+    assert host_model(100000, (1, 1, 1), tail=L.FS_TAIL_CLOSED, slice_units=1 << 24)["count"] == 5000150001

@@ -274,3 +274,21 @@ def test_golden_gf_large():
     assert max(range(len(h)), key=lambda i: h[i]) == 200 and h[200] == 1636210748
     h2 = gf.hist_u64(12000, W.C2L.gens)
     assert sha(hist_bytes(h2)) == "2ca42f377ddc1ad1e41fed67b2246c454a24da2ae7b4f0f2873f62c3179ca5a4"
+
+
+def test_count_pair_and_d3_vs_dp():
+    """oracle.gf.count_pair / count_d3 (linear-congruence counts) against the coin-change DP
+    and brute force, including non-coprime pairs, gcd not dividing n and n = 0."""
+    import random
+
+    rng = random.Random(7)
+    for _ in range(300):
+        a, b = rng.randint(1, 30), rng.randint(1, 30)
+        n = rng.randint(0, 400)
+        assert gf.count_pair(n, a, b) == gf.count(n, (a, b)) == sum(
+            1 for x in range(n // a + 1) if (n - a * x) % b == 0)
+    for _ in range(100):
+        g = tuple(rng.randint(1, 25) for _ in range(3))
+        n = rng.randint(0, 600)
+        assert gf.count_d3(n, g) == gf.count(n, g)
+    assert gf.count_pair(-1, 2, 3) == 0
