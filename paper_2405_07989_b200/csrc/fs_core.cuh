@@ -79,6 +79,9 @@ struct Consts {
   uint32_t cadv2_skip;   // 1: that table walks live nodes only (8 words per entry; NEXT-3)
   uint32_t t3_off;       // word offset of the count's two-level ascend table (0: none; fs_host.cu)
   uint32_t hadv_off;     // word offset of the histogram's 8-copy closed-tail table (0: none; fs_host.cu)
+  uint32_t qtab_off;     // word offset of the count's state-pair table (0: none; fs_host.cu)
+  uint32_t q1_off;       // word offset of its single-step table
+  uint32_t t2q_off;      // word offset of the count's one-level ascend table in state form (0: none)
   uint32_t radv_off;     // word offset of the materialise advance table (0: none; fs_host.cu):
                          //   4 words per rho {next | inc << 11, k0(next), ad0(next), 0}
   int32_t dl;            // t - s: change of a row's length from one valid a_{d-1} to the next

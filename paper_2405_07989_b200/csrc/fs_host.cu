@@ -247,7 +247,8 @@ int fs_validate_and_build(fs_plan *p, uint64_t n, const uint32_t *gens, int d, i
       const uint32_t cadv_off = ((uint32_t)p->ktab.size() + 3u) & ~3u;
       // (count: a group of FS_CC_GROUP nodes sums its rows in 32 bits before they are folded into
       // the lane's 64-bit total, so the plan requires FS_CC_GROUP nodes' rows < 2^31)
-      const bool group_fits = consumer != FS_CONSUMER_COUNT || (uint64_t)FS_CC_GROUP * (xmax / c.s + 1) < (1ull << 31);
+      const uint64_t kMaxGroup = FS_CC_GROUP > FS_CQ_GROUP ? FS_CC_GROUP : FS_CQ_GROUP;
+      const bool group_fits = consumer != FS_CONSUMER_COUNT || kMaxGroup * (xmax / c.s + 1) < (1ull << 31);
       if ((consumer == FS_CONSUMER_COUNT || want_hist) && e.tail == FS_TAIL_CLOSED && L >= 1 && c.s >= 2 &&
           group_fits && xmax * c.s < (1ull << 32) && c.q + 1u < (1u << (32 - fs::kCAdvShift)) &&
           4ull * cadv_off + 4ull * cw * c.gA + 16384ull <= (1ull << fs::kCAdvShift)) {
@@ -375,6 +376,110 @@ int fs_validate_and_build(fs_plan *p, uint64_t n, const uint32_t *gens, int d, i
             }
           }
           c.cadv2_off = c2o;
+        }
+        // Count, gcd(g_{d-1}, g_d) = 1: the STATE form.  With A = Q s + a (a = A mod s), a node's
+        // rows are floor((A - k0(rho)) / s) + 1 = Q + [a >= k0(rho)] (a - k0 + s lies in
+        // [1, 2s - 1]), and an advance moves (rho, a) to (next(rho), (a + inc) mod s) and Q up by
+        // floor((a + inc) / s) -- all functions of the state sigma = (rho, a).  One 16 B entry
+        // per state and copy serves K = FS_QK consecutive advances:
+        //   {link = address of sigma_K's entry (same copy), E_K, K D_K, 0}
+        // where node i of the K has rows Q + e_i, E_K = e_1 + .. + e_K and D_K is the quotient
+        // increment over the K advances: a lane keeping QK = K Q adds the K nodes' rows as
+        // QK + E_K (one predicated IADD3) and steps QK += K D_K -- no division, no multiply.
+        // 8 interleaved copies as above.  The jump table J[sigma][r - 1] =
+        // {128 sigma_r | D_r << 16, E_r}, r = 1..K-1, makes a run's remaining advance count a
+        // multiple of K at its entry (r of them taken at once), so each K-block of a group lies
+        // wholly inside the run or wholly past its end and one predicate masks it.
+#ifndef FS_NO_QTAB
+        if (c.cadv2_off != 0 && c.h == 1u && L >= 1 && (uint64_t)c.gA * c.s <= 384u) {
+#else
+        if (false) {
+#endif
+          constexpr uint32_t K = FS_QK;
+          const uint32_t S = c.gA * c.s;
+          struct St {
+            uint32_t sig, d, e;  // next state, quotient increment, rows offset of the new node
+          };
+          auto step_q = [&](uint32_t sig) {
+            const uint32_t rho = sig / c.s, a = sig % c.s;
+            const fs::Adv w = ar.step(rho, c);
+            const uint32_t a2 = a + w.inc, d = a2 / c.s, a1 = a2 % c.s;
+            return St{w.next * c.s + a1, d, d + (a1 >= w.k0 ? 1u : 0u)};
+          };
+          // r advances from sigma: (state, quotient increment D_r, E_r = sum of rows - r Q)
+          auto jump = [&](uint32_t sig, uint32_t r) {
+            St out{sig, 0u, 0u};
+            for (uint32_t i = 0; i < r; ++i) {
+              const St t = step_q(out.sig);
+              out.e += out.d + t.e;  // node i's rows: Q + (D so far) + its own offset
+              out.d += t.d;
+              out.sig = t.sig;
+            }
+            return out;
+          };
+          const uint32_t qo = ((uint32_t)p->ktab.size() + 3u) & ~3u;
+          const uint32_t q1o = qo + 32u * S;
+          const uint32_t need_end = q1o + 2u * (K - 1u) * S;
+          bool ok = 4ull * need_end + 16384ull <= (1ull << 16);
+          std::vector<uint32_t> qt(need_end - qo, 0u);
+          for (uint32_t sig = 0; sig < S && ok; ++sig) {
+            const St sk = jump(sig, K);
+            if ((uint64_t)K * sk.d >= (1ull << 16)) ok = false;
+            for (uint32_t j = 0; j < 8u; ++j) {
+              uint32_t *ent = &qt[4u * (8u * sig + j)];
+              ent[0] = 4u * qo + 16u * (8u * sk.sig + j);
+              ent[1] = sk.e;
+              ent[2] = K * sk.d;
+              ent[3] = 0u;
+            }
+            for (uint32_t r = 1; r < K; ++r) {
+              const St sr = jump(sig, r);
+              if (sr.d >= 65536u) ok = false;
+              qt[32u * S + 2u * ((K - 1u) * sig + r - 1u)] = (128u * sr.sig) | (sr.d << 16);
+              qt[32u * S + 2u * ((K - 1u) * sig + r - 1u) + 1u] = sr.e;
+            }
+          }
+          if (ok) {
+            p->ktab.resize(qo, 0u);
+            p->ktab.insert(p->ktab.end(), qt.begin(), qt.end());
+            c.qtab_off = qo;
+            c.q1_off = q1o;
+            // the one-level ascend in state form (L >= 2), keyed by (r, m): r = R_{L-1} mod g_L
+            // and m = floor(R_{L-1} / g_L) mod K.  The ascend moves r to r' = (r + g_{L-1}) mod g_L
+            // and the new run's a_L to floor(R_{L-1} / g_L) + dQ, whose residue mod K,
+            // j = (m + dQ) mod K, is the number of advances enter_q would take at once (when the
+            // budget covers the run); the entry holds the new run's first node plus those j
+            // advances, precomputed: {rel((r', j)) | dQ << 16, 128 sigma_j | Q_j << 16,
+            // rows of the j + 1 nodes, j}.
+            if (c.t2_off != 0) {
+              const uint32_t gL = gens[L - 1], gL1 = gens[L - 2];
+              const uint32_t t2qo = ((uint32_t)p->ktab.size() + 3u) & ~3u;
+              bool fits = 4ull * (t2qo + 4u * K * gL) + 16384ull <= (1ull << 16);
+              std::vector<uint32_t> tq(4u * K * gL, 0u);
+              for (uint32_t r = 0; r < gL && fits; ++r) {
+                const uint32_t R2 = r + gL1, dQ = R2 / gL, r2 = R2 % gL;
+                const uint32_t A0 = r2 / c.gA, rho0 = r2 % c.gA, Q0 = A0 / c.s, a0 = A0 % c.s;
+                const uint32_t sig0 = rho0 * c.s + a0, k0 = fs::k0_arith(rho0, c);
+                const uint32_t rows0 = Q0 + (a0 >= k0 ? 1u : 0u);
+                for (uint32_t m = 0; m < K; ++m) {
+                  const uint32_t jn = (m + dQ) % K;
+                  const St sj = jump(sig0, jn);
+                  const uint32_t Qj = Q0 + sj.d, rows = rows0 + jn * Q0 + sj.e;
+                  if (dQ >= 65536u || Qj >= 65536u || (uint64_t)K * (Qj + 65536u) >= (1ull << 32)) fits = false;
+                  uint32_t *ent = &tq[4u * (K * r + m)];
+                  ent[0] = (4u * t2qo + 16u * (K * r2 + jn)) | (dQ << 16);
+                  ent[1] = (128u * sj.sig) | (Qj << 16);
+                  ent[2] = rows;
+                  ent[3] = jn;
+                }
+              }
+              if (fits) {
+                p->ktab.resize(t2qo, 0u);
+                p->ktab.insert(p->ktab.end(), tq.begin(), tq.end());
+                c.t2q_off = t2qo;
+              }
+            }
+          }
         }
         // gcd(g_{d-1}, g_d) = h > 1: a level-L node whose residual h does not divide has no
         // factorization (the paper's common-divisor skip for the last two generators, P:174,
@@ -757,12 +862,34 @@ uint64_t host_count_tables_slice(const fs_plan *p, const KT &ktab, fs::Lane<D> &
   const fs::Consts &c = p->c;
   const uint32_t *W = p->ktab.data();
   constexpr int L = D - 2;
-  constexpr uint32_t G = FS_CC_GROUP;
+  const bool qform = c.qtab_off != 0;  // the kernel's state form (cq_group, enter_q, t2q_ascend)
+  const uint32_t G = qform ? FS_CQ_GROUP : FS_CC_GROUP;
+  const uint32_t t2off = qform ? c.t2q_off : c.t2_off;
   uint64_t n = 0;
+  uint32_t hq = 0, Q = 0;  // state form: word index of the lane's state entry, quotient
   auto take_entry = [&]() {
     const int32_t x = st.cur + (int32_t)c.s;
     st.cur = -1;
     n += fs::divq((uint32_t)(x > 0 ? x : 0), c.dvS);
+  };
+  constexpr uint32_t K = FS_QK;
+  // fs_kernels.cuh enter_q: the entered node (A, rho) as a state; r = st.k mod K advances now
+  auto enter_q_from = [&](uint32_t sig128, uint32_t q) {
+    const uint32_t r = st.k % K;
+    if (r) {
+      const uint32_t *w = W + c.q1_off + 2u * ((K - 1u) * (sig128 / 128u) + r - 1u);
+      n += (uint64_t)r * q + w[1];
+      q += w[0] >> 16;
+      sig128 = w[0] & 0xffffu;
+      st.k -= r;
+    }
+    Q = K * q;  // the group keeps QK = K Q
+    hq = c.qtab_off + (sig128 + 16u * j) / 4u;
+  };
+  auto enter_q = [&]() {
+    if (!qform) return;
+    const uint32_t q = fs::divq(st.A, c.dvS);
+    enter_q_from(128u * (st.rho * c.s + (st.A - q * c.s)), q);
   };
   uint32_t t2w = 0, q2 = 0, t3w = 0, q3 = 0;  // word indices of the t2 / t3 entries
   auto t2_sync = [&]() {
@@ -770,7 +897,8 @@ uint64_t host_count_tables_slice(const fs_plan *p, const KT &ktab, fs::Lane<D> &
       if (!c.t2_off) return;
       const uint32_t R1 = st.R[L - 2];
       q2 = fs::divq(R1, c.dv[L - 1]);
-      t2w = c.t2_off + 4u * (R1 - q2 * c.g[L - 1]);
+      const uint32_t r = R1 - q2 * c.g[L - 1];
+      t2w = t2off + (qform ? 4u * (K * r + (q2 & (K - 1u))) : 4u * r);
     }
   };
   auto t3_sync = [&]() {
@@ -784,15 +912,25 @@ uint64_t host_count_tables_slice(const fs_plan *p, const KT &ktab, fs::Lane<D> &
   take_entry();
   t2_sync();
   t3_sync();
+  enter_q();
   while (!fs::needs_refill<D, 1>(st, budget)) {
-    if constexpr (D >= 3) {  // cc_group2: G nodes, two per paired-table entry
+    uint32_t gsum = 0;  // the kernel's 32-bit group sum (folded into 64 bits per group)
+    if (qform) {  // cq_group: G nodes in blocks of K, one predicate per block (kk = 0 mod K)
+      const uint32_t kk = st.k;
+      for (uint32_t v = 0; v < G / K; ++v) {
+        const uint32_t *w = W + hq;
+        hq = w[0] / 4u;
+        if (K * v < kk) gsum += Q + w[1];  // Q holds K Q here
+        Q += w[2];
+      }
+      st.k = kk > G ? kk - G : 0u;
+    } else if constexpr (D >= 3) {  // cc_group2: G nodes, two per paired-table entry
       const bool skip = c.cadv2_skip != 0;
       const uint32_t ew = skip ? 8u : 4u;  // words per entry
       uint32_t h = c.cadv2_off + ew * (8u * st.rho + j);
       uint32_t A = st.A;
       const uint32_t kk = st.k;
       uint32_t cum = 0;  // advances taken (skip form), else 2 per pair
-      uint32_t gsum = 0;  // the kernel's 32-bit group sum (folded into 64 bits per group)
       for (uint32_t v = 0; v < G / 2; ++v) {
         const uint32_t *w = W + h;
         h = w[0] / 4u;
@@ -805,16 +943,16 @@ uint64_t host_count_tables_slice(const fs_plan *p, const KT &ktab, fs::Lane<D> &
         if (c2 <= kk) gsum += (uint32_t)(((uint64_t)(uint32_t)x2 * c.mhi) >> 32);
         cum = c2;
       }
-      n += gsum;
       st.rho = (h - c.cadv2_off) / (8u * ew);
       st.A = A;
       st.k = kk > cum ? kk - cum : 0u;
     }
+    n += gsum;
     fs::sync_k<D, 1>(st, budget);
     if (fs::needs_slow<D>(st, budget)) {
       bool done = false;
       if constexpr (D >= 4) {
-        if (c.t2_off && st.a[L - 2] > 0u) {  // t2_ascend
+        if (c.t2_off && st.a[L - 2] > 0u && (!qform || c.t2q_off)) {  // t2_ascend / t2q_ascend
           const uint32_t *w = W + t2w;
           t2w = (w[0] & 0xffffu) / 4u;
           q2 += w[0] >> 16;
@@ -822,12 +960,24 @@ uint64_t host_count_tables_slice(const fs_plan *p, const KT &ktab, fs::Lane<D> &
           st.R[L - 2] += c.g[L - 2];
           st.a[L - 1] = q2;
           st.lsum = st.lsum - 1u + q2;
-          st.rho = w[1] & 0xffffu;
-          st.A = w[1] >> 16;
           st.cur = -1;
-          n += w[2];
           budget -= 1u;
           fs::sync_k<D, 1>(st, budget);
+          if (qform && st.k == st.a[L - 1]) {  // t2q_ascend: entry node + j advances, precomputed
+            n += w[2];
+            Q = K * (w[1] >> 16);
+            hq = c.qtab_off + ((w[1] & 0xffffu) + 16u * j) / 4u;
+            st.k -= w[3];
+          } else if (qform) {  // the budget ends inside the run: the entry node, then enter_q
+            const uint32_t r2 = (t2w - t2off) / 4u / K;  // R_L of the new run's first node
+            const uint32_t A0 = r2 / c.gA, rho0 = r2 % c.gA, q0 = A0 / c.s, a0 = A0 % c.s;
+            n += q0 + (a0 >= ktab(rho0, c) ? 1u : 0u);
+            enter_q_from(128u * (rho0 * c.s + a0), q0);
+          } else {
+            st.rho = w[1] & 0xffffu;
+            st.A = w[1] >> 16;
+            n += w[2];
+          }
           done = true;
         }
       }
@@ -848,9 +998,10 @@ uint64_t host_count_tables_slice(const fs_plan *p, const KT &ktab, fs::Lane<D> &
           st.cur = -1;
           n += w[2] & 0xffffu;
           q2 = aL;
-          t2w = c.t2_off + 4u * (w[3] & 0xffffu);
+          t2w = t2off + (qform ? 4u * (K * (w[3] & 0xffffu) + (aL & (K - 1u))) : 4u * (w[3] & 0xffffu));
           budget -= 1u;
           fs::sync_k<D, 1>(st, budget);
+          enter_q();
           done = true;
         }
       }
@@ -860,6 +1011,7 @@ uint64_t host_count_tables_slice(const fs_plan *p, const KT &ktab, fs::Lane<D> &
         take_entry();
         t2_sync();
         t3_sync();
+        enter_q();
       }
     }
   }

@@ -16,11 +16,20 @@ constexpr int kBlock = 256;          // threads per persistent CTA
 #ifndef FS_CC_GROUP
 #define FS_CC_GROUP 16  // steps per group of the closed-tail count (cc_group)
 #endif
+#ifndef FS_QK
+// nodes per entry of the count's state-form table (cq_group; a power of two).  C3 (r2b/r2c):
+// K = 2: 9.45 ms, 4: 7.0 ms, 8: 5.0 ms (with 32-node groups)
+#define FS_QK 8
+#endif
+#ifndef FS_CQ_GROUP
+#define FS_CQ_GROUP 32  // nodes per group of the state-form count (C3: 16 -> 5.93, 32 -> 5.0, 64 -> 5.41 ms)
+#endif
 #ifndef FS_CC_MINB
-// __launch_bounds__ min blocks per SM of the closed-tail count kernel (d <= 9): 5 CTAs of 256
-// threads (<= 48 registers, no spills) hide more of the table walk's latency than 4 (C3:
-// 14.7 -> 13.8 ms); 6 spills.  Larger d keep the compiler's choice (no spills).
-#define FS_CC_MINB 5
+// __launch_bounds__ min blocks per SM of the closed-tail count kernel (d <= 9).  Round 1 (pair
+// table with umulhi): 5 CTAs of 256 threads (<= 48 registers) beat 4 (C3 14.7 -> 13.8 ms).  The
+// state-form walk (cq_group) needs a few more registers: at 5 it spills (10.66 ms), at 4 it does
+// not (9.07 ms, r2b).  Larger d keep the compiler's choice (no spills).
+#define FS_CC_MINB 4
 #endif
 // Materialise (M1) per-lane staging: two 64 B halves + room for one row spilling past them
 // (rows are <= 64 B); lane stride 196 B = 49 words (odd) so lanes at equal positions hit

@@ -568,14 +568,16 @@ __device__ __forceinline__ bool t2_can_ascend(const Lane<D> &st) {
   else
     return false;
 }
-template <int D>
+template <int D, bool QFORM = false>
 __device__ __forceinline__ void t2_sync(const Lane<D> &st, const Consts &c, uint32_t t2base, uint32_t &t2a,
                                         uint32_t &q2) {
   if constexpr (D >= 4) {
     constexpr int L = D - 2;
     const uint32_t R1 = st.R[L - 2];
     q2 = divq(R1, c.dv[L - 1]);
-    t2a = t2base + 16u * (R1 - q2 * c.g[L - 1]);
+    const uint32_t r = R1 - q2 * c.g[L - 1];
+    // state form (t2q): entries keyed by (r, q2 mod FS_QK)
+    t2a = t2base + (QFORM ? 16u * (FS_QK * r + (q2 & (FS_QK - 1u))) : 16u * r);
   }
 }
 template <int D>
@@ -619,7 +621,7 @@ __device__ __forceinline__ void t3_sync(const Lane<D> &st, const Consts &c, uint
     t3a = t3base + 16u * (R3 - q3 * c.g[L - 2]);
   }
 }
-template <int D>
+template <int D, bool QFORM = false>
 __device__ __forceinline__ void t3_ascend(Lane<D> &st, const Consts &c, uint32_t &t3a, uint32_t &q3, uint32_t t2base,
                                           uint32_t &t2a, uint32_t &q2, uint32_t &cnt) {
   if constexpr (D >= 5) {
@@ -639,7 +641,7 @@ __device__ __forceinline__ void t3_ascend(Lane<D> &st, const Consts &c, uint32_t
     st.cur = -1;  // the entry node's rows are taken here
     cnt += w.z & 0xffffu;
     q2 = aL;
-    t2a = t2base + 16u * (w.w & 0xffffu);
+    t2a = t2base + (QFORM ? 16u * (FS_QK * (w.w & 0xffffu) + (aL & (FS_QK - 1u))) : 16u * (w.w & 0xffffu));
   }
 }
 
@@ -659,6 +661,102 @@ __device__ __forceinline__ void t2_ascend_hist(Lane<D> &st, const Consts &c, uin
     st.rho = w.y & 0xffffu;
     st.A = w.y >> 16;
     st.cur = (int32_t)w.z;
+  }
+}
+
+// Count, STATE form (Consts::qtab_off, fs_host.cu): between groups a lane keeps its node as a
+// state sigma = (rho, A mod s) -- held as the shared address of its entry in the lane's copy of
+// the state table, in st.rho -- and K times its quotient, QK = K floor(A / s), in st.A (K =
+// FS_QK).  A node's rows are Q + e with e from the table, so a block of K advances costs one
+// LDS.128, one predicate, one predicated add (QK + E_K) and one add (QK += K D_K): no division,
+// no multiply.  enter_q converts the entered node (A, rho) to that form and takes the run's
+// first r = st.k mod K advances at once (jump table), so every later K-block lies wholly inside
+// the run or wholly past its end and one predicate masks it.
+template <int D>
+__device__ __forceinline__ void enter_q_from(Lane<D> &st, uint32_t sig128, uint32_t q, uint32_t qbase_lane,
+                                             uint32_t q1base, uint32_t &cnt) {
+  constexpr uint32_t K = FS_QK;
+  const uint32_t r = st.k & (K - 1u);
+  if (r) {
+    uint32_t w0, w1;
+    asm("ld.shared.v2.u32 {%0, %1}, [%2];"
+        : "=r"(w0), "=r"(w1)
+        : "r"(q1base + 8u * ((K - 1u) * (sig128 >> 7) + r - 1u)));
+    cnt += r * q + w1;
+    q += w0 >> 16;
+    sig128 = w0 & 0xffffu;
+    st.k -= r;  // applied to a_L and the budget by the next sync_k
+  }
+  st.rho = qbase_lane + sig128;
+  st.A = K * q;
+}
+
+template <int D>
+__device__ __forceinline__ void enter_q(Lane<D> &st, const Consts &c, uint32_t qbase_lane, uint32_t q1base,
+                                        uint32_t &cnt) {
+  const uint32_t q = divq(st.A, c.dvS);
+  enter_q_from<D>(st, 128u * (st.rho * c.s + (st.A - q * c.s)), q, qbase_lane, q1base, cnt);
+}
+
+template <int D, int G>
+__device__ __forceinline__ void cq_group(Lane<D> &st, uint32_t &cnt) {
+  constexpr uint32_t K = FS_QK;
+  static_assert(G % K == 0, "nodes per group must be a multiple of FS_QK");
+  uint32_t h = st.rho, QK = st.A;
+  const uint32_t kk = st.k;  // a multiple of K (enter_q)
+  uint32_t n = cnt;
+#pragma unroll
+  for (int v = 0; v < G / (int)K; ++v) {
+    uint32_t w0, w1, w2, w3;
+    asm("ld.shared.v4.u32 {%0, %1, %2, %3}, [%4];" : "=r"(w0), "=r"(w1), "=r"(w2), "=r"(w3) : "r"(h));
+    (void)w3;
+    h = w0;
+    // n += QK + E_K for a block inside the run
+    asm("{\n\t.reg .pred p;\n\t.reg .u32 t;\n\tsetp.lt.u32 p, %1, %2;\n\tadd.u32 t, %3, %4;\n\t@p add.u32 %0, %0, t;\n\t}"
+        : "+r"(n)
+        : "r"(K * (uint32_t)v), "r"(kk), "r"(QK), "r"(w1));
+    QK += w2;
+  }
+  cnt = n;
+  st.rho = h;
+  st.A = QK;
+  st.k = kk > (uint32_t)G ? kk - (uint32_t)G : 0u;
+}
+
+// The one-level ascend in state form (Consts::t2q_off), keyed by r = R_{L-1} mod g_L and
+// m = floor(R_{L-1} / g_L) mod K: the new run's first node plus the j = a_L mod K advances that
+// enter_q would take, precomputed (one LDS.128).  When the slice's budget ends inside the new run
+// (once per slice) the entry node is taken and enter_q runs with the budget's remainder instead.
+template <int D>
+__device__ __forceinline__ void t2q_ascend(Lane<D> &st, const Consts &c, uint32_t ktab_base, uint32_t t2base,
+                                           uint32_t &t2a, uint32_t &q2, uint32_t &budget, uint32_t qbase_lane,
+                                           uint32_t q1base, uint32_t &cnt) {
+  if constexpr (D >= 4) {
+    constexpr int L = D - 2;
+    constexpr uint32_t K = FS_QK;
+    const uint4 w = lds128(t2a);
+    t2a = w.x & ((1u << kCAdvShift) - 1u);
+    q2 += w.x >> 16;
+    st.a[L - 2] -= 1u;
+    st.R[L - 2] += c.g[L - 2];
+    st.a[L - 1] = q2;
+    st.cur = -1;
+    budget -= 1u;  // the entry node
+    sync_k<D, 1>(st, budget);
+    if (st.k == q2) {
+      cnt += w.z;
+      st.rho = qbase_lane + (w.y & 0xffffu);
+      st.A = K * (w.y >> 16);
+      st.k -= w.w;
+    } else {
+      const uint32_t r2 = (t2a - t2base) / (16u * K);  // R_L of the new run's first node
+      const uint32_t A0 = divq(r2, c.dvA), rho0 = r2 - A0 * c.gA;
+      const uint32_t q0 = divq(A0, c.dvS), a0 = A0 - q0 * c.s;
+      uint32_t k0;
+      asm("ld.shared.u32 %0, [%1];" : "=r"(k0) : "r"(ktab_base + 4u * rho0));  // k0 table
+      cnt += q0 + (a0 >= k0 ? 1u : 0u);
+      enter_q_from<D>(st, 128u * (rho0 * c.s + a0), q0, qbase_lane, q1base, cnt);
+    }
   }
 }
 
@@ -926,9 +1024,12 @@ __global__ void __launch_bounds__(kBlock, (CONS == kConsRowsAny || CONS == FS_CO
   // count-only group table (closed tail): its link words get the table's shared address
   const bool cfast = KTAB && CONS == kConsCountClosed && c.cadv_off != 0 && ktab_base < 16384u;
   const bool hfast = KTAB && CONS == kConsHistClosed && c.cadv_off != 0 && P.hist_smem && ktab_base < 16384u;
-  const bool t2fast = cfast && D >= 4 && c.t2_off != 0;
+  const bool qfast = cfast && c.qtab_off != 0;  // count in state form (cq_group)
+  const bool t2fast = cfast && D >= 4 && c.t2_off != 0 && (!qfast || c.t2q_off != 0);
   const bool t2h = hfast && D >= 4 && c.t2_off != 0;  // histogram: one-level ascend by table
-  const uint32_t t2base = ktab_base + 4u * c.t2_off;
+  const uint32_t t2base = ktab_base + 4u * (qfast ? c.t2q_off : c.t2_off);
+  const uint32_t qbase_lane = ktab_base + 4u * c.qtab_off + 16u * (threadIdx.x & 7u);
+  const uint32_t q1base = ktab_base + 4u * c.q1_off;
   uint32_t t2a = t2base, q2 = 0;  // count: ascend-table entry of r = R_{L-1} mod g_L, Q = R_{L-1} / g_L
   const bool t3fast = t2fast && D >= 5 && c.t3_off != 0;
   const uint32_t t3base = ktab_base + 4u * c.t3_off;
@@ -950,6 +1051,10 @@ __global__ void __launch_bounds__(kBlock, (CONS == kConsRowsAny || CONS == FS_CO
       v += ktab_base;
     if (cfast && c.t3_off != 0u && D >= 5 && i >= c.t3_off && i < c.t3_off + 4u * c.g[D >= 5 ? D - 4 : 0] &&
         ((i - c.t3_off) & 3u) == 0u)
+      v += ktab_base;
+    if (cfast && c.qtab_off != 0u && i >= c.qtab_off && i < c.q1_off && ((i - c.qtab_off) & 3u) == 0u) v += ktab_base;
+    if (cfast && c.t2q_off != 0u && D >= 4 && i >= c.t2q_off && i < c.t2q_off + 4u * FS_QK * c.g[D >= 4 ? D - 3 : 0] &&
+        ((i - c.t2q_off) & 3u) == 0u)
       v += ktab_base;
     ktab_s[i] = v;
   }
@@ -1034,8 +1139,10 @@ __global__ void __launch_bounds__(kBlock, (CONS == kConsRowsAny || CONS == FS_CO
             sync_k<D, ALPHA>(st, budget);
             if (CONS == FS_CONSUMER_ROWS) e_rows.start((u - P.unit0) * (uint64_t)EmitRows<D, B>::kRB);
             if (cfast) acc += take_entry_rows<D>(st, c);
-            if (t2fast || t2h) t2_sync<D>(st, c, t2base, t2a, q2);
+            if (qfast) t2_sync<D, true>(st, c, t2base, t2a, q2);
+            else if (t2fast || t2h) t2_sync<D>(st, c, t2base, t2a, q2);
             if (t3fast) t3_sync<D>(st, c, t3base, t3a, q3);
+            if (qfast) enter_q<D>(st, c, qbase_lane, q1base, e_count.n);
             if (hfast) take_entry_hist<D>(st, c, e_hcl);
           }
         }
@@ -1059,7 +1166,9 @@ __global__ void __launch_bounds__(kBlock, (CONS == kConsRowsAny || CONS == FS_CO
       const bool had = budget != 0;
       // UNROLL branch-free fast steps, then one (warp-uniform) check for lanes parked on an
       // ascend; the rare slow lanes run the generic successor step together.
-      if (CONS == kConsCountClosed && B == 32 && cfast && c.cadv2_off != 0u && (UNROLL % 2) == 0) {
+      if (CONS == kConsCountClosed && B == 16 && qfast) {
+        cq_group<D, FS_CQ_GROUP>(st, e_count.n);
+      } else if (CONS == kConsCountClosed && B == 32 && cfast && c.cadv2_off != 0u && (UNROLL % 2) == 0) {
         // (the count ignores B: its B = 32 instantiation is the live-node walk, Consts::cadv2_skip,
         // so the common kernel carries none of that code)
         cc_group2_skip<D, (UNROLL % 2) == 0 ? UNROLL : 2>(st, c, ktab_base + 4u * c.cadv2_off, e_count.n);
@@ -1121,24 +1230,34 @@ __global__ void __launch_bounds__(kBlock, (CONS == kConsRowsAny || CONS == FS_CO
       if (__any_sync(kFull, slow)) {
         if (slow) {
           if (t2fast && t2_can_ascend<D>(st)) {  // one-level ascend by table (count)
-            t2_ascend<D>(st, c, t2a, q2, e_count.n);
-            budget -= 1u;
-            sync_k<D, ALPHA>(st, budget);
+            if (qfast) {
+              t2q_ascend<D>(st, c, ktab_base, t2base, t2a, q2, budget, qbase_lane, q1base, e_count.n);
+            } else {
+              t2_ascend<D>(st, c, t2a, q2, e_count.n);
+              budget -= 1u;
+              sync_k<D, ALPHA>(st, budget);
+            }
           } else if (t2h && t2_can_ascend<D>(st)) {  // one-level ascend by table (histogram)
             t2_ascend_hist<D>(st, c, t2a, q2);
             budget -= 1u;
             sync_k<D, ALPHA>(st, budget);
           } else if (t3fast && t3_can_ascend<D>(st)) {  // two-level ascend by table (count)
-            t3_ascend<D>(st, c, t3a, q3, t2base, t2a, q2, e_count.n);
+            if (qfast)
+              t3_ascend<D, true>(st, c, t3a, q3, t2base, t2a, q2, e_count.n);
+            else
+              t3_ascend<D>(st, c, t3a, q3, t2base, t2a, q2, e_count.n);
             budget -= 1u;
             sync_k<D, ALPHA>(st, budget);
+            if (qfast) enter_q<D>(st, c, qbase_lane, q1base, e_count.n);
           } else {
           slow_step<D, NEED_AD, ALPHA>(st, c, kt, budget);
           if (CAND) enter_candidates<D>(st, c);
           sync_k<D, ALPHA>(st, budget);
           if (cfast) acc += take_entry_rows<D>(st, c);
-          if (t2fast || t2h) t2_sync<D>(st, c, t2base, t2a, q2);
+          if (qfast) t2_sync<D, true>(st, c, t2base, t2a, q2);
+          else if (t2fast || t2h) t2_sync<D>(st, c, t2base, t2a, q2);
           if (t3fast) t3_sync<D>(st, c, t3base, t3a, q3);
+          if (qfast) enter_q<D>(st, c, qbase_lane, q1base, e_count.n);
           }
           if (hfast) take_entry_hist<D>(st, c, e_hcl);
           if (CONS == FS_CONSUMER_ROWS && budget == 0) rows_slice_done(P, e_rows, fin, fin_soff, fin_goff, fin_len);
