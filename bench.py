@@ -125,6 +125,13 @@ def microbench():
 
 
 OPS_NODE_CLOSED = 8  # node entry (5) + closed-form row count floor(a*/s) + 1: max, mulhi, add (NEXT-1)
+# Closed-tail count in STATE form (fs_kernels.cuh cq_group; info["state_block"] = K > 0): the
+# level-L nodes of a run are walked K at a time through the (rho, A mod s) automaton table:
+OPS_BLOCK_STATE = 3  # per K-block: quotient step, masked row-count add, block mask (the table
+#                      load is an LSU op)
+OPS_RUN_STATE = 12   # per run (level-(L-1) node): one-level ascend (prefix/residual update, a_L),
+#                      budget/run-length min, entry rows add, state + quotient decode, run-length
+#                      remainder adjust
 
 
 OPS_NODE_HIST_CLOSED = 12  # closed-tail histogram: node entry (5) + rows (3) + first-row length (2) + two
@@ -139,6 +146,11 @@ def ops_model(info, closed: bool = False, hist: bool = False, any_: bool = False
     nodes = info["nodes_per_level"]
     L = info["level"]
     deep = sum(nodes[1:L]) if L >= 2 else 0
+    K = info.get("state_block", 0)
+    if closed and K and not hist and not any_:
+        runs = nodes[L - 1] if L >= 1 else 1
+        deep2 = sum(nodes[1:L - 1]) if L >= 3 else 0
+        return OPS_BLOCK_STATE * nodes[L] / K + OPS_RUN_STATE * runs + OPS_DEEP * deep2
     if closed:
         per = OPS_NODE_HIST_CLOSED if hist else OPS_NODE_ANY_CLOSED if any_ else OPS_NODE_CLOSED
         return per * nodes[L] + OPS_DEEP * deep
@@ -147,7 +159,8 @@ def ops_model(info, closed: bool = False, hist: bool = False, any_: bool = False
 
 OPS_CAND = 5  # one candidate of the paper's index-(d-1) loop: residue add, conditional subtract,
 #              zero test, accumulate, loop (SURVEY 8(d) c_step)
-OPS_MODEL_DOC = ("closed tail: 8 int ops per level-L node (entry 5 + closed-form row count 3) + 12 per "
+OPS_MODEL_DOC = ("closed tail, state form (the headline): 3 int ops per block of K level-L nodes + 12 per run "
+                 "(level-(L-1) node) + 12 per deeper node; closed tail, residue form: 8 per level-L node + 12 per "
                  "deeper node; per-row tail: 5 per node + 4 per row + 12 per deeper node; Skip ablations: "
                  "5 per candidate + 5 per node + 12 per deeper node (DESIGN.md section 6)")
 

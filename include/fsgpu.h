@@ -115,7 +115,13 @@ enum {
  *               per-lane shared-memory slot with 16 B stores and the warp copies all 32
  *               lanes' slots out with coalesced 16 B stores (row shapes whose batch is at
  *               most 112 B; others use the next kernel); FS_ROWS_STAGED (1) -- the round-1
- *               kernels (per-step emission, per-lane linear staging / per-warp ring). */
+ *               kernels (per-step emission, per-lane linear staging / per-warp ring).
+ *   slicing     node-unit plans (count / hist / any) with slice_units = 0:
+ *               FS_SLICES_AUTO (0) cuts the rank's range into equal-COST slices at run starts
+ *               (cost = level-L nodes + a per-run weight; guided: large slices first, small
+ *               ones last) when d >= 4 and the range holds many more runs than lanes, else into
+ *               equal node-count slices; FS_SLICES_COST (1) / FS_SLICES_UNIFORM (2) force one
+ *               of the two (tests).  Same results either way. */
 typedef struct {
     int device;
     void *cuda_stream;
@@ -127,13 +133,15 @@ typedef struct {
     int tail;
     int gen_order;
     int rows_impl;
-    int reserved[4];
+    int slicing;
+    int reserved[3];
 } fs_exec_t;
 
 enum { FS_ORDER_CANONICAL = 0, FS_ORDER_ANY = 1, FS_ORDER_INCREASING = 2 };
 enum { FS_TAIL_ROWS = 0, FS_TAIL_CLOSED = 1, FS_TAIL_SKIP_OFF = 2, FS_TAIL_SKIP_PAPER = 3 };
 enum { FS_GENORDER_GIVEN = 0, FS_GENORDER_AUTO = 1 };
 enum { FS_ROWS_BATCH = 0, FS_ROWS_STAGED = 1 };
+enum { FS_SLICES_AUTO = 0, FS_SLICES_COST = 1, FS_SLICES_UNIFORM = 2 };
 
 /* ---------------------------------------------------------------------------------
  * north_star entry points: current CUDA device, default stream, whole instance.
@@ -219,6 +227,9 @@ typedef struct {
     uint32_t grid, block;       /* persistent launch shape */
     uint64_t nodes_per_level[FS_MAX_D]; /* #prefixes (a_1..a_k) with residual >= 0, k = 0..L */
     uint64_t table_bytes;
+    uint32_t state_block;       /* count plans: level-L nodes per table step of the state-form
+                                   walk (FS_QK), 0 if the plan does not use it */
+    uint32_t cost_slices;       /* 1: equal-cost slices (slice-start table of two kernels) */
 } fs_plan_info_t;
 
 int fs_plan_create(uint64_t n, const uint32_t *gens, int d, int consumer, const fs_exec_t *ex,

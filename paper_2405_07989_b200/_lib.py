@@ -19,6 +19,7 @@ FS_ORDER_CANONICAL, FS_ORDER_ANY, FS_ORDER_INCREASING = 0, 1, 2
 FS_TAIL_ROWS, FS_TAIL_CLOSED, FS_TAIL_SKIP_OFF, FS_TAIL_SKIP_PAPER = 0, 1, 2, 3
 FS_GENORDER_GIVEN, FS_GENORDER_AUTO = 0, 1
 FS_ROWS_BATCH, FS_ROWS_STAGED = 0, 1
+FS_SLICES_AUTO, FS_SLICES_COST, FS_SLICES_UNIFORM = 0, 1, 2
 
 u64 = ctypes.c_uint64
 i64 = ctypes.c_int64
@@ -39,7 +40,8 @@ class ExecT(ctypes.Structure):
         ("tail", ctypes.c_int),
         ("gen_order", ctypes.c_int),
         ("rows_impl", ctypes.c_int),
-        ("reserved", ctypes.c_int * 4),
+        ("slicing", ctypes.c_int),
+        ("reserved", ctypes.c_int * 3),
     ]
 
 
@@ -62,6 +64,8 @@ class PlanInfoT(ctypes.Structure):
         ("block", ctypes.c_uint32),
         ("nodes_per_level", ctypes.c_uint64 * FS_MAX_D),
         ("table_bytes", ctypes.c_uint64),
+        ("state_block", ctypes.c_uint32),
+        ("cost_slices", ctypes.c_uint32),
     ]
 
 

@@ -40,6 +40,9 @@ fs::KParams base_params(const fs_plan *p) {
   kp.unit0 = p->unit_begin;
   kp.unit1 = p->unit_end;
   kp.T = p->T;
+  kp.gn0 = p->gn0;
+  kp.gn1 = p->gn1;
+  kp.cost_slices = p->cost_slices ? 1 : 0;
   kp.num_slices = p->num_slices;
   kp.num_claims = p->num_slices;
   kp.queue = p->scratch_dev;
@@ -128,6 +131,8 @@ int fs_plan_info(const fs_plan *p, fs_plan_info_t *info) {
   info->block = p->block;
   for (int i = 0; i < FS_MAX_D; ++i) info->nodes_per_level[i] = p->nodes_per_level[i];
   info->table_bytes = p->U.size() * 8 + p->ktab.size() * 4;
+  info->state_block = p->c.qtab_off ? (uint32_t)FS_QK : 0u;
+  info->cost_slices = p->cost_slices ? 1u : 0u;
   return FS_OK;
 }
 
@@ -503,6 +508,6 @@ int64_t fs_enumerate(uint64_t n, const uint32_t *gens, int d, int B, void *out_d
   return r;
 }
 
-uint64_t fsdbg_total_launches(void) { return g_fs_total_launches; }
+uint64_t fsdbg_total_launches(void) { return g_fs_total_launches.load(); }
 
 }  // extern "C"

@@ -329,6 +329,84 @@ FS_HD uint64_t unrank(Lane<D> &st, const Consts &c, const KT &kt, uint64_t u) {
   return u;
 }
 
+// Unit range [u, e) of slice `sl` of a rank's range [unit0, unit1).  Node-unit plans cut the
+// range in three phases (guided slices, fs_host.cu): n0 slices of 4T units, n1 of 2T, then slices
+// of T -- large slices while there is plenty of work (fewer refills), small ones at the end (a
+// short tail); row-unit plans and forced slice sizes use n0 = n1 = 0 (uniform T).
+FS_HD void slice_range(uint64_t unit0, uint64_t unit1, uint64_t T, uint64_t n0, uint64_t n1, uint64_t sl,
+                       uint64_t &u, uint64_t &e) {
+  uint64_t off, len;
+  if (sl < n0) {
+    off = sl * 4 * T;
+    len = 4 * T;
+  } else if (sl < n0 + n1) {
+    off = n0 * 4 * T + (sl - n0) * 2 * T;
+    len = 2 * T;
+  } else {
+    off = n0 * 4 * T + n1 * 2 * T + (sl - n0 - n1) * T;
+    len = T;
+  }
+  u = unit0 + off;
+  e = u + len < unit1 ? u + len : unit1;
+}
+
+// Equal-COST slicing (node-unit plans, L >= 2; fs_host.cu).  CW[k][r] = cost below a level-k
+// prefix with residual r: w_node per level-L node plus w_run per run (a level-(L-1) prefix: the
+// level-L nodes it holds plus its ascend), stored like U (level 0 compactly: entry x =
+// CW[0][n - x g_1]).  cost_boundary(target) is the node-unit index of the start of the run in
+// which the lex-ordered cumulative cost passes `target` (the total units for target >= total
+// cost); pre[0..L-1] receives that run's first node (a_L at its maximum).  Rank partitions and
+// slices both cut the lex order there, so every slice starts at a run start.
+template <int D>
+FS_HD uint64_t cost_boundary(const Consts &c, const uint64_t *CW, uint64_t target, uint32_t *pre) {
+  constexpr int L = D - 2;
+  uint64_t units = 0;
+  if constexpr (L >= 2) {
+    const uint64_t stride = (uint64_t)c.n + 1;
+    uint32_t R = c.n;
+    uint64_t rem = target;
+    if (target >= ldU(CW)) {  // past the end: no run
+      for (int k = 0; k < L; ++k) pre[k] = 0;
+      return ldU(c.U);
+    }
+#pragma unroll
+    for (int k = 0; k < L - 1; ++k) {
+      const uint64_t *Ck = k == 0 ? CW : CW + c.u0_len + (uint64_t)(k - 1) * stride;
+      const uint64_t *Uk = k == 0 ? c.U : c.U + c.u0_len + (uint64_t)(k - 1) * stride;
+      const uint32_t g = c.g[k];
+      const uint32_t top = divq(R, c.dv[k]);
+      // cost of the subtrees a_k >= x is Ck[R - x g] (nonincreasing in x): the largest x whose
+      // subtrees a_k >= x cost more than rem holds the boundary
+      uint32_t lo = 0, hi = top + 1;
+      while (hi - lo > 1) {
+        const uint32_t mid = (lo + hi) >> 1;
+        if (ldU(Ck + (k == 0 ? mid : R - mid * g)) > rem)
+          lo = mid;
+        else
+          hi = mid;
+      }
+      if (lo < top) {
+        rem -= ldU(Ck + (k == 0 ? lo + 1 : R - (lo + 1) * g));
+        units += ldU(Uk + (k == 0 ? lo + 1 : R - (lo + 1) * g));
+      }
+      R -= lo * g;
+      pre[k] = lo;
+    }
+    pre[L - 1] = divq(R, c.dv[L - 1]);  // the run's first node: a_L at its maximum
+  }
+  return units;
+}
+
+// Cost target of the start of slice j of an equal-cost guided slicing of [cb, ce): S0 slices
+// of 4c, S1 of 2c, then slices of c (S2 = S - S0 - S1 of them, c = (ce - cb) / (4 S2) when
+// 4 S0 + 2 S1 = 3 S2).
+FS_HD uint64_t cost_target(uint64_t cb, uint64_t ce, uint64_t S0, uint64_t S1, uint64_t S, uint64_t j) {
+  const uint64_t S2 = S - S0 - S1;
+  const uint64_t den = 4 * S0 + 2 * S1 + S2;
+  const uint64_t f = j < S0 ? 4 * j : j < S0 + S1 ? 4 * S0 + 2 * (j - S0) : 4 * S0 + 2 * S1 + (j - S0 - S1);
+  return cb + (uint64_t)((unsigned __int128)(ce - cb) * f / den);
+}
+
 // After unrank(): node-unit plans (alpha = 1) start at the node's entry, which is consumed
 // here (returns 1); row-unit plans (alpha = 0) skip to row `off` of the node (returns 0).
 template <int D, bool NEED_AD>

@@ -5,6 +5,7 @@
 // (P:196-200), device upload, and the host model used by CPU tests.
 #include <cuda_runtime.h>
 #include <stdint.h>
+#include <stdlib.h>
 #include <string.h>
 
 #include <algorithm>
@@ -612,62 +613,58 @@ int fs_validate_and_build(fs_plan *p, uint64_t n, const uint32_t *gens, int d, i
   }
 
   // W-way partition: contiguous ranges of the lex order (P:196-200 bounds, P:230-231 workers).
-  // Row plans: equal rows (each rank's output offset is then known a priori).  Node-unit
-  // plans: equal COST, cost = nodes + kRunCost x runs (a run = the level-L nodes under one
-  // (a_1..a_{L-1}); a run costs its group tail and ascend on top of its nodes -- fitted on C3
-  // per-rank timings: 12.8 node-equivalents per run), with boundaries at run starts.  Equal
-  // nodes left the lex-largest rank (short runs) 12 % slower than the mean at W = 8.
+  // Row plans: equal rows (each rank's output offset is then known a priori).  Node-unit plans
+  // with L >= 2: equal COST, cost = w_node per level-L node + w_run per run (a run = the level-L
+  // nodes under one (a_1..a_{L-1}), which costs its ascend and entry on top of its nodes), with
+  // boundaries at run starts (fs::cost_boundary).  The weights are per kernel: the residue-form
+  // kernels spend ~12 node-equivalents per run (a least-squares fit of round-1 per-rank C3
+  // timings); the state-form count (Consts::qtab_off) walks 8 nodes per table step, so a run's
+  // ascend weighs far more: 80 node-equivalents balanced the W = 8 ranks of C3 within 10 % (r2e:
+  // 12 -> 21 % spread, 40 -> 22 %, 80 -> 10 %, 160 -> 17 %).
   const uint64_t U = p->total_units;
   const uint64_t W = (uint64_t)e.world, r = (uint64_t)e.rank;
   p->unit_begin = (uint64_t)((u128)U * r / W);
   p->unit_end = (uint64_t)((u128)U * (r + 1) / W);
-  if (W > 1 && c.alpha == 1u && d >= 4 && !p->U.empty()) {
+  p->CW.clear();
+  p->cost_slices = false;
+  p->gn0 = p->gn1 = 0;
+  if (c.alpha == 1u && d >= 4 && !p->U.empty()) {
     const int L = d - 2;
-    const uint64_t N1 = n + 1;
-    constexpr uint64_t kRunCost = 12;
-    // CW[k][r]: cost below a prefix of length k (0-based positions < k fixed) with residual r
-    std::vector<uint64_t> CW((size_t)L * N1), arr(N1);
+    const uint64_t N1 = n + 1, X0 = c.u0_len;
+    uint64_t w_run = c.qtab_off ? 80 : 12;
+    if (const char *ev = getenv("FS_RUN_COST")) w_run = strtoull(ev, nullptr, 10);  // tuning experiments only
+    // CW (same layout as U): levels L-1 .. 1 in full, level 0 compactly
+    std::vector<uint64_t> arr(N1);
     for (uint64_t x = 0; x <= n; ++x) arr[x] = 1;  // one node
+    p->CW.assign((size_t)X0 + (size_t)(L - 1) * N1, 0);
     bool ok = true;
-    for (int k = L - 1; k >= 0 && ok; --k) {
+    for (int k = L - 1; k >= 1 && ok; --k) {
       const uint64_t gk = gens[k];
       for (uint64_t x = gk; x <= n; ++x) arr[x] += arr[x - gk];
       if (k == L - 1)
-        for (uint64_t x = 0; x <= n; ++x) arr[x] += kRunCost;  // each length-(L-1) prefix is a run
+        for (uint64_t x = 0; x <= n; ++x) arr[x] += w_run;  // each length-(L-1) prefix is a run
       for (uint64_t x = 0; x <= n; ++x)
         if (arr[x] >= (1ull << 62)) ok = false;
-      memcpy(&CW[(size_t)k * N1], arr.data(), N1 * 8);
+      memcpy(&p->CW[(size_t)X0 + (size_t)(k - 1) * N1], arr.data(), N1 * 8);
     }
-    if (ok) {
-      const uint64_t C = CW[n];  // CW[0][n]
-      // node-unit index of the start of the run where the cost before reaches `target`
-      auto boundary = [&](uint64_t target) -> uint64_t {
-        if (target >= C) return U;
-        uint64_t R = n, units = 0, rem = target;
-        for (int k = 0; k < L - 1; ++k) {
-          const uint64_t gk = gens[k], top = R / gk;
-          const uint64_t *Ck = &CW[(size_t)k * N1];
-          // U[k][r] (level 0 compact: r = n - x g_1 is stored at x)
-          auto Uat = [&](uint64_t rr) -> uint64_t {
-            return k == 0 ? p->U[(n - rr) / gens[0]] : p->U[(size_t)c.u0_len + (size_t)(k - 1) * N1 + rr];
-          };
-          // cost of the subtrees with a_k >= x is Ck[R - x gk] (nonincreasing in x): the
-          // largest x whose subtrees a_k >= x cost more than rem holds the boundary
-          uint64_t lo = 0, hi = top + 1;
-          while (hi - lo > 1) {
-            const uint64_t mid = (lo + hi) / 2;
-            if (Ck[R - mid * gk] > rem) lo = mid; else hi = mid;
-          }
-          if (lo < top) {
-            rem -= Ck[R - (lo + 1) * gk];
-            units += Uat(R - (lo + 1) * gk);
-          }
-          R -= lo * gk;
-        }
-        return units;  // the run (a_1..a_{L-1}) starts here
-      };
-      p->unit_begin = boundary((uint64_t)((u128)C * r / W));
-      p->unit_end = r + 1 == W ? U : boundary((uint64_t)((u128)C * (r + 1) / W));
+    uint64_t acc = 0;
+    for (uint64_t x = X0; x-- > 0 && ok;) {
+      acc += arr[n - x * gens[0]];
+      if (acc >= (1ull << 62)) ok = false;
+      p->CW[x] = acc;
+    }
+    if (!ok) {
+      p->CW.clear();
+    } else {
+      c.U = p->U.data();
+      const uint64_t C = p->CW[0];
+      uint32_t pre[FS_MAX_D];
+      p->cost_begin = (uint64_t)((u128)C * r / W);
+      p->cost_end = (uint64_t)((u128)C * (r + 1) / W);
+      if (W > 1) {
+        p->unit_begin = fs_host_cost_boundary(p, p->cost_begin, pre);
+        p->unit_end = r + 1 == W ? U : fs_host_cost_boundary(p, p->cost_end, pre);
+      }
     }
   }
   if (consumer == FS_CONSUMER_ROWS) {
@@ -687,7 +684,49 @@ int fs_validate_and_build(fs_plan *p, uint64_t n, const uint32_t *gens, int d, i
   if (consumer == FS_CONSUMER_ROWS) T = (T + 63) & ~63ull;  // slices start 128 B aligned
   p->T = T;
   p->num_slices = span ? ceil_div_u64(span, T) : 0;
+  if (!p->CW.empty() && e.slice_units == 0 && span && e.slicing != FS_SLICES_UNIFORM) {
+    // Equal-cost, guided slices (node units): the rank's cost range is cut at run starts into
+    // S0 slices of cost 4c (the first half), S1 of 2c (the next quarter) and S2 of c (the last
+    // quarter), S2 = 3 per resident lane.  Equal cost balances lanes whatever the lex region
+    // (runs are short where a_1 is large, long where it is small); the large early slices keep
+    // refills (claim + slice entry, ~100 warp instructions) rare, and when the last 4c slice is
+    // claimed there are still 6c of smaller slices per lane queued behind it.  A slice's first
+    // node prefix and its node count come from the slice-start table (fs_build_slice_starts).
+    // Slices are cut at run starts only, so this needs many more runs than lanes (C5, 231 runs of
+    // ~3300 nodes, keeps uniform node slices, which split runs: 0.07 ms vs 0.36 ms).
+    const uint64_t S2 = 3 * kTargetLanes;
+    const uint64_t runs_share = (uint64_t)((u128)p->nodes_per_level[d - 3] * (p->cost_end - p->cost_begin) /
+                                           std::max<uint64_t>(1, p->CW[0]));
+    // a slice's node count (< its cost + one run) must fit the kernel's 32-bit budget
+    const bool forced = e.slicing == FS_SLICES_COST;  // (tests: at any size, S2 <= runs / 2)
+    const uint64_t s2 = forced ? std::max<uint64_t>(1, std::min<uint64_t>(S2, runs_share / 2)) : S2;
+    // automatic: for the closed-tail kernels, whose per-run cost the weights model (the per-row
+    // kernels keep node slices: C3 per-row count 190 ms with them, 210 ms with cost slices)
+    const bool closed_kernel = e.tail == FS_TAIL_CLOSED && (consumer == FS_CONSUMER_COUNT || consumer == FS_CONSUMER_HIST);
+    if ((forced || (closed_kernel && runs_share >= 8 * kTargetLanes)) &&
+        (p->cost_end - p->cost_begin) / s2 + n + 1024 < (1ull << 31)) {
+      p->gn0 = s2 / 2;
+      p->gn1 = s2 / 2;
+      p->num_slices = p->gn0 + p->gn1 + s2;
+      p->cost_slices = true;
+      p->T = std::max<uint64_t>(1, span / p->num_slices);  // reported average
+    }
+  }
   return FS_OK;
+}
+
+uint64_t fs_host_cost_boundary(const fs_plan *p, uint64_t target, uint32_t *pre) {
+  fs::Consts c = p->c;
+  c.U = p->U.data();
+  switch (p->d) {
+#define FS_CASE(DD) \
+  case DD:          \
+    return fs::cost_boundary<DD>(c, p->CW.data(), target, pre);
+    FS_CASE(4) FS_CASE(5) FS_CASE(6) FS_CASE(7) FS_CASE(8) FS_CASE(9)
+    FS_CASE(10) FS_CASE(11) FS_CASE(12) FS_CASE(13) FS_CASE(14) FS_CASE(15) FS_CASE(16)
+#undef FS_CASE
+  }
+  return 0;
 }
 
 void fs_plan_free_device(fs_plan *p) {
@@ -696,6 +735,8 @@ void fs_plan_free_device(fs_plan *p) {
   cudaGetDevice(&prev);
   cudaSetDevice(p->device);
   if (p->U_dev) cudaFree(p->U_dev);
+  if (p->CW_dev) cudaFree(p->CW_dev);
+  p->CW_dev = nullptr;
   if (p->ktab_dev) cudaFree(p->ktab_dev);
   if (p->scratch_dev) cudaFree(p->scratch_dev);
   if (p->diff_dev) cudaFree(p->diff_dev);
@@ -733,6 +774,11 @@ int fs_plan_upload_impl(fs_plan *p) {
     if (cudaMalloc(&p->U_dev, p->U.size() * 8) != cudaSuccess) return FS_ENOMEM;
     if (cudaMemcpyAsync(p->U_dev, p->U.data(), p->U.size() * 8, cudaMemcpyHostToDevice, p->stream) !=
         cudaSuccess)
+      return FS_ECUDA;
+  }
+  if (p->cost_slices) {
+    if (cudaMalloc(&p->CW_dev, p->CW.size() * 8) != cudaSuccess) return FS_ENOMEM;
+    if (cudaMemcpyAsync(p->CW_dev, p->CW.data(), p->CW.size() * 8, cudaMemcpyHostToDevice, p->stream) != cudaSuccess)
       return FS_ECUDA;
   }
   if (!p->ktab.empty()) {
@@ -1061,8 +1107,24 @@ template <int D, int ALPHA, class KT>
 void host_model_d(const fs_plan *p, const KT &ktab, HostSink &sink, uint64_t *slice_counts, uint32_t *slice_first) {
   const Consts &c = p->c;
   for (uint64_t sl = 0; sl < p->num_slices; ++sl) {
-    uint64_t u = p->unit_begin + sl * p->T;
-    uint32_t budget = (uint32_t)std::min<uint64_t>(p->T, p->unit_end - u);
+    uint64_t u, e;
+    if (p->cost_slices) {  // the slice-start table's cost boundaries (fs_build_slice_starts)
+      uint32_t pre[FS_MAX_D];
+      const uint64_t S = p->num_slices;
+      u = sl == 0 ? p->unit_begin
+                  : fs_host_cost_boundary(p, fs::cost_target(p->cost_begin, p->cost_end, p->gn0, p->gn1, S, sl), pre);
+      e = sl + 1 == S ? p->unit_end
+                      : fs_host_cost_boundary(p, fs::cost_target(p->cost_begin, p->cost_end, p->gn0, p->gn1, S, sl + 1), pre);
+      if (e <= u) {  // an empty slice (two targets inside one run)
+        if (slice_counts) slice_counts[sl] = 0;
+        if (slice_first)
+          for (int i = 0; i < D; ++i) slice_first[sl * D + i] = 0xFFFFFFFFu;
+        continue;
+      }
+    } else {
+      fs::slice_range(p->unit_begin, p->unit_end, p->T, p->gn0, p->gn1, sl, u, e);
+    }
+    uint32_t budget = (uint32_t)(e - u);
     fs::Lane<D> st;
     uint64_t off = fs::unrank<D, true>(st, c, ktab, u);
     budget -= fs::position_in_node<D, true>(st, c, off);

@@ -5,6 +5,7 @@
 #include <cuda_runtime.h>
 #include <stdint.h>
 
+#include <atomic>
 #include <vector>
 
 #include "../../include/fsgpu.h"
@@ -62,7 +63,9 @@ constexpr int kConsCountSkipPaper = 8;    // internal consumer: count, Skip=pape
 struct KParams {
   Consts c;
   uint64_t unit0, unit1;     // this rank's unit range (global unit indices)
-  uint64_t T;                // units per slice
+  uint64_t T;                // units per slice (the last phase's, for guided slices)
+  uint64_t gn0, gn1;         // uniform slices: 0, 0 (node-space phases of slice_range, unused)
+  int cost_slices;           // slices from the slice-start table: L prefix words + node count
   uint64_t num_slices;
   uint64_t num_claims;       // num_slices, or the next power of two when claims are permuted
   uint32_t claim_bits;       // log2(num_claims) when permuted
@@ -117,6 +120,11 @@ struct fs_plan {
   uint64_t unit_begin = 0, unit_end = 0;
   uint64_t row_begin = 0, row_end = 0;
   uint64_t T = 1, num_slices = 0;
+  uint64_t gn0 = 0, gn1 = 0;  // cost slices: S0 slices of cost 4c, S1 of 2c, then c (else 0, 0)
+  std::vector<uint64_t> CW;   // cost tables (fs::cost_boundary; layout of U), node-unit plans, L >= 2
+  bool cost_slices = false;   // equal-cost guided slices: prefix + node count per slice in the table
+  uint64_t cost_begin = 0, cost_end = 0;  // this rank's cost range
+  uint64_t *CW_dev = nullptr;
   uint64_t hist_len = 0;
   uint64_t nodes_per_level[FS_MAX_D] = {0};
   // device side
@@ -134,6 +142,7 @@ struct fs_plan {
 };
 
 // host helpers (fs_host.cu)
+uint64_t fs_host_cost_boundary(const fs_plan *p, uint64_t target, uint32_t *pre);
 int fs_validate_and_build(fs_plan *p, uint64_t n, const uint32_t *gens, int d, int consumer,
                           const fs_exec_t *ex);
 int fs_plan_upload_impl(fs_plan *p);
@@ -148,7 +157,7 @@ int fs_launch_hist_finalize(const fs::KParams &kp, unsigned long long *scratch, 
 uint64_t fs_hist_finalize_scratch(uint64_t hist_len, uint32_t dstride);
 // builds p->starts_dev on p->stream (node-unit plans with L >= 1; skipped when too large)
 int fs_build_slice_starts(fs_plan *p);
-extern unsigned long long g_fs_total_launches;
+extern std::atomic<unsigned long long> g_fs_total_launches;  // launches enqueued by the library (all threads)
 // lockstep batch materialise kernel (fs_k_rowsb.cu)
 bool fs_rows_batch_supported(const fs_plan *p, int B);
 bool fs_rows_batch_shape_ok(int d);

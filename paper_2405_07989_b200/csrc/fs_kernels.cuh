@@ -42,8 +42,8 @@ constexpr unsigned kFull = 0xffffffffu;
 // units, the row offset inside the node; the residuals are re-derived -- the state unrank()
 // would produce.  Returns the offset (node units: 0, the slice starts at a node's entry).
 template <int D>
-__device__ __forceinline__ uint32_t starts_stride(const Consts &c) {
-  return (uint32_t)(D - 2) + (c.alpha ? 0u : 1u);
+__device__ __forceinline__ uint32_t starts_stride(const Consts &c, int cost_slices = 0) {
+  return (uint32_t)(D - 2) + (c.alpha && !cost_slices ? 0u : 1u);
 }
 template <int D, bool NEED_AD, class KT>
 __device__ __forceinline__ uint64_t start_from_table(Lane<D> &st, const Consts &c, const KT &kt, const uint32_t *p) {
@@ -66,6 +66,32 @@ __device__ __forceinline__ uint64_t start_from_table(Lane<D> &st, const Consts &
   return c.alpha ? 0u : __ldg(p + L);
 }
 
+// Equal-cost slices (KParams::cost_slices): one thread per slice finds the slice's first node
+// by a cost-space unrank (fs::cost_boundary, at a run start) and stores its prefix; the second
+// kernel stores each slice's node count (next start - this start) in word L.
+template <int D>
+__global__ void fs_slice_starts_cost_kernel(const KParams P, const uint64_t *CW, uint64_t cb, uint64_t ce,
+                                            uint32_t *out, unsigned long long *ustart) {
+  constexpr int L = D - 2;
+  for (uint64_t sl = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; sl < P.num_slices;
+       sl += (uint64_t)gridDim.x * blockDim.x) {
+    uint32_t pre[L > 0 ? L : 1];
+    const uint64_t u = cost_boundary<D>(P.c, CW, cost_target(cb, ce, P.gn0, P.gn1, P.num_slices, sl), pre);
+#pragma unroll
+    for (int k = 0; k < L; ++k) out[sl * (L + 1) + k] = pre[k];
+    ustart[sl] = u;
+  }
+}
+template <int D>
+__global__ void fs_slice_budgets_kernel(const KParams P, uint32_t *out, const unsigned long long *ustart) {
+  constexpr int L = D - 2;
+  for (uint64_t sl = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; sl < P.num_slices;
+       sl += (uint64_t)gridDim.x * blockDim.x) {
+    const uint64_t e = sl + 1 < P.num_slices ? ustart[sl + 1] : P.unit1;
+    out[sl * (L + 1) + L] = (uint32_t)(e - ustart[sl]);
+  }
+}
+
 // One thread per slice: unrank the slice's first unit and store the node prefix (plan setup).
 template <int D>
 __global__ void fs_slice_starts_kernel(const KParams P, uint32_t *out) {
@@ -75,7 +101,9 @@ __global__ void fs_slice_starts_kernel(const KParams P, uint32_t *out) {
        sl += (uint64_t)gridDim.x * blockDim.x) {
     Lane<D> st;
     KTabArith kt;
-    const uint64_t off = unrank<D, false>(st, P.c, kt, P.unit0 + sl * P.T);
+    uint64_t u, e;
+    slice_range(P.unit0, P.unit1, P.T, P.gn0, P.gn1, sl, u, e);
+    const uint64_t off = unrank<D, false>(st, P.c, kt, u);
 #pragma unroll
     for (int k = 0; k < L; ++k) out[sl * stride + k] = st.a[k];
     if (!P.c.alpha) out[sl * stride + L] = (uint32_t)off;
@@ -1128,12 +1156,18 @@ __global__ void __launch_bounds__(kBlock, (CONS == kConsRowsAny || CONS == FS_CO
           alive = false;
         } else {
           const uint64_t sl = P.permute ? bitrev_bits(idx, P.claim_bits) : idx;
-          if (sl < P.num_slices) {
-            const uint64_t u = P.unit0 + sl * P.T;
-            const uint64_t e = u + P.T < P.unit1 ? u + P.T : P.unit1;
-            budget = (uint32_t)(e - u);
-            const uint64_t off = P.starts ? start_from_table<D, NEED_AD>(st, c, kt, P.starts + sl * (uint64_t)starts_stride<D>(c))
-                                          : unrank<D, NEED_AD>(st, c, kt, u);
+          uint64_t u = 0, e = 0;
+          if (P.cost_slices) {  // equal-cost slices: node count from the slice-start table
+            if (sl < P.num_slices) e = __ldg(P.starts + sl * (uint64_t)(D - 2 + 1) + (D - 2));
+          } else if (sl < P.num_slices) {
+            slice_range(P.unit0, P.unit1, P.T, P.gn0, P.gn1, sl, u, e);
+            e -= u;
+          }
+          if (e != 0) {  // (an empty cost slice -- two targets inside one run -- is skipped)
+            budget = (uint32_t)e;
+            const uint64_t off =
+                P.starts ? start_from_table<D, NEED_AD>(st, c, kt, P.starts + sl * (uint64_t)starts_stride<D>(c, P.cost_slices))
+                         : unrank<D, NEED_AD>(st, c, kt, u);
             budget -= position_in_node<D, NEED_AD>(st, c, off);
             if (CAND) enter_candidates<D>(st, c);
             sync_k<D, ALPHA>(st, budget);

@@ -4,7 +4,7 @@
 #include "../../include/fsgpu.h"
 #include "fs_internal.h"
 
-unsigned long long g_fs_total_launches = 0;
+std::atomic<unsigned long long> g_fs_total_launches{0};
 
 int fs_dispatch_count(fs_plan *p, int B, const fs::KParams &kp, cudaStream_t s, bool q, uint32_t *g);
 int fs_dispatch_hist(fs_plan *p, int B, const fs::KParams &kp, cudaStream_t s, bool q, uint32_t *g);

@@ -18,7 +18,12 @@ from paper_2405_07989_b200 import workloads as W  # noqa: E402
 
 def build(name):
     """A callable launching the workload once."""
-    if name in ("c3count", "c3closed", "c5count", "c3auto", "c3autoclosed"):
+    if name.startswith("c3autoclosed_w"):  # rank r of a W-way partition: c3autoclosed_w8r0
+        world, rank = (int(x) for x in name[len("c3autoclosed_w"):].split("r"))
+        p = api.Plan(W.C3.n, W.C3.gens, L.FS_CONSUMER_COUNT, tail=1, gen_order=1, rank=rank, world=world)
+        out = torch.zeros(1, dtype=torch.int64, device="cuda")
+        fn = lambda: p.count_async(out)
+    elif name in ("c3count", "c3closed", "c5count", "c3auto", "c3autoclosed"):
         inst = W.C5 if name == "c5count" else W.C3
         p = api.Plan(inst.n, inst.gens, L.FS_CONSUMER_COUNT, tail=1 if "closed" in name else 0,
                      gen_order=1 if "auto" in name else 0)

@@ -445,8 +445,9 @@ def test_plan_async_and_launch_count():
         assert p.last_launches() == 1
     torch.cuda.synchronize()
     assert int(out.item()) == 681152
-    # 3 count kernels + the plan's one-time slice-start table (built at upload)
-    assert L.lib().fsdbg_total_launches() - before == 4
+    # 3 count kernels + the plan's one-time slice-start table (built at upload; two kernels
+    # for equal-cost slices)
+    assert L.lib().fsdbg_total_launches() - before == 3 + (2 if p.info["cost_slices"] else 1)
 
 
 def test_errors_on_gpu():
@@ -461,3 +462,26 @@ def test_errors_on_gpu():
     h = torch.empty(3, dtype=torch.int64, device="cuda")
     with pytest.raises(ValueError):  # hist_cap too small
         api.fs_length_set(100, (3, 5), hist=h)
+
+
+@pytest.mark.parametrize("inst", [i for i in ALL if len(i.gens) >= 4][:30], ids=ids)
+def test_cost_slices(oracle_mod, inst):
+    """Equal-cost slices forced at small sizes (automatic only when a rank holds many more runs
+    than lanes): slices cut at run starts by a cost-space unrank on the device, node counts
+    from the slice-start table, empty slices skipped -- count, histogram and any, both tails,
+    given and auto generator order, 1 and 3 ranks."""
+    n, g = inst.n, inst.gens
+    want = oracle.run(n, g, hist_len=oracle.hist_len_for(n, g))
+    C = L.FS_SLICES_COST
+    for go in (L.FS_GENORDER_GIVEN, L.FS_GENORDER_AUTO):
+        for tail in (L.FS_TAIL_ROWS, L.FS_TAIL_CLOSED):
+            assert api.fs_count_ex(n, g, tail=tail, gen_order=go, slicing=C) == want["count"]
+            parts = [api.fs_count_ex(n, g, rank=r, world=3, tail=tail, gen_order=go, slicing=C) for r in range(3)]
+            assert sum(parts) == want["count"]
+            h = api.fs_length_set_ex(n, g, tail=tail, gen_order=go, slicing=C)
+            assert hist_list(h, len(want["hist"])) == want["hist"]
+        lmax = max(i for i, v in enumerate(want["hist"]) if v) if want["count"] else 0
+        found, wit = api.fs_any_ex(n, g, L.FS_PRED_LEN_GE, lmax, tail=L.FS_TAIL_CLOSED, gen_order=go, slicing=C)
+        assert found == bool(want["count"])
+        if found:
+            assert sum(a * b for a, b in zip(wit, g)) == n and sum(wit) >= lmax
