@@ -52,6 +52,18 @@ uint32_t fsdbg_magic_div(uint32_t x, uint32_t g);
  * stores over `param` bytes (0 = 8 GiB) -> *result_out = GB/s (best of 5), *aux_out = bytes. */
 int fsdbg_microbench(int kind, uint64_t param, double *result_out, double *aux_out);
 
+/* Slice audit on the device (the bounds partition the lex order into
+ * disjoint slices, so every factorization belongs to exactly one of them): runs the plan's
+ * closed-tail count (tail = FS_TAIL_CLOSED, node-unit plan) and writes, besides the total to
+ * count_dev (device uint64[1]), every slice's row count to slice_counts_dev (device
+ * uint64[num_slices], zeroed first; an empty slice stays 0).  FS_EINVAL for other plans. */
+int fsdbg_count_slices(fs_plan *plan, uint64_t *count_dev, uint64_t *slice_counts_dev);
+
+/* Host computation of the plan's slicing: the first node-unit index of slice sl (uniform or
+ * equal-cost slices) in *unit_out and, for d >= 3, that node's prefix a_1..a_L (stream order)
+ * in prefix_out (uint32[d], may be NULL).  FS_EINVAL if sl >= num_slices. */
+int fsdbg_slice_start(const fs_plan *plan, uint64_t sl, uint64_t *unit_out, uint32_t *prefix_out);
+
 /* Device count of the launches the library made since load (all plans). */
 uint64_t fsdbg_total_launches(void);
 

@@ -177,3 +177,27 @@ def count_d3(n: int, gens: Sequence[int]) -> int:
     coin-change DP (count) would need O(n) memory and time."""
     g1, g2, g3 = (int(x) for x in gens)
     return sum(count_pair(n - x * g1, g2, g3) for x in range(n // g1 + 1))
+
+
+def prefix_ranker(n: int, gens: Sequence[int]):
+    """rows_before_prefix with the suffix tables computed once: returns rank(prefix) = the number
+    of factorizations lex-greater (decreasing-lex order) than every row that
+    starts with `prefix`, i.e. the canonical index of the first such row.  Rows lex-greater
+    agree with the prefix before some coordinate k and exceed it there:
+        rank(p) = sum_k sum_{y > p_k} |Z(R_k - y g_k, gens[k+1:])| = sum_k |Z(R_k - (p_k + 1) g_k, gens[k:])|
+    (R_k = n - sum_{j<k} p_j g_j; the second form sums the first over y by the coin recurrence)."""
+    S = suffix_tables(n, gens)
+
+    def rank(prefix: Sequence[int]) -> int:
+        R, before = n, 0
+        for k, x in enumerate(prefix):
+            g = int(gens[k])
+            r = R - (int(x) + 1) * g
+            if r >= 0:
+                before += S[k][r]
+            R -= int(x) * g
+            if R < 0:
+                raise ValueError("prefix overshoots n")
+        return before
+
+    return rank

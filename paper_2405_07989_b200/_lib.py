@@ -101,6 +101,8 @@ EXPORTS = {
     "fsdbg_magic": (ctypes.c_int, [ctypes.c_uint32, u32p, u32p]),
     "fsdbg_magic_div": (ctypes.c_uint32, [ctypes.c_uint32, ctypes.c_uint32]),
     "fsdbg_total_launches": (ctypes.c_uint64, []),
+    "fsdbg_count_slices": (ctypes.c_int, [vp, vp, vp]),
+    "fsdbg_slice_start": (ctypes.c_int, [vp, u64, u64p, u32p]),
     "fsdbg_microbench": (ctypes.c_int, [ctypes.c_int, u64, ctypes.POINTER(ctypes.c_double),
                                         ctypes.POINTER(ctypes.c_double)]),
 }

@@ -159,6 +159,44 @@ int fs_plan_count_async(fs_plan *p, uint64_t *count_dev) {
   return finish(p, fs_launch(p, cons, 16, kp, p->stream));
 }
 
+// Slice audit (include/fsgpu_debug.h): the closed-tail count with every slice's row count written
+// to slice_counts_dev[sl] (the lane that ran the slice stores it when the slice is complete).
+int fsdbg_count_slices(fs_plan *p, uint64_t *count_dev, uint64_t *slice_counts_dev) {
+  if (!count_dev || !slice_counts_dev) return FS_EINVAL;
+  if (!p || p->ex.tail != FS_TAIL_CLOSED || p->c.alpha != 1u) return FS_EINVAL;
+  int rc = prepare(p, false);
+  if (rc != FS_OK) return rc;
+  DeviceGuard g(p->device);
+  if (cudaMemsetAsync(count_dev, 0, 8, p->stream) != cudaSuccess) return FS_ECUDA;
+  if (p->num_slices &&
+      cudaMemsetAsync(slice_counts_dev, 0, p->num_slices * 8, p->stream) != cudaSuccess)
+    return FS_ECUDA;
+  fs::KParams kp = base_params(p);
+  kp.count_out = reinterpret_cast<unsigned long long *>(count_dev);
+  kp.slice_counts = reinterpret_cast<unsigned long long *>(slice_counts_dev);
+  return finish(p, fs_launch(p, fs::kConsCountClosed, 16, kp, p->stream));
+}
+
+// The first node-unit index of slice sl and that node's prefix a_1..a_L (host computation of the
+// plan's slicing: uniform, or equal-cost boundaries).
+int fsdbg_slice_start(const fs_plan *p, uint64_t sl, uint64_t *unit_out, uint32_t *prefix_out) {
+  if (!p || !unit_out || sl >= p->num_slices) return FS_EINVAL;
+  uint64_t u, e;
+  uint32_t pre[FS_MAX_D];
+  if (p->cost_slices) {
+    u = fs_host_cost_boundary(p, fs::cost_target(p->cost_begin, p->cost_end, p->gn0, p->gn1, p->num_slices, sl), pre);
+  } else {
+    fs::slice_range(p->unit_begin, p->unit_end, p->T, p->gn0, p->gn1, sl, u, e);
+  }
+  *unit_out = u;
+  if (prefix_out && p->d >= 3 && u < p->total_units) {
+    int64_t row = 0;
+    int rc = fsdbg_unrank(p, u, prefix_out, &row);
+    if (rc != FS_OK) return rc;
+  }
+  return FS_OK;
+}
+
 int fs_plan_hist_async(fs_plan *p, uint64_t *hist_dev, uint64_t hist_cap) {
   if (!p || !hist_dev || hist_cap < p->hist_len) return FS_EINVAL;
   int rc = prepare(p, false);
@@ -202,6 +240,8 @@ int fs_plan_any_async(fs_plan *p, int pred, uint64_t pred_arg, int *found_dev, u
   if (rc != FS_OK) return rc;
   DeviceGuard g(p->device);
   if (cudaMemsetAsync(found_dev, 0, 4, p->stream) != cudaSuccess) return FS_ECUDA;
+  // (a witness is written only when found; zeroed so a copy of it is always defined)
+  if (witness_dev && cudaMemsetAsync(witness_dev, 0, 4u * (size_t)p->d, p->stream) != cudaSuccess) return FS_ECUDA;
   fs::KParams kp = base_params(p);
   kp.pred = pred;
   kp.pred_arg = pred_arg;

@@ -101,6 +101,8 @@ struct KParams {
   uint64_t filt_arg;
   int count_only;
   const uint32_t *starts;
+  // audit (debug, count consumers with the closed tail): per-slice row counts, or nullptr
+  unsigned long long *slice_counts;
 };
 
 }  // namespace fs

@@ -484,6 +484,7 @@ struct EmitCompact {
       return;
     }
     flush(P, true);
+    __syncwarp();  // the ring's last rows were written by other lanes (cond), possibly without a flush
     const uint32_t r = rows();
     if (r == 0) return;
     const int lane = threadIdx.x & 31;
@@ -1113,6 +1114,8 @@ __global__ void __launch_bounds__(kBlock, (CONS == kConsRowsAny || CONS == FS_CO
   st.ad = 0;
   st.lsum = 0;
   st.k = st.kb = 0;
+  // state form: a lane without a slice still walks the table (masked) -- start it on a valid state
+  if (qfast) st.rho = qbase_lane;
   uint32_t budget = 0;
   bool alive = true;
   uint64_t acc = 0;
@@ -1142,9 +1145,17 @@ __global__ void __launch_bounds__(kBlock, (CONS == kConsRowsAny || CONS == FS_CO
   e_cmp.filt_arg = P.filt_arg;
   e_cmp.count_only = P.count_only != 0;
 
+  // slice audit (KParams::slice_counts, closed-tail count): the lane's current slice and its
+  // running total at the slice's start, in shared memory (touched at refills only)
+  __shared__ unsigned long long audit_s[CONS == kConsCountClosed ? 2 * kBlock : 1];
+  if (CONS == kConsCountClosed && P.slice_counts) audit_s[2 * threadIdx.x] = ~0ull;
   for (;;) {
     const bool need = alive && needs_refill<D, ALPHA>(st, budget);
     const unsigned needm = __ballot_sync(kFull, need);
+    if (CONS == kConsCountClosed && P.slice_counts && need) {  // the lane's slice is complete
+      const unsigned long long sl0 = audit_s[2 * threadIdx.x];
+      if (sl0 != ~0ull) P.slice_counts[sl0] = acc + e_count.n - audit_s[2 * threadIdx.x + 1];
+    }
     if (needm) {
       const int leader = __ffs(needm) - 1;
       unsigned long long base = 0;
@@ -1162,6 +1173,10 @@ __global__ void __launch_bounds__(kBlock, (CONS == kConsRowsAny || CONS == FS_CO
           } else if (sl < P.num_slices) {
             slice_range(P.unit0, P.unit1, P.T, P.gn0, P.gn1, sl, u, e);
             e -= u;
+          }
+          if (CONS == kConsCountClosed && P.slice_counts) {
+            audit_s[2 * threadIdx.x] = e != 0 ? sl : ~0ull;
+            audit_s[2 * threadIdx.x + 1] = acc + e_count.n;
           }
           if (e != 0) {  // (an empty cost slice -- two targets inside one run -- is skipped)
             budget = (uint32_t)e;

@@ -292,3 +292,22 @@ def test_count_pair_and_d3_vs_dp():
         n = rng.randint(0, 600)
         assert gf.count_d3(n, g) == gf.count(n, g)
     assert gf.count_pair(-1, 2, 3) == 0
+
+
+def test_prefix_ranker_vs_enumeration(oracle_mod):
+    """oracle.gf.prefix_ranker: for every prefix length, the canonical index of the first row
+    with that prefix equals its position in the nested-loop enumeration (and rows_before_prefix)."""
+    import random
+
+    rng = random.Random(3)
+    for _ in range(25):
+        d = rng.randint(2, 5)
+        g = tuple(rng.randint(1, 12) for _ in range(d))
+        n = rng.randint(0, 60)
+        rows = oracle.rows_as_tuples(oracle.rows(n, g, B=32), d, 32)
+        rank = gf.prefix_ranker(n, g)
+        for i, row in enumerate(rows):
+            for k in range(d + 1):
+                first = next(j for j, r in enumerate(rows) if r[:k] == row[:k])
+                assert rank(row[:k]) == first == gf.rows_before_prefix(n, g, row[:k])
+            assert rank(row) == i
