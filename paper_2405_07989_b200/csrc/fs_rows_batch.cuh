@@ -33,6 +33,14 @@ constexpr int cgcd(int a, int b) { return b == 0 ? a : cgcd(b, a % b); }
 #define FS_RB_BLOCK 128  // threads per CTA of the batch kernel (measured: 128 > 192 > 256)
 #endif
 constexpr int kRbBlock = FS_RB_BLOCK;
+#ifndef FS_RB_TMA
+// M1 / increasing order: per-lane bulk (TMA, cp.async.bulk) copies of each group's segment
+// instead of the warp's LDS/STG copy loop.  Measured on C2-XL (r2f): 4.87 ms with it vs 4.78 ms
+// without (and 640 B segments: 7.0 ms, fewer resident warps), so the copy instructions are not
+// what holds M1 at 0.83 of the copy peak; kept as an option, off by default.
+#define FS_RB_TMA 0
+#endif
+constexpr bool kRbTma = FS_RB_TMA != 0;
 
 #ifndef FS_RB_GMAX
 #define FS_RB_GMAX 320  // bytes per lane per flush group (upper bound)
@@ -308,6 +316,9 @@ __global__ void __launch_bounds__(kRbBlock, 1) fs_rows_batch_kernel(const KParam
     }
     __syncwarp();
     for (uint32_t grp = 0; grp < groups; ++grp) {
+      // M1 / increasing order with per-lane bulk copies: the previous group's copy must have
+      // read the lane's slot before the slot is overwritten
+      if (!ANY && kRbTma) asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");
 #pragma unroll 1
       for (int b = 0; b < G::NBUF; ++b) {
         uint32_t wd[G::BW];
@@ -338,6 +349,22 @@ __global__ void __launch_bounds__(kRbBlock, 1) fs_rows_batch_kernel(const KParam
 #pragma unroll
         for (int i = 0; i < G::BW / 4; ++i)
           sts128(myslot + bs * G::BB + 16u * i, wd[4 * i], wd[4 * i + 1], wd[4 * i + 2], wd[4 * i + 3]);
+      }
+      if (!ANY && kRbTma) {
+        // M1 / increasing order: each live lane's group is ONE contiguous segment of FG bytes at
+        // its slice's exact offset -- stored by the TMA engine with one bulk copy from the lane's
+        // slot (cp.async.bulk, 16 B-aligned, FG a multiple of 16) instead of the warp's LDS/STG
+        // copy loop; the fence orders the lane's st.shared before the async-proxy read.
+        if ((uint32_t)lane < nlive) {
+          unsigned char *gdst = dst0 + (uint64_t)lane * SS +
+                                (REV ? (P.T - (uint64_t)(grp + 1) * G::GR) * (uint64_t)G::RB : (uint64_t)grp * G::FG);
+          asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+          asm volatile("cp.async.bulk.global.shared::cta.bulk_group [%0], [%1], %2;" ::"l"(gdst), "r"(myslot),
+                       "n"(G::FG)
+                       : "memory");
+          asm volatile("cp.async.bulk.commit_group;" ::: "memory");
+        }
+        continue;
       }
       __syncwarp();
       if (G::kPhase && nlive == 32u) {  // every slot live: addresses by phase, no checks
@@ -383,6 +410,7 @@ __global__ void __launch_bounds__(kRbBlock, 1) fs_rows_batch_kernel(const KParam
       __syncwarp();
     }
   }
+  if (!ANY && kRbTma) asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");  // all copies complete
 }
 
 // The rank's ragged slice: canonical rows [unit0 + first, unit0 + first + rows) (fewer than
