@@ -136,6 +136,12 @@ OPS_RUN_STATE = 12   # per run (level-(L-1) node): one-level ascend (prefix/resi
 
 OPS_NODE_HIST_CLOSED = 12  # closed-tail histogram: node entry (5) + rows (3) + first-row length (2) + two
 #                            difference-array updates (2)
+# Closed-tail histogram in STATE form (fs_kernels.cuh hq_group; info["state_block"] = 8 for a
+# histogram plan): per level-L node two offset extracts, two base adds and the two
+# difference-array updates; per 8-node block the two base steps and the link; per run the
+# one-level ascend (12) plus the entered node's state and bases (one division, 10)
+OPS_NODE_HIST_STATE = 6
+OPS_RUN_HIST_STATE = 22
 OPS_NODE_ANY_CLOSED = 14   # closed-tail any: node entry (5) + rows (3) + a_d of the first row (2) + the
 #                            progression's extreme length (2) + compare/flag (2)
 
@@ -147,9 +153,12 @@ def ops_model(info, closed: bool = False, hist: bool = False, any_: bool = False
     L = info["level"]
     deep = sum(nodes[1:L]) if L >= 2 else 0
     K = info.get("state_block", 0)
-    if closed and K and not hist and not any_:
+    if closed and K and not any_:
         runs = nodes[L - 1] if L >= 1 else 1
         deep2 = sum(nodes[1:L - 1]) if L >= 3 else 0
+        if hist:
+            return (OPS_NODE_HIST_STATE * nodes[L] + OPS_BLOCK_STATE * nodes[L] / K + OPS_RUN_HIST_STATE * runs
+                    + OPS_DEEP * deep2)
         return OPS_BLOCK_STATE * nodes[L] / K + OPS_RUN_STATE * runs + OPS_DEEP * deep2
     if closed:
         per = OPS_NODE_HIST_CLOSED if hist else OPS_NODE_ANY_CLOSED if any_ else OPS_NODE_CLOSED
@@ -161,6 +170,7 @@ OPS_CAND = 5  # one candidate of the paper's index-(d-1) loop: residue add, cond
 #              zero test, accumulate, loop (SURVEY 8(d) c_step)
 OPS_MODEL_DOC = ("closed tail, state form (the headline): 3 int ops per block of K level-L nodes + 12 per run "
                  "(level-(L-1) node) + 12 per deeper node; closed tail, residue form: 8 per level-L node + 12 per "
+                 "deeper node; histogram, state form: 6 per level-L node + 3 per 8-node block + 22 per run + 12 per "
                  "deeper node; per-row tail: 5 per node + 4 per row + 12 per deeper node; Skip ablations: "
                  "5 per candidate + 5 per node + 12 per deeper node (DESIGN.md section 6)")
 
@@ -656,6 +666,10 @@ def extras(args, world, rank, local, dev, stream, peaks, peaks_kind, barrier, ma
         ("hist_auto_order", W.C4, L.FS_CONSUMER_HIST, {"gen_order": AUTO}, "C4 histogram, NEXT-2 order", 2),
         ("hist_auto_order_closed", W.C4, L.FS_CONSUMER_HIST, {"gen_order": AUTO, "tail": 1},
          "C4 histogram, NEXT-1 + NEXT-2 (fs_length_set default)", 3),
+        ("hist_auto_order_closed_residue", W.C4, L.FS_CONSUMER_HIST, {"gen_order": AUTO, "tail": 1, "walk": 1},
+         "C4 histogram, NEXT-1 + NEXT-2, residue-form walk (ablation of the state form)", 2),
+        ("count_auto_order_closed_residue", W.C3, L.FS_CONSUMER_COUNT, {"gen_order": AUTO, "tail": 1, "walk": 1},
+         "C3 count, NEXT-1 + NEXT-2, residue-form walk (ablation of the state form)", 2),
         ("count_closed_tail", W.C3, L.FS_CONSUMER_COUNT, {"tail": 1}, "C3 count, NEXT-1 closed tail", 3),
         ("count_auto_order", W.C3, L.FS_CONSUMER_COUNT, {"gen_order": AUTO}, "C3 count, NEXT-2 order", 3),
         ("count_auto_order_closed", W.C3, L.FS_CONSUMER_COUNT, {"gen_order": AUTO, "tail": 1},

@@ -134,7 +134,9 @@ typedef struct {
     int gen_order;
     int rows_impl;
     int slicing;
-    int reserved[3];
+    int walk;          /* FS_WALK_*: state-form table walks where they fit (auto), or the residue
+                          form (ablation: one table step per node) */
+    int reserved[2];
 } fs_exec_t;
 
 enum { FS_ORDER_CANONICAL = 0, FS_ORDER_ANY = 1, FS_ORDER_INCREASING = 2 };
@@ -142,6 +144,7 @@ enum { FS_TAIL_ROWS = 0, FS_TAIL_CLOSED = 1, FS_TAIL_SKIP_OFF = 2, FS_TAIL_SKIP_
 enum { FS_GENORDER_GIVEN = 0, FS_GENORDER_AUTO = 1 };
 enum { FS_ROWS_BATCH = 0, FS_ROWS_STAGED = 1 };
 enum { FS_SLICES_AUTO = 0, FS_SLICES_COST = 1, FS_SLICES_UNIFORM = 2 };
+enum { FS_WALK_AUTO = 0, FS_WALK_RESIDUE = 1 };
 
 /* ---------------------------------------------------------------------------------
  * north_star entry points: current CUDA device, default stream, whole instance.
@@ -227,8 +230,8 @@ typedef struct {
     uint32_t grid, block;       /* persistent launch shape */
     uint64_t nodes_per_level[FS_MAX_D]; /* #prefixes (a_1..a_k) with residual >= 0, k = 0..L */
     uint64_t table_bytes;
-    uint32_t state_block;       /* count plans: level-L nodes per table step of the state-form
-                                   walk (FS_QK), 0 if the plan does not use it */
+    uint32_t state_block;       /* count and histogram plans: level-L nodes per table step of the
+                                   state-form walk, 0 if the plan does not use it */
     uint32_t cost_slices;       /* 1: equal-cost slices (slice-start table of two kernels) */
 } fs_plan_info_t;
 

@@ -20,6 +20,7 @@ FS_TAIL_ROWS, FS_TAIL_CLOSED, FS_TAIL_SKIP_OFF, FS_TAIL_SKIP_PAPER = 0, 1, 2, 3
 FS_GENORDER_GIVEN, FS_GENORDER_AUTO = 0, 1
 FS_ROWS_BATCH, FS_ROWS_STAGED = 0, 1
 FS_SLICES_AUTO, FS_SLICES_COST, FS_SLICES_UNIFORM = 0, 1, 2
+FS_WALK_AUTO, FS_WALK_RESIDUE = 0, 1
 
 u64 = ctypes.c_uint64
 i64 = ctypes.c_int64
@@ -41,7 +42,8 @@ class ExecT(ctypes.Structure):
         ("gen_order", ctypes.c_int),
         ("rows_impl", ctypes.c_int),
         ("slicing", ctypes.c_int),
-        ("reserved", ctypes.c_int * 3),
+        ("walk", ctypes.c_int),
+        ("reserved", ctypes.c_int * 2),
     ]
 
 

@@ -20,7 +20,7 @@ def _torch():
 
 def _exec(device: Optional[int] = None, stream=None, rank: int = 0, world: int = 1,
           slice_units: int = 0, ctas_per_sm: int = 0, order: int = 0, tail: int = 0,
-          gen_order: int = 0, rows_impl: int = 0, slicing: int = 0) -> L.ExecT:
+          gen_order: int = 0, rows_impl: int = 0, slicing: int = 0, walk: int = 0) -> L.ExecT:
     ex = L.ExecT()
     ex.device = -1 if device is None else int(device)
     ex.cuda_stream = None if stream is None else ctypes.c_void_p(int(stream))
@@ -33,6 +33,7 @@ def _exec(device: Optional[int] = None, stream=None, rank: int = 0, world: int =
     ex.gen_order = int(gen_order)
     ex.rows_impl = int(rows_impl)
     ex.slicing = int(slicing)
+    ex.walk = int(walk)
     return ex
 
 
@@ -96,19 +97,22 @@ def fs_enumerate(n: int, gens: Sequence[int], B: int = 16, cap: Optional[int] = 
 
 # ------------------------------------------------------------------ _ex variants
 def fs_count_ex(n, gens, *, device=None, stream=None, rank=0, world=1, slice_units=0, ctas_per_sm=0,
-                tail=L.FS_TAIL_ROWS, gen_order=L.FS_GENORDER_GIVEN, slicing=L.FS_SLICES_AUTO) -> int:
+                tail=L.FS_TAIL_ROWS, gen_order=L.FS_GENORDER_GIVEN, slicing=L.FS_SLICES_AUTO, walk=L.FS_WALK_AUTO) -> int:
     g, d = L.gens_array(gens)
-    ex = _exec(device, _stream_handle(stream), rank, world, slice_units, ctas_per_sm, 0, tail, gen_order, 0, slicing)
+    ex = _exec(device, _stream_handle(stream), rank, world, slice_units, ctas_per_sm, 0, tail, gen_order, 0, slicing,
+               walk)
     out = ctypes.c_uint64(0)
     L.check(L.lib().fs_count_ex(int(n), g, d, ctypes.byref(ex), ctypes.byref(out)), "fs_count_ex")
     return int(out.value)
 
 
 def fs_length_set_ex(n, gens, hist=None, *, device=None, stream=None, rank=0, world=1, slice_units=0,
-                     ctas_per_sm=0, gen_order=L.FS_GENORDER_GIVEN, tail=L.FS_TAIL_ROWS, slicing=L.FS_SLICES_AUTO):
+                     ctas_per_sm=0, gen_order=L.FS_GENORDER_GIVEN, tail=L.FS_TAIL_ROWS, slicing=L.FS_SLICES_AUTO,
+                     walk=L.FS_WALK_AUTO):
     torch = _torch()
     g, d = L.gens_array(gens)
-    ex = _exec(device, _stream_handle(stream), rank, world, slice_units, ctas_per_sm, 0, tail, gen_order, 0, slicing)
+    ex = _exec(device, _stream_handle(stream), rank, world, slice_units, ctas_per_sm, 0, tail, gen_order, 0, slicing,
+               walk)
     if hist is None:
         hist = torch.empty(hist_len(n, gens), dtype=torch.int64,
                            device="cuda" if device is None else "cuda:%d" % device)
@@ -179,14 +183,14 @@ class Plan:
     def __init__(self, n: int, gens: Sequence[int], consumer: int = L.FS_CONSUMER_COUNT, *,
                  device: Optional[int] = None, stream=None, rank: int = 0, world: int = 1,
                  slice_units: int = 0, ctas_per_sm: int = 0, order: int = 0, tail: int = 0,
-                 gen_order: int = 0, rows_impl: int = 0, slicing: int = 0):
+                 gen_order: int = 0, rows_impl: int = 0, slicing: int = 0, walk: int = 0):
         self.n = int(n)
         self.gens = tuple(int(x) for x in gens)
         self.consumer = consumer
         g, d = L.gens_array(gens)
         self._stream = stream
         ex = _exec(device, _stream_handle(stream), rank, world, slice_units, ctas_per_sm, order, tail, gen_order,
-                   rows_impl, slicing)
+                   rows_impl, slicing, walk)
         h = ctypes.c_void_p()
         L.check(L.lib().fs_plan_create(self.n, g, d, int(consumer), ctypes.byref(ex), ctypes.byref(h)),
                 "fs_plan_create")

@@ -131,7 +131,9 @@ int fs_plan_info(const fs_plan *p, fs_plan_info_t *info) {
   info->block = p->block;
   for (int i = 0; i < FS_MAX_D; ++i) info->nodes_per_level[i] = p->nodes_per_level[i];
   info->table_bytes = p->U.size() * 8 + p->ktab.size() * 4;
-  info->state_block = p->c.qtab_off ? (uint32_t)FS_QK : 0u;
+  info->state_block = p->c.qtab_off ? (uint32_t)FS_QK
+                      : (p->consumer == FS_CONSUMER_HIST && p->ex.tail == FS_TAIL_CLOSED && p->d >= 2 &&
+                         fs_hist_closed_shape(p).hq) ? (uint32_t)FS_HK : 0u;
   info->cost_slices = p->cost_slices ? 1u : 0u;
   return FS_OK;
 }
@@ -207,16 +209,13 @@ int fs_plan_hist_async(fs_plan *p, uint64_t *hist_dev, uint64_t hist_cap) {
   kp.hist_out = reinterpret_cast<unsigned long long *>(hist_dev);
   if (p->ex.tail == FS_TAIL_CLOSED && p->d >= 2) {
     // closed tail: strided difference array + finalize (two or four launches)
-    kp.diff_len = (uint32_t)(p->hist_len + p->c.dstride);
-    // 32-bit shared difference bins only while one inner-loop iteration of a CTA (256 lanes x
-    // FS_CC_GROUP nodes, <= 2^29 at < 2^17 rows per node) changes a bin by less than the
-    // kernel's 2^30 drain guard, so a bin stays below 2^31; else 64-bit global atomics
-    const uint64_t max_node_rows = (p->n / p->c.gA) / p->c.s + 1;
-    kp.hist_smem = kp.diff_len <= fs::kHistSmemMax && max_node_rows < (1ull << 17) ? 1u : 0u;
-    // group-form kernels spread the shared updates over 32 lane-private copies (one bank
-    // each: no bank conflicts) when they fit
-    kp.hist_rep = (kp.hist_smem && p->c.cadv_off && (size_t)(kp.diff_len + 1) * FS_HIST_REP * 4 <= fs::kHistRepBytes)
-                      ? (uint32_t)FS_HIST_REP : 1u;
+    const fs_hist_shape hs = fs_hist_closed_shape(p);
+    kp.diff_len = hs.diff_len;
+    kp.hist_smem = hs.hist_smem;
+    kp.hist_rep = hs.hist_rep;
+    kp.hist_hq = hs.hq;
+    kp.diff_slen = hs.slen;
+    kp.diff_sbias = hs.sbias;
     const uint64_t scratch = fs_hist_finalize_scratch(p->hist_len, p->c.dstride);
     if (!p->diff_dev && cudaMalloc(&p->diff_dev, ((size_t)kp.diff_len + scratch) * 8) != cudaSuccess) return FS_ENOMEM;
     if (cudaMemsetAsync(p->diff_dev, 0, (size_t)kp.diff_len * 8, p->stream) != cudaSuccess) return FS_ECUDA;

@@ -82,6 +82,8 @@ struct Consts {
   uint32_t qtab_off;     // word offset of the count's state-pair table (0: none; fs_host.cu)
   uint32_t q1_off;       // word offset of its single-step table
   uint32_t t2q_off;      // word offset of the count's one-level ascend table in state form (0: none)
+  uint32_t hq_off;       // word offset of the histogram's state-form table (0: none; fs_host.cu)
+  uint32_t hq_bias;      // its difference-array index bias (s - 1: rowless nodes reach index -(s-1))
   uint32_t radv_off;     // word offset of the materialise advance table (0: none; fs_host.cu):
                          //   4 words per rho {next | inc << 11, k0(next), ad0(next), 0}
   int32_t dl;            // t - s: change of a row's length from one valid a_{d-1} to the next

@@ -83,6 +83,7 @@ int fs_validate_and_build(fs_plan *p, uint64_t n, const uint32_t *gens, int d, i
   if (ex) e = *ex;
   if (e.world <= 0) e.world = 1;
   if (e.rank < 0 || e.rank >= e.world) return FS_EINVAL;
+  if (e.walk != FS_WALK_AUTO && e.walk != FS_WALK_RESIDUE) return FS_EINVAL;
 
   p->n = n;
   p->d = d;
@@ -291,6 +292,83 @@ int fs_validate_and_build(fs_plan *p, uint64_t n, const uint32_t *gens, int d, i
             p->ktab.resize(ho, 0u);
             p->ktab.insert(p->ktab.end(), hv.begin(), hv.end());
           }
+          // Histogram, gcd(g_{d-1}, g_d) = 1: the STATE form (fs_kernels.cuh hq_group), the
+          // count's automaton (below) carrying each node's two difference-array indices.  A lane
+          // holds the NEXT node to take, as a state sigma = (rho, a = A mod s) with Q = A div s,
+          // and a base X = lsum_p + s Q, lsum_p = a_1 + .. + a_L of the node plus one (the
+          // node's predecessor in the run; an entered node is its run's first, a_L one below
+          // that virtual predecessor).  A node's rows are Q + [a >= k0(rho)] and node i of the
+          // next 8 (i = 0: the next node itself; D_i the quotient increment from it) has first-
+          // row length l0_i = lsum_p - (i + 1) + a*_i + ad0_i = X + o_i with
+          //   o_i = s D_i - (i + 1) + a_i - k0(rho_i) + ad0(rho_i)
+          // and lengths l0_i + j dl, j < rows (dl = t - s): +1 / -1 at two difference indices,
+          // with Y = X + Q dl,
+          //   dl > 0: +1 at X + o_i,                          -1 at Y + o_i + (D_i + e_i) dl
+          //   dl < 0: +1 at Y + o_i - (D_i + e_i - 1) |dl|,   -1 at X + o_i + |dl|
+          // (e_i = [a_i >= k0_i]); a node without rows (Q + D_i + e_i = 0) puts both at one
+          // index (net zero) -- the kernel's shared array has margins for them (hq_bias below
+          // 0, t + |dl| above the top length).  One entry per state serves 8 nodes, two 16 B
+          // vectors: {link0, dP, dM, link1} and the 8 nodes' offsets as signed bytes
+          // {P_0, M_0, P_1, M_1, ..} (index units; the kernel scales them by the 128 B index
+          // stride of the 32 lane-private copies), dP / dM the bases' steps over the 8 nodes in
+          // bytes, link0 / link1 the addresses of sigma_8's two vectors.  Vector v of
+          // (sigma, copy j) lives at byte 16 (C (2 sigma + (v xor (sigma mod 2))) + j), C = FS_HQ_COPIES.
+          if (c.h == 1u && L >= 1 && (uint64_t)c.gA * c.s <= FS_HQ_MAX_STATES && e.walk != FS_WALK_RESIDUE) {
+            constexpr uint32_t K = FS_HK, C = FS_HQ_COPIES;
+            static_assert(K == 8, "two 16 B vectors per entry: 8 nodes of two signed bytes");
+            const int64_t str = 4 * FS_HIST_REP;  // bytes between difference-array indices
+            const uint32_t S = c.gA * c.s;
+            const uint32_t hqo = ((uint32_t)p->ktab.size() + 3u) & ~3u;
+            std::vector<uint32_t> hq(8u * C * S, 0u);
+            // 16 B slot of vector v of (sigma, copy j): the two vectors swap places on odd
+            // states, so two lanes reading one copy hit the same bank group only half the time
+            auto hq_slot = [&](uint32_t sig, uint32_t v, uint32_t j) { return C * (2u * sig + (v ^ (sig & 1u))) + j; };
+            bool ok = true;
+            auto fits8 = [](int64_t x) { return x >= -128 && x <= 127; };
+            for (uint32_t sig = 0; sig < S && ok; ++sig) {
+              uint32_t rho = sig / c.s, a = sig % c.s;
+              int64_t D = 0;
+              uint32_t w[8] = {0};
+              for (uint32_t i = 0; i < K; ++i) {  // node i = sigma_i
+                const int64_t k0 = ar(rho, c), e = a >= (uint32_t)k0 ? 1 : 0;
+                const int64_t ad0 = ((uint64_t)k0 * c.gA + rho) / c.gB;
+                const int64_t o = (int64_t)c.s * D - (int64_t)(i + 1) + (int64_t)a - k0 + ad0;
+                int64_t P, M;
+                if (c.dl > 0) {
+                  P = o;
+                  M = o + (D + e) * c.dl;
+                } else {
+                  P = o - (D + e - 1) * (int64_t)(-c.dl);
+                  M = o + (int64_t)(-c.dl);
+                }
+                if (!fits8(P) || !fits8(M)) ok = false;
+                const uint32_t pm = (uint32_t)(uint8_t)(int8_t)P | ((uint32_t)(uint8_t)(int8_t)M << 8);
+                w[4 + i / 2] |= pm << (16 * (i % 2));
+                const fs::Adv st = ar.step(rho, c);  // to sigma_{i+1}
+                const uint32_t a2 = a + st.inc;
+                D += a2 / c.s;
+                a = a2 % c.s;
+                rho = st.next;
+              }
+              const int64_t dX = (int64_t)c.s * D - (int64_t)K, dY = dX + D * c.dl;
+              w[1] = (uint32_t)(int32_t)((c.dl > 0 ? dX : dY) * str);
+              w[2] = (uint32_t)(int32_t)((c.dl > 0 ? dY : dX) * str);
+              const uint32_t sigK = rho * c.s + a;
+              for (uint32_t j = 0; j < C; ++j) {
+                for (uint32_t v = 0; v < 2u; ++v)
+                  for (uint32_t q = 0; q < 4u; ++q) hq[4u * hq_slot(sig, v, j) + q] = w[4u * v + q];
+                // links to both vectors of sigma_8's entry (same copy)
+                hq[4u * hq_slot(sig, 0, j)] = 4u * hqo + 16u * hq_slot(sigK, 0, j);
+                hq[4u * hq_slot(sig, 0, j) + 3u] = 4u * hqo + 16u * hq_slot(sigK, 1, j);
+              }
+            }
+            if (ok) {
+              p->ktab.resize(hqo, 0u);
+              p->ktab.insert(p->ktab.end(), hq.begin(), hq.end());
+              c.hq_off = hqo;
+              c.hq_bias = c.s - 1u;
+            }
+          }
         }
         c.cadv_off = cadv_off;
         c.cadv_words = cw;
@@ -392,7 +470,7 @@ int fs_validate_and_build(fs_plan *p, uint64_t n, const uint32_t *gens, int d, i
         // multiple of K at its entry (r of them taken at once), so each K-block of a group lies
         // wholly inside the run or wholly past its end and one predicate masks it.
 #ifndef FS_NO_QTAB
-        if (c.cadv2_off != 0 && c.h == 1u && L >= 1 && (uint64_t)c.gA * c.s <= 384u) {
+        if (c.cadv2_off != 0 && c.h == 1u && L >= 1 && (uint64_t)c.gA * c.s <= 384u && e.walk != FS_WALK_RESIDUE) {
 #else
         if (false) {
 #endif
@@ -807,6 +885,8 @@ struct HostSink {
   uint64_t slice_rows = 0;
   std::vector<int64_t> diffv;
   int64_t *diff = nullptr;
+  std::vector<int64_t> hq_sh;  // state-form histogram: one lane-copy of the kernel's shared array
+  bool hq_bad = false;
   uint32_t first[FS_MAX_D];
   bool have_first = false;
   // any-predicate (fsdbg_host_any): pred_arg in the caller's coordinates; pred_arg_int with
@@ -898,6 +978,74 @@ struct HostNodeSink {
     }
   }
 };
+
+// The state-form histogram (fs_kernels.cuh hq_group / hq_tail / enter_h) replayed on the host
+// for one lane and one slice, reading the same table words (links are byte offsets from the
+// table start; copy j = lane mod FS_HQ_COPIES), with the kernel's shared index arithmetic: every
+// update lands in `sh` (one lane-copy of the shared array, index = address / stride), and the
+// replay fails (bad) if an address leaves the array or is not index-aligned.  Ascends take the
+// generic slow_step (the kernel's t2 ascend table is pinned separately).
+template <int D, class KT>
+void host_hist_tables_slice(const fs_plan *p, const KT &ktab, fs::Lane<D> &st, uint32_t &budget, uint32_t j,
+                            std::vector<int64_t> &sh, bool &bad) {
+  const fs::Consts &c = p->c;
+  const uint32_t *W = p->ktab.data();
+  constexpr int L = D - 2;
+  constexpr uint32_t K = FS_HK, C = FS_HQ_COPIES, STR = 4u * FS_HIST_REP;
+  uint32_t h = 0, h1 = 0, bP = 0, bM = 0;
+  auto upd = [&](uint32_t addr, int64_t v) {
+    // (the last index is the kernel's junk word for masked nodes: never a real update)
+    if (addr % STR != 0u || addr / STR + 1u >= sh.size()) {
+      bad = true;
+      return;
+    }
+    sh[addr / STR] += v;
+  };
+  // enter_h: the entered node (A, rho; entry unit not charged) becomes the next node to take,
+  // a_L and lsum those of its virtual predecessor (one more)
+  auto enter = [&]() {
+    if constexpr (L >= 1) {
+      st.a[L - 1] += 1u;
+      st.lsum += 1u;
+    }
+    st.cur = -1;
+    fs::sync_k<D, 1>(st, budget);
+    const uint32_t Q = st.A / c.s, a = st.A % c.s;
+    const uint32_t X = STR * (st.lsum + c.s * Q + c.hq_bias);
+    const uint32_t Y = X + STR * Q * (uint32_t)c.dl;
+    const uint32_t sig = st.rho * c.s + a;
+    h = c.hq_off + 4u * (C * (2u * sig + (sig & 1u)) + j);
+    h1 = c.hq_off + 4u * (C * (2u * sig + (1u - (sig & 1u))) + j);
+    bP = c.dl > 0 ? X : Y;
+    bM = c.dl > 0 ? Y : X;
+  };
+  enter();
+  while (!fs::needs_refill<D, 1>(st, budget)) {
+    const uint32_t kk = st.k;
+    for (uint32_t v = 0; v < FS_HQ_GROUP / K; ++v) {  // hq_group: masked 8-node blocks
+      if (kk <= K * v) break;
+      const uint32_t *w = W + h, *w1 = W + h1;
+      for (uint32_t i = 0; i < K; ++i) {
+        if (K * v + i >= kk) continue;  // masked (the kernel's junk word)
+        const uint32_t pm = w1[i / 2u] >> (16u * (i % 2u));
+        upd(bP + STR * (uint32_t)(int32_t)(int8_t)(pm & 0xffu), 1);
+        upd(bM + STR * (uint32_t)(int32_t)(int8_t)((pm >> 8) & 0xffu), -1);
+      }
+      h = w[0] / 4u;
+      h1 = w[3] / 4u;
+      bP += w[1];
+      bM += w[2];
+    }
+    st.k = kk > FS_HQ_GROUP ? kk - FS_HQ_GROUP : 0u;
+    fs::sync_k<D, 1>(st, budget);
+    if (!fs::needs_slow<D>(st, budget)) continue;
+    if (!fs::advance<D>(st, c)) {  // (a_L = 0: the ascend) end of stream
+      budget = 0;
+      break;
+    }
+    enter();
+  }
+}
 
 // The kernels' count-only closed tail with the tables (fs_kernels.cuh cc_group2, t2_ascend,
 // t3_ascend) replayed on the host for one lane, reading the same host table words: the link
@@ -1164,6 +1312,12 @@ void host_model_d(const fs_plan *p, const KT &ktab, HostSink &sink, uint64_t *sl
         budget = 0;
         st.cur = -1;
       }
+      if (sink.diff && !sink.hq_sh.empty()) {  // the kernel's state-form histogram
+        budget += 1u;  // (position_in_node charged the entry unit: enter_h takes it as a node)
+        host_hist_tables_slice<D>(p, ktab, st, budget, (uint32_t)(sl % FS_HQ_COPIES), sink.hq_sh, sink.hq_bad);
+        budget = 0;
+        st.cur = -1;
+      }
       while (!fs::needs_refill<D, ALPHA>(st, budget)) {
         if (count_only) {  // the kernels' count-only closed step
           uint64_t cnt = 0;
@@ -1236,6 +1390,8 @@ extern "C" int fsdbg_host_model(const fs_plan *p, uint64_t *count_out, uint64_t 
   if (closed_hist) {
     sink.diffv.assign(p->hist_len + p->c.dstride + 1, 0);
     sink.diff = sink.diffv.data();
+    const fs_hist_shape hs = fs_hist_closed_shape(p);
+    if (hs.hq) sink.hq_sh.assign(hs.slen, 0);
   }
   if (p->d == 1) {
     // one slice, one unit at most
@@ -1259,6 +1415,17 @@ extern "C" int fsdbg_host_model(const fs_plan *p, uint64_t *count_out, uint64_t 
       default:
         return FS_EINVAL;
     }
+  }
+  if (closed_hist && !sink.hq_sh.empty()) {  // the shared array's indices hq_bias + l; margins net to zero
+    const fs_hist_shape hs = fs_hist_closed_shape(p);
+    for (uint64_t i = 0; i < sink.hq_sh.size(); ++i) {
+      const int64_t l = (int64_t)i - (int64_t)hs.sbias;
+      if (l >= 0 && l < (int64_t)hs.diff_len)
+        sink.diff[l] += sink.hq_sh[i];
+      else if (sink.hq_sh[i] != 0)
+        sink.hq_bad = true;
+    }
+    if (sink.hq_bad) return FS_ERANGE;  // the replay left the kernel's shared array
   }
   if (closed_hist) {  // strided prefix sums of the difference array
     const uint64_t L = p->hist_len, S = p->c.dstride;
@@ -1350,3 +1517,30 @@ extern "C" int fsdbg_magic(uint32_t g, uint32_t *m_out, uint32_t *sh_out) {
 }
 
 extern "C" uint32_t fsdbg_magic_div(uint32_t x, uint32_t g) { return fs::divq(x, fs_make_div(g)); }
+
+// The closed-tail histogram's launch shape.  32-bit shared difference bins only while one
+// inner-loop iteration of a CTA (256 lanes x FS_CC_GROUP nodes, <= 2^29 at < 2^17 rows per node)
+// changes a bin by less than the kernel's 2^30 drain guard, so a bin stays below 2^31; else
+// 64-bit global atomics.  Group-form kernels spread the shared updates over 32 lane-private
+// copies (one bank each: no bank conflicts) when they fit; the state form (hq_group) needs
+// them (its table offsets are pre-multiplied by the copies' index stride) and margins for
+// rowless nodes (shared index = length + hq_bias, up to the top length + t + dstride).
+fs_hist_shape fs_hist_closed_shape(const fs_plan *p) {
+  fs_hist_shape h{};
+  h.diff_len = (uint32_t)(p->hist_len + p->c.dstride);
+  const uint64_t max_node_rows = (p->n / p->c.gA) / (p->c.s ? p->c.s : 1) + 1;
+  h.hist_smem = h.diff_len <= fs::kHistSmemMax && max_node_rows < (1ull << 17) ? 1u : 0u;
+  h.hist_rep = (h.hist_smem && p->c.cadv_off && (size_t)(h.diff_len + 1) * FS_HIST_REP * 4 <= fs::kHistRepBytes)
+                   ? (uint32_t)FS_HIST_REP : 1u;
+  h.slen = h.diff_len + 1u;
+  h.sbias = 0;
+  // (+ 1: a junk index, the target of masked nodes)
+  const uint64_t slen_hq = (uint64_t)p->c.hq_bias + p->hist_len + p->c.t + p->c.dstride + 2;
+  if (p->c.hq_off && h.hist_rep == (uint32_t)FS_HIST_REP && slen_hq * FS_HIST_REP * 4 <= fs::kHistRepBytes) {
+    h.hq = 1;
+    h.slen = (uint32_t)slen_hq;
+    h.sbias = p->c.hq_bias;
+  }
+  return h;
+}
+

@@ -44,6 +44,18 @@ constexpr uint32_t kHistRepBytes = 49152; // lane-private difference-array copie
 #ifndef FS_HIST_REP
 #define FS_HIST_REP 32  // difference-array copies per CTA (lane l uses copy l mod FS_HIST_REP)
 #endif
+#ifndef FS_HK
+#define FS_HK 8  // advances per entry of the histogram's state-form table (hq_group)
+#endif
+#ifndef FS_HQ_COPIES
+#define FS_HQ_COPIES 4  // interleaved copies of that table (lane l reads copy l mod FS_HQ_COPIES)
+#endif
+#ifndef FS_HQ_GROUP
+#define FS_HQ_GROUP 16  // nodes per group of the state-form histogram (C4: 16 -> 18.8, 32 -> 19.1, 64 -> 23.4 ms)
+#endif
+#ifndef FS_HQ_MAX_STATES
+#define FS_HQ_MAX_STATES 512  // g_{d-1} s bound for that table (48 FS_HQ_COPIES bytes per state)
+#endif
 #ifndef FS_HC_MINB
 #define FS_HC_MINB 1  // __launch_bounds__ min blocks per SM of the closed-tail histogram kernel (d <= 9)
 #endif
@@ -92,6 +104,9 @@ struct KParams {
   unsigned long long *diff_out;
   uint32_t diff_len;
   uint32_t hist_rep;  // closed-tail histogram: 32 = one difference-array copy per lane (bank-private), else 1
+  uint32_t hist_hq;   // closed-tail histogram in state form (Consts::hq_off, hist_rep = FS_HIST_REP)
+  uint32_t diff_slen; // shared difference-array entries per copy (diff_len + 1, or with the state form's margins)
+  uint32_t diff_sbias;// shared index of global difference index 0 (0, or Consts::hq_bias)
   // node-unit plans: the prefix a_1..a_L of every slice's first node (num_slices x L words,
   // built once per plan by fs_build_slice_starts), so a refill is L independent loads instead
   // of the unrank's O(L log n) dependent ones; nullptr = unrank
@@ -157,6 +172,12 @@ int fs_occupancy_grid(fs_plan *p, int consumer, int B, uint32_t *grid_out);
 // closed-tail histogram finalize (1 or 3 launches); scratch: fs_hist_finalize_scratch() u64s
 int fs_launch_hist_finalize(const fs::KParams &kp, unsigned long long *scratch, cudaStream_t stream, int *launches);
 uint64_t fs_hist_finalize_scratch(uint64_t hist_len, uint32_t dstride);
+// closed-tail histogram launch shape (fs_plan_hist_async, and the host model that replays it):
+// global difference entries, whether the state form runs, and its shared entries per copy
+struct fs_hist_shape {
+  uint32_t diff_len, hist_smem, hist_rep, hq, slen, sbias;
+};
+fs_hist_shape fs_hist_closed_shape(const fs_plan *p);
 // builds p->starts_dev on p->stream (node-unit plans with L >= 1; skipped when too large)
 int fs_build_slice_starts(fs_plan *p);
 extern std::atomic<unsigned long long> g_fs_total_launches;  // launches enqueued by the library (all threads)

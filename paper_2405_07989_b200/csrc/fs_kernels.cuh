@@ -1018,6 +1018,89 @@ __device__ __forceinline__ void hc_group_dl(Lane<D> &st, const Consts &c, uint32
     hc_group<D, G, PACKED, 0>(st, c, tab, k, nrows);
 }
 
+// Length histogram, STATE form (Consts::hq_off, KParams::hist_hq; table layout in fs_host.cu).
+// Between groups a lane keeps its node as the shared address of its state's entry (st.rho) and
+// two byte addresses in its lane-private difference-array copy, bP (st.A) and bM: node i of
+// the next 8 puts +1 at bP + 128 P_i and -1 at bM + 128 M_i, with P_i / M_i signed bytes of the
+// entry's second vector -- per node two byte extracts (PRMT), two scaled adds (LEA) and two
+// shared reductions; no division, no multiply.  Blocks past the end of the run or slice are
+// skipped (one branch per block); inside the last block the nodes past the end are sent to
+// the lane's junk word (two selects per node), so no node needs a separate tail pass.
+template <int I>
+__device__ __forceinline__ void hq_node(uint32_t bP, uint32_t bM, uint32_t w, bool ok, uint32_t junk) {
+  constexpr uint32_t kSelP = (2u * I) | ((2u * I + 8u) << 4) | ((2u * I + 8u) << 8) | ((2u * I + 8u) << 12);
+  constexpr uint32_t kSelM = (2u * I + 1u) | ((2u * I + 9u) << 4) | ((2u * I + 9u) << 8) | ((2u * I + 9u) << 12);
+  uint32_t p, m;
+  asm("prmt.b32 %0, %1, 0, %2;" : "=r"(p) : "r"(w), "n"(kSelP));  // sign-extended byte 2I
+  asm("prmt.b32 %0, %1, 0, %2;" : "=r"(m) : "r"(w), "n"(kSelM));  // sign-extended byte 2I + 1
+  const uint32_t aP = ok ? bP + (p << 7) : junk;
+  const uint32_t aM = ok ? bM + (m << 7) : junk;
+  asm volatile("red.shared.add.u32 [%0], %1;" ::"r"(aP), "r"(1u) : "memory");
+  asm volatile("red.shared.add.u32 [%0], %1;" ::"r"(aM), "r"(0xffffffffu) : "memory");
+}
+
+template <int D, int G>
+__device__ __forceinline__ void hq_group(Lane<D> &st, uint32_t &h1, uint32_t &bM, uint32_t junk, uint32_t &nrows) {
+  constexpr uint32_t K = FS_HK;
+  static_assert(K == 8, "two 16 B vectors per entry: 8 nodes of two signed bytes");
+  static_assert(4u * FS_HIST_REP == 128u, "offsets are scaled by the 32 copies' 128 B index stride");
+  static_assert(G % K == 0, "nodes per group must be a multiple of FS_HK");
+  uint32_t h = st.rho, hv = h1, bP = st.A, m = bM;
+  const uint32_t kk = st.k;
+#pragma unroll
+  for (int v = 0; v < G / (int)K; ++v) {
+    if (kk > K * (uint32_t)v) {
+      const uint4 w0 = lds128(h), w1 = lds128(hv);
+      const uint32_t b = K * (uint32_t)v;
+      hq_node<0>(bP, m, w1.x, b + 0u < kk, junk);
+      hq_node<1>(bP, m, w1.x, b + 1u < kk, junk);
+      hq_node<0>(bP, m, w1.y, b + 2u < kk, junk);
+      hq_node<1>(bP, m, w1.y, b + 3u < kk, junk);
+      hq_node<0>(bP, m, w1.z, b + 4u < kk, junk);
+      hq_node<1>(bP, m, w1.z, b + 5u < kk, junk);
+      hq_node<0>(bP, m, w1.w, b + 6u < kk, junk);
+      hq_node<1>(bP, m, w1.w, b + 7u < kk, junk);
+      h = w0.x;
+      hv = w0.w;
+      bP += w0.y;
+      m += w0.z;
+    }
+  }
+  st.rho = h;
+  h1 = hv;
+  st.A = bP;
+  bM = m;
+  const uint32_t done = kk < (uint32_t)G ? kk : (uint32_t)G;
+  st.k = kk - done;
+  nrows += done;  // (dl != 0: a node changes any difference index by at most 1)
+}
+
+// A lane that has just entered a node (A, rho; its entry unit not charged to the budget) takes
+// it as the NEXT node of the state walk: a_L and lsum become those of the node's virtual
+// predecessor in the run (one more), so the walk's lazy counters charge the node like an
+// advance; then the state sigma = (rho, A mod s), Q = floor(A / s), X = lsum + s Q and
+// Y = X + Q dl as addresses in the lane's difference-array copy (dbase: shared index 0;
+// length l lives at index l + hq_bias).
+template <int D, int ALPHA>
+__device__ __forceinline__ void enter_h(Lane<D> &st, const Consts &c, uint32_t hq_lane, uint32_t dbase,
+                                        uint32_t &h1, uint32_t &bM, uint32_t &budget) {
+  constexpr uint32_t STR = 4u * FS_HIST_REP;
+  if constexpr (D >= 3) {
+    st.a[D - 3] += 1u;
+    st.lsum += 1u;
+  }
+  st.cur = -1;
+  sync_k<D, ALPHA>(st, budget);
+  const uint32_t Q = divq(st.A, c.dvS), a = st.A - Q * c.s;
+  const uint32_t X = dbase + STR * (st.lsum + c.s * Q + c.hq_bias);
+  const uint32_t Y = X + STR * Q * (uint32_t)c.dl;
+  const uint32_t sig = st.rho * c.s + a, e0 = hq_lane + 32u * FS_HQ_COPIES * sig;
+  st.rho = e0 + ((sig & 1u) ? 16u * FS_HQ_COPIES : 0u);  // vector 0 (the vectors swap on odd states)
+  h1 = e0 + ((sig & 1u) ? 0u : 16u * FS_HQ_COPIES);
+  st.A = c.dl > 0 ? X : Y;
+  bM = c.dl > 0 ? Y : X;
+}
+
 template <int D, int CONS, int B, bool KTAB>
 __global__ void __launch_bounds__(kBlock, (CONS == kConsRowsAny || CONS == FS_CONSUMER_ROWS ? 4
                                            : CONS == kConsCountClosed              ? (D <= 9 ? FS_CC_MINB : 1)
@@ -1046,7 +1129,7 @@ __global__ void __launch_bounds__(kBlock, (CONS == kConsRowsAny || CONS == FS_CO
   uint32_t *hist_s = ktab_s + kt_words;
   const uint32_t hist_words =
       !(HISTLIKE && P.hist_smem) ? 0u
-      : ((CONS == kConsHistClosed ? (P.diff_len + 1u) * P.hist_rep : P.hist_len) + 3u) & ~3u;
+      : ((CONS == kConsHistClosed ? P.diff_slen * P.hist_rep : P.hist_len) + 3u) & ~3u;
   unsigned char *stage = reinterpret_cast<unsigned char *>(hist_s + hist_words);
 
   const uint32_t ktab_base = (uint32_t)__cvta_generic_to_shared(ktab_s);
@@ -1056,6 +1139,12 @@ __global__ void __launch_bounds__(kBlock, (CONS == kConsRowsAny || CONS == FS_CO
   const bool qfast = cfast && c.qtab_off != 0;  // count in state form (cq_group)
   const bool t2fast = cfast && D >= 4 && c.t2_off != 0 && (!qfast || c.t2q_off != 0);
   const bool t2h = hfast && D >= 4 && c.t2_off != 0;  // histogram: one-level ascend by table
+  const bool hqf = hfast && P.hist_hq && c.hq_off != 0;  // histogram in state form (hq_group)
+  const uint32_t hq_lane = ktab_base + 4u * c.hq_off + 16u * (threadIdx.x & (FS_HQ_COPIES - 1u));
+  uint32_t hq_bm = 0, hq_h1 = 0;  // state form: -1 base address (bP lives in st.A), second vector's address
+  // ... and its junk word (the last index of its copy), the target of masked nodes
+  const uint32_t hq_junk = (uint32_t)__cvta_generic_to_shared(hist_s) + 4u * (threadIdx.x & (FS_HIST_REP - 1u)) +
+                           4u * FS_HIST_REP * (P.diff_slen - 1u);
   const uint32_t t2base = ktab_base + 4u * (qfast ? c.t2q_off : c.t2_off);
   const uint32_t qbase_lane = ktab_base + 4u * c.qtab_off + 16u * (threadIdx.x & 7u);
   const uint32_t q1base = ktab_base + 4u * c.q1_off;
@@ -1082,6 +1171,10 @@ __global__ void __launch_bounds__(kBlock, (CONS == kConsRowsAny || CONS == FS_CO
         ((i - c.t3_off) & 3u) == 0u)
       v += ktab_base;
     if (cfast && c.qtab_off != 0u && i >= c.qtab_off && i < c.q1_off && ((i - c.qtab_off) & 3u) == 0u) v += ktab_base;
+    if (hqf && i >= c.hq_off && i < c.hq_off + 8u * FS_HQ_COPIES * c.gA * c.s) {  // link0 / link1 of vector 0
+      const uint32_t r = i - c.hq_off, sig = r / (8u * FS_HQ_COPIES), slot = (r / 4u) % (2u * FS_HQ_COPIES);
+      if (slot / FS_HQ_COPIES == (sig & 1u) && ((r & 3u) == 0u || (r & 3u) == 3u)) v += ktab_base;
+    }
     if (cfast && c.t2q_off != 0u && D >= 4 && i >= c.t2q_off && i < c.t2q_off + 4u * FS_QK * c.g[D >= 4 ? D - 3 : 0] &&
         ((i - c.t2q_off) & 3u) == 0u)
       v += ktab_base;
@@ -1123,7 +1216,9 @@ __global__ void __launch_bounds__(kBlock, (CONS == kConsRowsAny || CONS == FS_CO
   EmitCount<D> e_count{0};
   EmitHist<D> e_hist{hist_s, P.hist_out, P.hist_smem, 0};
   const uint32_t hrep = CONS == kConsHistClosed && P.hist_rep > 1u ? P.hist_rep : 1u;
-  EmitHistClosed<D> e_hcl{hist_s + (hrep > 1u ? (threadIdx.x & (hrep - 1u)) : 0u), P.diff_out, P.hist_smem, hrep, 0};
+  // (shared index = difference index + diff_sbias: the state form's margin below index 0)
+  EmitHistClosed<D> e_hcl{hist_s + P.diff_sbias * hrep + (hrep > 1u ? (threadIdx.x & (hrep - 1u)) : 0u), P.diff_out,
+                          P.hist_smem, hrep, 0};
   const HcConsts hck = hc_consts(c, (uint32_t)__cvta_generic_to_shared(hist_s), hrep);
   EmitAny<D> e_any{P.pred, P.pred_arg, P.found, P.witness, false};
   EmitRows<D, B> e_rows;
@@ -1192,7 +1287,12 @@ __global__ void __launch_bounds__(kBlock, (CONS == kConsRowsAny || CONS == FS_CO
             else if (t2fast || t2h) t2_sync<D>(st, c, t2base, t2a, q2);
             if (t3fast) t3_sync<D>(st, c, t3base, t3a, q3);
             if (qfast) enter_q<D>(st, c, qbase_lane, q1base, e_count.n);
-            if (hfast) take_entry_hist<D>(st, c, e_hcl);
+            if (hqf) {  // (position_in_node charged the entry unit: the walk takes it as a node)
+              budget += 1u;
+              enter_h<D, ALPHA>(st, c, hq_lane, hck.dbase, hq_h1, hq_bm, budget);
+            } else if (hfast) {
+              take_entry_hist<D>(st, c, e_hcl);
+            }
           }
         }
       }
@@ -1228,6 +1328,8 @@ __global__ void __launch_bounds__(kBlock, (CONS == kConsRowsAny || CONS == FS_CO
       } else if (CONS == kConsAnyClosed) {
 #pragma unroll
         for (int u = 0; u < UNROLL; ++u) fast_step_closed<D>(st, c, kt, budget, e_any);
+      } else if (hqf) {
+        hq_group<D, FS_HQ_GROUP>(st, hq_h1, hq_bm, hq_junk, e_hcl.n);
       } else if (hfast && c.hadv_off != 0u) {
         const uint32_t htab = ktab_base + 4u * c.hadv_off;
         if (c.dl > 0)
@@ -1277,7 +1379,19 @@ __global__ void __launch_bounds__(kBlock, (CONS == kConsRowsAny || CONS == FS_CO
       sync_k<D, ALPHA>(st, budget);
       const bool slow = needs_slow<D>(st, budget);
       if (__any_sync(kFull, slow)) {
-        if (slow) {
+        if (slow && hqf) {  // state-form histogram: the ascend, the new run's entry node is the next node
+          bool ok = true;
+          if (t2h && t2_can_ascend<D>(st)) {
+            t2_ascend_hist<D>(st, c, t2a, q2);
+          } else {
+            ok = advance<D>(st, c);
+            if (t2h) t2_sync<D>(st, c, t2base, t2a, q2);
+          }
+          if (ok)
+            enter_h<D, ALPHA>(st, c, hq_lane, hck.dbase, hq_h1, hq_bm, budget);
+          else
+            budget = 0;  // end of stream
+        } else if (slow) {
           if (t2fast && t2_can_ascend<D>(st)) {  // one-level ascend by table (count)
             if (qfast) {
               t2q_ascend<D>(st, c, ktab_base, t2base, t2a, q2, budget, qbase_lane, q1base, e_count.n);
@@ -1320,12 +1434,13 @@ __global__ void __launch_bounds__(kBlock, (CONS == kConsRowsAny || CONS == FS_CO
         acc += e_count.n;
         e_count.n = 0;
       }
-      if (HISTLIKE && P.hist_smem) {
+      if (HISTLIKE && P.hist_smem && (!hqf || it + UNROLL >= INNER)) {
         // overflow guard of the 32-bit shared bins / difference array: the rows added by the
         // warp this iteration (an upper bound of any bin's change) are summed per CTA, and
         // every 2^30 of them the bins are drained to global memory (as sign-extended values
         // for the difference array).  The plan bounds one iteration's rows per CTA far below
-        // 2^30 (fs_capi.cu), so no bin can pass 2^31 between drains.
+        // 2^30 (fs_capi.cu), so no bin can pass 2^31 between drains.  (State form: nodes, at
+        // most 1 per index each, counted over the whole inner loop -- <= 2^15 per CTA.)
         const uint32_t mine = CONS == kConsHistClosed ? e_hcl.n : e_hist.n;
         e_hist.n = 0;
         e_hcl.n = 0;
@@ -1335,7 +1450,7 @@ __global__ void __launch_bounds__(kBlock, (CONS == kConsRowsAny || CONS == FS_CO
           if ((old >> 30) != ((old + wsum) >> 30)) {
             if (CONS == kConsHistClosed) {
               for (uint32_t i = 0; i < P.diff_len * hrep; ++i) {
-                const int32_t v = (int32_t)atomicExch(&hist_s[i], 0u);
+                const int32_t v = (int32_t)atomicExch(&hist_s[i + P.diff_sbias * hrep], 0u);
                 if (v) atomicAdd(&P.diff_out[i / hrep], (unsigned long long)(long long)v);
               }
             } else {
@@ -1376,7 +1491,7 @@ __global__ void __launch_bounds__(kBlock, (CONS == kConsRowsAny || CONS == FS_CO
     for (uint32_t i = threadIdx.x; i < P.diff_len; i += blockDim.x) {
       int64_t v = 0;
       for (uint32_t j = 0; j < hrep; ++j)  // lane-private copies, rotated so lanes hit distinct banks
-        v += (int32_t)hist_s[i * hrep + ((j + threadIdx.x) & (hrep - 1u))];
+        v += (int32_t)hist_s[(i + P.diff_sbias) * hrep + ((j + threadIdx.x) & (hrep - 1u))];
       if (v) atomicAdd(&P.diff_out[i], (unsigned long long)v);
     }
   }
@@ -1427,7 +1542,7 @@ static size_t smem_bytes(const KParams &kp, int consumer) {
   size_t b = (size_t)((kp.c.ktab_len + 3u) & ~3u) * 4;
   if (consumer == FS_CONSUMER_HIST && kp.hist_smem) b += (size_t)((kp.hist_len + 3u) & ~3u) * 4;
   if (consumer == kConsHistClosed && kp.hist_smem)
-    b += (size_t)(((kp.diff_len + 1u) * (kp.hist_rep > 1u ? kp.hist_rep : 1u) + 3u) & ~3u) * 4;
+    b += (size_t)((kp.diff_slen * (kp.hist_rep > 1u ? kp.hist_rep : 1u) + 3u) & ~3u) * 4;
   if (consumer == FS_CONSUMER_ROWS) b += (size_t)kBlock * kLaneStride + (kBlock / 32) * 32;
   if (consumer == kConsRowsAny) b += (size_t)(kBlock / 32) * kWarpBuf;
   return b;

@@ -6,10 +6,10 @@ from paper_2405_07989_b200.api import Plan
 
 
 def host_model(n, gens, consumer=L.FS_CONSUMER_COUNT, *, rank=0, world=1, slice_units=0, B=16, cap=None,
-               want_hist=False, want_rows=False, want_slices=False, tail=0, gen_order=0, slicing=0):
+               want_hist=False, want_rows=False, want_slices=False, tail=0, gen_order=0, slicing=0, walk=0):
     """Run the kernels' per-lane code on the host (sequential, slice by slice)."""
     p = Plan(n, gens, consumer, rank=rank, world=world, slice_units=slice_units, tail=tail, gen_order=gen_order,
-             slicing=slicing)
+             slicing=slicing, walk=walk)
     info = p.info
     d = len(gens)
     cnt = ctypes.c_uint64(0)

@@ -337,3 +337,46 @@ def test_host_model_group_counts_beyond_32_bits():
         r = host_model(n, (1, 1, 2), tail=L.FS_TAIL_CLOSED, slice_units=T)
         assert r["count"] == want
     assert host_model(100000, (1, 1, 1), tail=L.FS_TAIL_CLOSED, slice_units=1 << 24)["count"] == 5000150001
+
+
+def test_hist_state_form_host_replay(oracle_mod):
+    """The state-form histogram table (fs_host.cu, hq_group) replayed on the host: every
+    instance's histogram equals the oracle's, the residue-form walk gives the same, and every
+    difference update stays inside the kernel's shared array with its margins (else ERANGE)."""
+    import random
+
+    rng = random.Random(11)
+    used = 0
+    signs = set()
+    tried = 0
+    while used < 40 and tried < 4000:
+        tried += 1
+        d = rng.randint(3, 7)
+        g = [rng.randint(1, 30) for _ in range(d)]
+        n = rng.randint(0, 300)
+        go = rng.randint(0, 1)
+        p = Plan(n, g, L.FS_CONSUMER_HIST, tail=L.FS_TAIL_CLOSED, gen_order=go)
+        if not p.info["state_block"]:
+            continue
+        used += 1
+        want = oracle.hist(n, g)
+        for T in (0, 1, 9):
+            r = host_model(n, g, L.FS_CONSUMER_HIST, slice_units=T, want_hist=True, tail=L.FS_TAIL_CLOSED,
+                           gen_order=go)
+            assert r["info"]["state_block"] == 8
+            assert r["hist"] == want, (n, g, go, T)
+        r = host_model(n, g, L.FS_CONSUMER_HIST, want_hist=True, tail=L.FS_TAIL_CLOSED, gen_order=go,
+                       walk=L.FS_WALK_RESIDUE)
+        assert r["info"]["state_block"] == 0 and r["hist"] == want
+        gi = sorted(g, reverse=True) if go else g
+        signs.add((gi[-2] > gi[-1]))
+    assert used == 40 and signs == {True, False}
+
+
+def test_hist_state_form_c3_gens(oracle_mod):
+    """C3's generators (largest-first: g_{d-1}, g_d = 14, 13, dl = +1) at oracle-sized n."""
+    for n in (300, 650):
+        r = host_model(n, W.C3.gens, L.FS_CONSUMER_HIST, want_hist=True, tail=L.FS_TAIL_CLOSED,
+                       gen_order=L.FS_GENORDER_AUTO)
+        assert r["info"]["state_block"] == 8
+        assert r["hist"] == oracle.hist(n, W.C3.gens)
