@@ -233,6 +233,8 @@ typedef struct {
     uint32_t state_block;       /* count and histogram plans: level-L nodes per table step of the
                                    state-form walk, 0 if the plan does not use it */
     uint32_t cost_slices;       /* 1: equal-cost slices (slice-start table of two kernels) */
+    uint32_t dead_levels;       /* bit q: coordinate q's subtrees are skipped when the gcd of the
+                                   generators after it does not divide their residual (NEXT-3) */
 } fs_plan_info_t;
 
 int fs_plan_create(uint64_t n, const uint32_t *gens, int d, int consumer, const fs_exec_t *ex,

@@ -68,6 +68,7 @@ class PlanInfoT(ctypes.Structure):
         ("table_bytes", ctypes.c_uint64),
         ("state_block", ctypes.c_uint32),
         ("cost_slices", ctypes.c_uint32),
+        ("dead_levels", ctypes.c_uint32),
     ]
 
 

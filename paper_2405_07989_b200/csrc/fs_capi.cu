@@ -135,6 +135,7 @@ int fs_plan_info(const fs_plan *p, fs_plan_info_t *info) {
                       : (p->consumer == FS_CONSUMER_HIST && p->ex.tail == FS_TAIL_CLOSED && p->d >= 2 &&
                          fs_hist_closed_shape(p).hq) ? (uint32_t)FS_HK : 0u;
   info->cost_slices = p->cost_slices ? 1u : 0u;
+  info->dead_levels = p->c.cd_mask;
   return FS_OK;
 }
 

@@ -86,6 +86,12 @@ struct Consts {
   uint32_t hq_bias;      // its difference-array index bias (s - 1: rowless nodes reach index -(s-1))
   uint32_t radv_off;     // word offset of the materialise advance table (0: none; fs_host.cu):
                          //   4 words per rho {next | inc << 11, k0(next), ad0(next), 0}
+  // NEXT-3 for k >= 3 trailing generators: bit j (0-based coordinate j <= L - 2) set
+  // when G_j = gcd(g_{j+1}, .., g_d) > 1 -- a node (a_1..a_j) whose residual G_j does not divide
+  // roots a subtree without factorizations, which advance_cd() skips (charging its DP units)
+  uint32_t cd_mask;
+  uint32_t cd_g[FS_MAX_D];
+  Div cd_dv[FS_MAX_D];
   int32_t dl;            // t - s: change of a row's length from one valid a_{d-1} to the next
   uint32_t dstride;      // stride of the closed-tail length-difference array (|dl|, or 1 if 0)
   uint8_t perm[FS_MAX_D];  // internal coordinate j is the caller's coordinate perm[j]
@@ -292,6 +298,81 @@ FS_HD bool advance(Lane<D> &st, const Consts &c) {
   }
 }
 
+// NEXT-3 beyond the last two generators ("the same applies if the last n generators
+// share a common denominator"): after an ascend, a node (a_1..a_j), j <= L - 1, whose residual
+// is not a multiple of G_j = gcd(g_{j+1}, .., g_d) has no factorization below it.  The lane is at
+// the first node of that subtree (the ascend re-solved every deeper coordinate greedily), so
+// the subtree's units -- U[j][R_j] - U[j][R_j - g_j] from the exact DP, node entries for
+// count / hist / any plans, rows (none) for materialise -- are charged at once, the deeper
+// coordinates are zeroed (the lane stands on the subtree's last node) and the ascend repeats.
+// Returns false at end of stream, or when the slice's budget ends inside a dead subtree.
+// (0-based below: coordinate q <= L - 2 has residual R[q] and divisor cd_g[q].)
+// The level an ascend from this state decrements: the rightmost nonzero a[q], q <= L - 2.
+template <int D>
+FS_HD int ascend_level(const Lane<D> &st) {
+  constexpr int L = D - 2;
+  int k = -1;
+#pragma unroll
+  for (int j = 0; j < L - 1; ++j)
+    if (st.a[j] > 0) k = j;
+  return k;
+}
+
+template <int D, int ALPHA>
+FS_HD bool ascend_cd(Lane<D> &st, const Consts &c, uint32_t &budget) {
+  constexpr int L = D - 2;
+  if constexpr (L >= 2) {
+    for (;;) {
+      const int k = ascend_level<D>(st);
+      if (!ascend<D>(st, c)) return false;
+      // the new subtrees are those at levels k .. L - 2 (the lane stands on their first node)
+      int j = -1;
+#pragma unroll
+      for (int q = 0; q < L - 1; ++q)
+        if (j < 0 && q >= k && ((c.cd_mask >> q) & 1u) && st.R[q] != divq(st.R[q], c.cd_dv[q]) * c.cd_g[q]) j = q;
+      if (j < 0) return true;
+      if (ALPHA) {
+        uint64_t u;
+        if (j == 0) {
+          const uint32_t top = divq(c.n, c.dv[0]), x = st.a[0];
+          u = ldU(c.U + x) - (x < top ? ldU(c.U + x + 1) : 0ull);
+        } else {
+          const uint64_t *Uj = c.U + c.u0_len + (uint64_t)(j - 1) * ((uint64_t)c.n + 1);
+          const uint32_t r = st.R[j];
+          u = ldU(Uj + r) - (r >= c.g[j] ? ldU(Uj + r - c.g[j]) : 0ull);
+        }
+        if (u >= budget) {  // the slice ends inside the dead subtree: nothing left to emit
+          budget = 0;
+          return false;
+        }
+        budget -= (uint32_t)u;
+      }
+      uint32_t lsum = 0;
+#pragma unroll
+      for (int q = 0; q < L; ++q) {
+        if (q > j) {
+          st.a[q] = 0;
+          st.R[q] = st.R[q - 1];
+        }
+        lsum += st.a[q];
+      }
+      st.lsum = lsum;
+    }
+  } else {
+    (void)budget;
+    return ascend<D>(st, c);
+  }
+}
+
+template <int D, int ALPHA>
+FS_HD bool advance_cd(Lane<D> &st, const Consts &c, uint32_t &budget) {
+  constexpr int L = D - 2;
+  if constexpr (L >= 2) {
+    if (c.cd_mask && st.a[L - 1] == 0) return ascend_cd<D, ALPHA>(st, c, budget);
+  }
+  return advance<D>(st, c);
+}
+
 // Position the lane at global unit index u (exact, from the DP tables), perform the node
 // entry, and return the offset of u inside the node's unit list (0 = the entry unit when
 // alpha = 1).
@@ -431,7 +512,7 @@ FS_HD bool needs_refill(const Lane<D> &st, uint32_t budget) {
 // by the next fast_step, so every emission happens with the warp converged.
 template <int D, bool NEED_AD, int ALPHA, class KT>
 FS_HD void slow_step(Lane<D> &st, const Consts &c, const KT &kt, uint32_t &budget) {
-  if (!advance<D>(st, c)) {
+  if (!advance_cd<D, ALPHA>(st, c, budget)) {
     budget = 0;  // end of stream
     return;
   }

@@ -146,6 +146,17 @@ int fs_validate_and_build(fs_plan *p, uint64_t n, const uint32_t *gens, int d, i
   // node units for count / hist / any; row units for materialise (exact offsets)
   c.alpha = (consumer == FS_CONSUMER_ROWS) ? 0u : 1u;
   c.beta = (consumer == FS_CONSUMER_ROWS) ? 1u : 0u;
+  // NEXT-3 for k >= 3 trailing generators (fs_core.cuh ascend_cd): suffix gcds G_q of the
+  // generators after coordinate q, for the node levels q <= d - 4 whose subtrees an ascend enters
+  if (d >= 4 && e.walk != FS_WALK_RESIDUE) {
+    uint32_t G = gcd32(gens[d - 1], gens[d - 2]);
+    for (int q = d - 4; q >= 0; --q) {
+      G = gcd32(G, gens[q + 1]);
+      c.cd_g[q] = G;
+      c.cd_dv[q] = fs_make_div(G > 1 ? G : 2);
+      if (G > 1) c.cd_mask |= 1u << q;
+    }
+  }
 
   if (d == 1) {
     // Z(n,(g)) = {(n/g)} iff g | n: one row or none; no tables, no nodes.
@@ -384,7 +395,9 @@ int fs_validate_and_build(fs_plan *p, uint64_t n, const uint32_t *gens, int d, i
         const uint32_t t2o = (t2_off + 3u) & ~3u;
         // (histogram: the same table with word 2 = a*0 = A0 - k0(rho0) of the entry node,
         // INT32_MIN when k0 = none; the kernel takes the node's length progression from it)
-        if ((consumer == FS_CONSUMER_COUNT || want_hist) && L >= 2 && gL <= 2048u && gL1 / gL + 1u < 65536u &&
+        // (not when a run can be dead -- the k >= 3 skip lives in the generic ascend)
+        if ((consumer == FS_CONSUMER_COUNT || want_hist) && L >= 2 && !((c.cd_mask >> (L - 2)) & 1u) &&
+            gL <= 2048u && gL1 / gL + 1u < 65536u &&
             c.gA < 65536u && 4ull * t2o + 16ull * gL + 16384ull <= (1ull << fs::kCAdvShift)) {
           p->ktab.resize(t2o + 4u * gL, 0u);
           for (uint32_t r = 0; r < gL; ++r) {
@@ -405,7 +418,8 @@ int fs_validate_and_build(fs_plan *p, uint64_t n, const uint32_t *gens, int d, i
           // {rel(r3') | dQ3 << 16, rho0 | A0 << 16, rows0 | r3' << 16, r2 | a_L << 16}.
           const uint32_t gL2 = L >= 3 ? gens[L - 3] : 0u;
           const uint32_t t3o = ((uint32_t)p->ktab.size() + 3u) & ~3u;
-          if (consumer == FS_CONSUMER_COUNT && L >= 3 && gL1 <= 2048u && gL2 / gL1 + 1u < 65536u && gL1 < 65536u && gL < 65536u &&
+          if (consumer == FS_CONSUMER_COUNT && L >= 3 && !((c.cd_mask >> (L - 3)) & 1u) && gL1 <= 2048u &&
+              gL2 / gL1 + 1u < 65536u && gL1 < 65536u && gL < 65536u &&
               4ull * t3o + 16ull * gL1 + 16384ull <= (1ull << fs::kCAdvShift)) {
             bool fits = true;
             std::vector<uint32_t> t3(4u * gL1, 0u);
@@ -1039,7 +1053,7 @@ void host_hist_tables_slice(const fs_plan *p, const KT &ktab, fs::Lane<D> &st, u
     st.k = kk > FS_HQ_GROUP ? kk - FS_HQ_GROUP : 0u;
     fs::sync_k<D, 1>(st, budget);
     if (!fs::needs_slow<D>(st, budget)) continue;
-    if (!fs::advance<D>(st, c)) {  // (a_L = 0: the ascend) end of stream
+    if (!fs::advance_cd<D, 1>(st, c, budget)) {  // (a_L = 0: the ascend) end of stream or slice
       budget = 0;
       break;
     }

@@ -1384,7 +1384,7 @@ __global__ void __launch_bounds__(kBlock, (CONS == kConsRowsAny || CONS == FS_CO
           if (t2h && t2_can_ascend<D>(st)) {
             t2_ascend_hist<D>(st, c, t2a, q2);
           } else {
-            ok = advance<D>(st, c);
+            ok = advance_cd<D, ALPHA>(st, c, budget);
             if (t2h) t2_sync<D>(st, c, t2base, t2a, q2);
           }
           if (ok)

@@ -485,3 +485,36 @@ def test_cost_slices(oracle_mod, inst):
         assert found == bool(want["count"])
         if found:
             assert sum(a * b for a, b in zip(wit, g)) == n and sum(wit) >= lmax
+
+
+def _state_form_instances():
+    """Instances whose fs_length_set runs the state-form histogram (hq_group): random ones with
+    gcd(g_{d-1}, g_d) = 1 in stream order (both signs of t - s), plus C3's generators."""
+    out = [W.Instance("C3g650", 650, W.C3.gens), W.Instance("C3g1100", 1100, W.C3.gens)]
+    for inst in W.random_instances(400, seed=5, d_max=7, g_max=30, n_max=350):
+        if len(out) == 14:
+            break
+        p = api.Plan(inst.n, inst.gens, L.FS_CONSUMER_HIST, tail=L.FS_TAIL_CLOSED, gen_order=L.FS_GENORDER_AUTO)
+        if p.info["state_block"] and gf.count(inst.n, inst.gens) <= 3000000:
+            out.append(inst)
+    return out
+
+
+@pytest.mark.parametrize("inst", _state_form_instances(), ids=ids)
+def test_hist_state_form_vs_residue_form(oracle_mod, inst):
+    """The state-form histogram walk equals the residue-form walk and the exact histogram, for
+    the default slices, tiny slices (many run starts inside blocks) and 3 virtual ranks."""
+    n, g = inst.n, inst.gens
+    want = gf.hist(n, g)
+    kw = dict(tail=L.FS_TAIL_CLOSED, gen_order=L.FS_GENORDER_AUTO)
+    assert api.Plan(n, g, L.FS_CONSUMER_HIST, **kw).info["state_block"] == 8
+    for T in (0, 1, 7):
+        h = api.fs_length_set_ex(n, g, slice_units=T, **kw)
+        assert hist_list(h, len(want)) == want, T
+    h = api.fs_length_set_ex(n, g, walk=L.FS_WALK_RESIDUE, **kw)
+    assert hist_list(h, len(want)) == want
+    tot = [0] * len(want)
+    for r in range(3):
+        h = hist_list(api.fs_length_set_ex(n, g, rank=r, world=3, **kw), len(want))
+        tot = [a + b for a, b in zip(tot, h)]
+    assert tot == want

@@ -380,3 +380,56 @@ def test_hist_state_form_c3_gens(oracle_mod):
                        gen_order=L.FS_GENORDER_AUTO)
         assert r["info"]["state_block"] == 8
         assert r["hist"] == oracle.hist(n, W.C3.gens)
+
+
+def _cd_instances():
+    """Instances whose last k >= 3 generators share a factor (NEXT-3 beyond the last two),
+    in stream order for gen_order given and auto."""
+    rng = random.Random(23)
+    out = [(300, (5, 7, 6, 9, 12), 0), (260, (11, 4, 6, 10, 8), 0), (240, (7, 5, 12, 18, 30, 24), 0),
+           (180, (3, 10, 15, 20, 25), 1), (200, (9, 8, 12, 16, 20, 4), 0)]
+    while len(out) < 24:
+        d = rng.randint(4, 7)
+        f = rng.choice((2, 3, 4, 6))
+        k = rng.randint(3, d - 1)
+        g = [rng.randint(1, 25) for _ in range(d - k)] + [f * rng.randint(1, 8) for _ in range(k)]
+        out.append((rng.randint(0, 260), tuple(g), rng.randint(0, 1)))
+    return out
+
+
+@pytest.mark.parametrize("case", _cd_instances(), ids=lambda c: "%d_%s_go%d" % (c[0], "-".join(map(str, c[1])), c[2]))
+def test_dead_subtree_skip(oracle_mod, case):
+    """NEXT-3 for k >= 3 trailing generators (fs_core.cuh ascend_cd): every consumer's host model
+    with the dead-subtree skip equals the oracle, at tiny slices (budgets ending inside a
+    skipped subtree) and over 3 ranks, and the plan reports the skipped levels."""
+    n, g, go = case
+    want = oracle.run(n, g, hist_len=oracle.hist_len_for(n, g))
+    levels = Plan(n, g, L.FS_CONSUMER_COUNT, gen_order=go).info["dead_levels"]
+    from math import gcd
+
+    def mask(gi):
+        m = 0
+        for q in range(len(gi) - 3):
+            G = 0
+            for x in gi[q + 1:]:
+                G = gcd(G, x)
+            m |= (G > 1) << q
+        return m
+
+    # (auto order keeps the given order unless largest-first has fewer level-L nodes)
+    assert levels == mask(list(g)) or (go and levels == mask(sorted(g, reverse=True)))
+    for T in (0, 1, 3, 7):
+        for tail in (L.FS_TAIL_ROWS, L.FS_TAIL_CLOSED):
+            r = host_model(n, g, L.FS_CONSUMER_COUNT, slice_units=T, tail=tail, gen_order=go, want_slices=True)
+            assert r["count"] == want["count"], (T, tail)
+        r = host_model(n, g, L.FS_CONSUMER_HIST, slice_units=T, want_hist=True, tail=L.FS_TAIL_CLOSED, gen_order=go)
+        assert r["hist"] == want["hist"], T
+    tot = sum(host_model(n, g, L.FS_CONSUMER_COUNT, rank=r, world=3, tail=L.FS_TAIL_CLOSED, gen_order=go)["count"]
+              for r in range(3))
+    assert tot == want["count"]
+    if not go:
+        r = host_model(n, g, L.FS_CONSUMER_ROWS, slice_units=8, want_rows=True, B=32)
+        assert r["rows"] == oracle.rows(n, g, B=32)
+    lmax = max((i for i, v in enumerate(want["hist"]) if v), default=0)
+    f, _ = host_any(n, g, L.FS_PRED_LEN_GE, lmax, tail=L.FS_TAIL_CLOSED, gen_order=go, slice_units=3)
+    assert f == bool(want["count"])
