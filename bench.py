@@ -679,6 +679,14 @@ def extras(args, world, rank, local, dev, stream, peaks, peaks_kind, barrier, ma
          "C2CD count, given order (gcd(18, 24) = 6: the closed tail walks live nodes only, NEXT-3)", 3),
         ("c2cd_count_rows", W.C2CD, L.FS_CONSUMER_COUNT, {},
          "C2CD count, given order, one step per row (no skip)", 3),
+        ("c2cd_hist_closed", W.C2CD, L.FS_CONSUMER_HIST, {"tail": 1},
+         "C2CD histogram, given order, closed tail over the live-node table (NEXT-3)", 3),
+        ("c3cd_count_closed", W.C3CD, L.FS_CONSUMER_COUNT, {"tail": 1},
+         "C3CD count (gcd(12, 18, 24) = 6), closed tail + dead-run skip in the ascend (NEXT-3, k = 3)", 3),
+        ("c3cd_count_closed_noskip", W.C3CD, L.FS_CONSUMER_COUNT, {"tail": 1, "walk": 1},
+         "C3CD count, closed tail, residue walk without the k >= 3 dead-subtree skip (ablation)", 3),
+        ("c3cd_hist_closed", W.C3CD, L.FS_CONSUMER_HIST, {"tail": 1},
+         "C3CD histogram, closed tail, live-node table + dead-run skip (NEXT-3)", 3),
         # E2 (Table 1 modulo on/off) re-run on B200: the index-(d-1) loop variants
         ("c2l_skip_off", W.C2L, L.FS_CONSUMER_COUNT, {"tail": 2}, "C2-L count, Skip=off (every candidate)", 2),
         ("c2l_skip_paper", W.C2L, L.FS_CONSUMER_COUNT, {"tail": 3}, "C2-L count, Skip=paper (P:170-176)", 2),

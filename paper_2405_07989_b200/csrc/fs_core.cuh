@@ -79,6 +79,7 @@ struct Consts {
   uint32_t cadv2_skip;   // 1: that table walks live nodes only (8 words per entry; NEXT-3)
   uint32_t t3_off;       // word offset of the count's two-level ascend table (0: none; fs_host.cu)
   uint32_t hadv_off;     // word offset of the histogram's 8-copy closed-tail table (0: none; fs_host.cu)
+  uint32_t hadv_skip;    // 1: that table walks live nodes only (gcd(g_{d-1}, g_d) > 1; NEXT-3)
   uint32_t qtab_off;     // word offset of the count's state-pair table (0: none; fs_host.cu)
   uint32_t q1_off;       // word offset of its single-step table
   uint32_t t2q_off;      // word offset of the count's one-level ascend table in state form (0: none)

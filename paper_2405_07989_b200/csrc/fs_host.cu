@@ -203,7 +203,9 @@ int fs_validate_and_build(fs_plan *p, uint64_t n, const uint32_t *gens, int d, i
       // paper's common-divisor skip for the last two generators):
       // the entry jumps over them -- `steps` advances at once, summed quotient increments;
       // steps = 0xFFFFFFFF when no residue of the cycle is live.  One 16 B load per advance.
-      if (consumer == FS_CONSUMER_ROWS && c.gA <= 1024u) {
+      // (also for any-predicate plans with gcd(g_{d-1}, g_d) > 1: the closed any walk jumps to
+      // live nodes by it, fast_step_closed_live)
+      if ((consumer == FS_CONSUMER_ROWS || (consumer == FS_CONSUMER_ANY && c.h > 1u)) && c.gA <= 1024u) {
         const uint32_t radv_off = ((uint32_t)p->ktab.size() + 3u) & ~3u;
         std::vector<uint32_t> rv(4u * c.gA, 0u);
         bool fits = true;
@@ -287,19 +289,37 @@ int fs_validate_and_build(fs_plan *p, uint64_t n, const uint32_t *gens, int d, i
         if (want_hist) {
           const uint32_t ho = ((uint32_t)p->ktab.size() + 3u) & ~3u;
           if (c.gA <= 128u) {  // <= 16 KB: the table shares shared memory with the bins
+            // gcd(g_{d-1}, g_d) = h > 1 (NEXT-3): each entry jumps to the next LIVE node
+            // (residual divisible by h), word 1 = summed quotient increments | advances << 16;
+            // a residue cycle without a live node gets a self-link of 0x7fff advances (the run
+            // ends before it).  The group masks by cumulative advances (hc_group8<.., SKIP>).
+            const bool skip = c.h > 1u;
             std::vector<uint32_t> hv(32u * c.gA, 0u);
             for (uint32_t rho = 0; rho < c.gA; ++rho) {
-              const fs::Adv w = ar.step(rho, c);
+              fs::Adv w = ar.step(rho, c);
+              uint32_t steps = 1, inc = w.inc;
+              while (skip && w.k0 == fs::kNone && steps <= c.gA) {
+                w = ar.step(w.next, c);
+                inc += w.inc;
+                ++steps;
+              }
+              const bool dead = w.k0 == fs::kNone;
+              if (skip && (dead || inc >= 65536u || steps >= 0x7fffu)) {
+                w.next = rho;
+                inc = 0;
+                steps = 0x7fffu;
+              }
               const uint32_t ad0 = w.k0 == fs::kNone ? 0u : (uint32_t)(((uint64_t)w.k0 * c.gA + w.next) / c.gB);
               for (uint32_t j = 0; j < 8u; ++j) {
                 uint32_t *ent = &hv[4u * (8u * rho + j)];
                 ent[0] = 4u * ho + 16u * (8u * w.next + j);
-                ent[1] = w.inc;
+                ent[1] = skip ? inc | steps << 16 : w.inc;
                 ent[2] = w.k0 == fs::kNone ? 0x80000000u : (uint32_t)((int32_t)c.s - (int32_t)w.k0);
                 ent[3] = w.k0 == fs::kNone ? 0u : ad0 - w.k0;
               }
             }
             c.hadv_off = ho;
+            c.hadv_skip = skip ? 1u : 0u;
             p->ktab.resize(ho, 0u);
             p->ktab.insert(p->ktab.end(), hv.begin(), hv.end());
           }

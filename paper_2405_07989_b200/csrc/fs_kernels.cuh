@@ -562,6 +562,32 @@ __device__ __forceinline__ void rows_slice_done(const KParams &P, EmitRows<D, B>
   }
 }
 
+// The closed-tail node step over the live-node advance table (Consts::radv_off, built for an
+// any-predicate plan when gcd(g_{d-1}, g_d) > 1: NEXT-3): one 16 B entry jumps `steps`
+// advances to the next node whose residual that gcd divides (summed quotient increments, its
+// k0); when fewer than `steps` advances are left (or the cycle holds no live node) the rest of
+// the run has no rows and the lane goes to its ascend.
+template <int D, class NodeEmit>
+__device__ __forceinline__ void fast_step_closed_live(Lane<D> &st, const Consts &c, uint32_t rtab, NodeEmit &ne) {
+  if (st.cur < 0 && st.k != 0u) {
+    uint32_t w0, w1, w2, w3;
+    asm("ld.shared.v4.u32 {%0, %1, %2, %3}, [%4];" : "=r"(w0), "=r"(w1), "=r"(w2), "=r"(w3) : "r"(rtab + 16u * st.rho));
+    (void)w2;
+    if (w3 <= st.k) {
+      st.k -= w3;
+      st.rho = w0 & ((1u << kAdvBits) - 1u);
+      st.A += w0 >> kAdvBits;
+      st.cur = (int32_t)st.A - (int32_t)w1;
+    } else {
+      st.k = 0u;
+    }
+  }
+  const bool em = st.cur >= 0;
+  const uint32_t rows = divq((uint32_t)(em ? st.cur : 0), c.dvS) + 1u;
+  ne.node(em, st, c, rows);
+  if (em) st.cur = -1;
+}
+
 __device__ __forceinline__ uint64_t bitrev_bits(uint64_t x, uint32_t bits) {
   return bits ? (__brevll(x) >> (64 - bits)) : 0ull;
 }
@@ -966,7 +992,10 @@ __device__ __forceinline__ void hc_group(Lane<D> &st, const Consts &c, uint32_t 
 
 // The histogram group over the 8-copy table (Consts::hadv_off): fields in separate words
 // (no unpacking on the ALU pipe) and a bank-group-private copy per quarter-warp lane.
-template <int D, int G, int DLS>
+// SKIP (Consts::hadv_skip, gcd(g_{d-1}, g_d) > 1, NEXT-3): each step jumps to the next live node
+// (word 1 = quotient increment | advances << 16); the cumulative advance count cum replaces
+// u + 1 in the first-row length and in the validity mask.
+template <int D, int G, int DLS, bool SKIP = false>
 __device__ __forceinline__ void hc_group8(Lane<D> &st, const Consts &c, uint32_t tab, const HcConsts &k,
                                           uint32_t &nrows) {
   if constexpr (D >= 3) {
@@ -976,18 +1005,24 @@ __device__ __forceinline__ void hc_group8(Lane<D> &st, const Consts &c, uint32_t
     // address of index l0 is base0 + dstr * (A + w3 - u): l0 = lsum0 - 1 - u + A + (ad0 - k0)
     const uint32_t bofs = st.lsum - 1u + (DLS < 0 ? (uint32_t)(-c.dl) : 0u);
     const uint32_t base0 = k.dbase + k.dstr * bofs;
-    uint32_t n = nrows;
+    uint32_t n = nrows, cum = 0;
 #pragma unroll
     for (int u = 0; u < G; ++u) {
       uint32_t w0, w1, w2, w3;
       asm("ld.shared.v4.u32 {%0, %1, %2, %3}, [%4];" : "=r"(w0), "=r"(w1), "=r"(w2), "=r"(w3) : "r"(h));
       h = w0;
-      A += w1;
+      if (SKIP) {
+        A += w1 & 0xffffu;
+        cum += w1 >> 16;
+      } else {
+        A += w1;
+      }
       const int32_t y = (int32_t)(A + w2);
       const uint32_t rows = __umulhi((uint32_t)(y > 0 ? y : 0), c.mhi);
-      if ((uint32_t)u < kk && rows != 0u) {  // valid step with rows: both updates
+      const bool ok = SKIP ? cum <= kk : (uint32_t)u < kk;
+      if (ok && rows != 0u) {  // valid step with rows: both updates
         n += rows;
-        const uint32_t a0 = base0 + k.dstr * (A + w3 - (uint32_t)u);  // l0 (t < s: l0 + s - t)
+        const uint32_t a0 = base0 + k.dstr * (A + w3 - (SKIP ? cum - 1u : (uint32_t)u));  // l0 (t < s: l0 + s - t)
         if (DLS > 0) {
           asm volatile("red.shared.add.u32 [%0], %1;" ::"r"(a0), "r"(1u) : "memory");
           asm volatile("red.shared.add.u32 [%0], %1;" ::"r"(a0 + rows * k.sstr), "r"(0xffffffffu) : "memory");
@@ -1003,7 +1038,10 @@ __device__ __forceinline__ void hc_group8(Lane<D> &st, const Consts &c, uint32_t
     nrows = n;
     st.rho = (h - tab) >> 7;
     st.A = A;
-    st.k = kk > (uint32_t)G ? kk - (uint32_t)G : 0u;
+    if (SKIP)
+      st.k = kk > cum ? kk - cum : 0u;
+    else
+      st.k = kk > (uint32_t)G ? kk - (uint32_t)G : 0u;
   }
 }
 
@@ -1325,6 +1363,10 @@ __global__ void __launch_bounds__(kBlock, (CONS == kConsRowsAny || CONS == FS_CO
         cc_group2<D, (UNROLL % 2) == 0 ? UNROLL : 2>(st, c, ktab_base + 4u * c.cadv2_off, e_count.n);
       } else if (cfast) {
         cc_group<D, UNROLL>(st, c, ktab_base + 4u * c.cadv_off, e_count.n);
+      } else if (CONS == kConsAnyClosed && KTAB && c.radv_off != 0u) {  // live nodes only (NEXT-3)
+        const uint32_t rt = ktab_base + 4u * c.radv_off;
+#pragma unroll
+        for (int u = 0; u < UNROLL; ++u) fast_step_closed_live<D>(st, c, rt, e_any);
       } else if (CONS == kConsAnyClosed) {
 #pragma unroll
         for (int u = 0; u < UNROLL; ++u) fast_step_closed<D>(st, c, kt, budget, e_any);
@@ -1332,7 +1374,14 @@ __global__ void __launch_bounds__(kBlock, (CONS == kConsRowsAny || CONS == FS_CO
         hq_group<D, FS_HQ_GROUP>(st, hq_h1, hq_bm, hq_junk, e_hcl.n);
       } else if (hfast && c.hadv_off != 0u) {
         const uint32_t htab = ktab_base + 4u * c.hadv_off;
-        if (c.dl > 0)
+        if (c.hadv_skip) {  // (gcd(g_{d-1}, g_d) > 1 implies s < g_d, t - s of either sign)
+          if (c.dl > 0)
+            hc_group8<D, UNROLL, 1, true>(st, c, htab, hck, e_hcl.n);
+          else if (c.dl < 0)
+            hc_group8<D, UNROLL, -1, true>(st, c, htab, hck, e_hcl.n);
+          else
+            hc_group8<D, UNROLL, 0, true>(st, c, htab, hck, e_hcl.n);
+        } else if (c.dl > 0)
           hc_group8<D, UNROLL, 1>(st, c, htab, hck, e_hcl.n);
         else if (c.dl < 0)
           hc_group8<D, UNROLL, -1>(st, c, htab, hck, e_hcl.n);

@@ -47,6 +47,9 @@ C5Q = Instance("C5Q", 10000, (1, 1, 2, 997, 1000))  # quick variant
 # C2's shape with a non-coprime last pair (gcd(18, 24) = 6: 5 of 6 level-L nodes have no
 # factorization) -- exercises the common-divisor skip of the materialise kernel (NEXT-3)
 C2CD = Instance("C2CD", 12000, (11, 13, 17, 18, 24))
+# ... and with the last THREE generators sharing 6 (gcd(12, 18, 24)): 5 of 6 level-(L-1)
+# subtrees (runs) are dead too -- the k >= 3 skip of the generic ascend (NEXT-3)
+C3CD = Instance("C3CD", 12000, (11, 13, 12, 18, 24))
 
 CONFIGS = {i.name: i for i in (C1, C2, C2L, C2XL, C3, C4, C5, C5Q)}
 

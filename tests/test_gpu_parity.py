@@ -518,3 +518,49 @@ def test_hist_state_form_vs_residue_form(oracle_mod, inst):
         h = hist_list(api.fs_length_set_ex(n, g, rank=r, world=3, **kw), len(want))
         tot = [a + b for a, b in zip(tot, h)]
     assert tot == want
+
+
+def _next3_instances():
+    """Non-coprime trailing generators in stream order (NEXT-3): the last two share a
+    factor (live-node walks of every closed consumer), or the last k >= 3 do (dead-subtree skip
+    in the generic ascend), for given and largest-first order."""
+    rng = random.Random(31)
+    out = [W.Instance("cd2a", 700, (11, 13, 17, 18, 24)), W.Instance("cd2b", 500, (7, 9, 10, 4, 6)),
+           W.Instance("cd3a", 600, (5, 7, 6, 9, 12)), W.Instance("cd3b", 420, (7, 5, 12, 18, 30, 24)),
+           W.Instance("cd4", 300, (9, 8, 12, 16, 20, 4)), W.Instance("cdall", 360, (6, 10, 14, 22))]
+    while len(out) < 20:
+        d = rng.randint(4, 7)
+        f = rng.choice((2, 3, 4, 6))
+        k = rng.randint(2, d - 1)
+        g = tuple([rng.randint(1, 25) for _ in range(d - k)] + [f * rng.randint(1, 8) for _ in range(k)])
+        n = rng.randint(50, 420)
+        if gf.count(n, g) <= 400000:
+            out.append(W.Instance("cdr%d" % len(out), n, g))
+    return out
+
+
+@pytest.mark.parametrize("inst", _next3_instances(), ids=ids)
+def test_next3_common_divisor_all_consumers(oracle_mod, inst):
+    """Every consumer on instances whose trailing generators share a factor: count (rows and
+    closed tails), histogram (closed: live-node table), any (closed: live-node step), and the
+    materialised rows, against the oracle; tiny slices and 3 virtual ranks for the skips."""
+    n, g = inst.n, inst.gens
+    want = oracle.run(n, g, hist_len=oracle.hist_len_for(n, g))
+    for go in (L.FS_GENORDER_GIVEN, L.FS_GENORDER_AUTO):
+        for T in (0, 1, 5):
+            for tail in (L.FS_TAIL_ROWS, L.FS_TAIL_CLOSED):
+                assert api.fs_count_ex(n, g, slice_units=T, tail=tail, gen_order=go) == want["count"], (go, T, tail)
+            h = api.fs_length_set_ex(n, g, slice_units=T, tail=L.FS_TAIL_CLOSED, gen_order=go)
+            assert hist_list(h, len(want["hist"])) == want["hist"], (go, T)
+        tot = sum(api.fs_count_ex(n, g, rank=r, world=3, tail=L.FS_TAIL_CLOSED, gen_order=go) for r in range(3))
+        assert tot == want["count"]
+        ls = [i for i, v in enumerate(want["hist"]) if v]
+        if ls:
+            for pred, arg, exp in ((L.FS_PRED_LEN_GE, ls[-1], True), (L.FS_PRED_LEN_GE, ls[-1] + 1, False),
+                                   (L.FS_PRED_LEN_LE, ls[0], True), (L.FS_PRED_LEN_EQ, ls[len(ls) // 2], True)):
+                f, wit = api.fs_any_ex(n, g, pred, arg, tail=L.FS_TAIL_CLOSED, gen_order=go, slice_units=3)
+                assert f == exp, (pred, arg)
+                if f:
+                    assert sum(a * b for a, b in zip(wit, g)) == n
+    r, off, t = api.fs_enumerate_ex(n, g, B=32)
+    assert r == want["count"] and rows_bytes(t) == oracle.rows(n, g, B=32)
