@@ -530,7 +530,9 @@ int fs_validate_and_build(fs_plan *p, uint64_t n, const uint32_t *gens, int d, i
             }
             return out;
           };
-          const uint32_t qo = ((uint32_t)p->ktab.size() + 3u) & ~3u;
+          // (128 B aligned like the kernel's dynamic shared memory: an entry address's bits 4-6
+          // are then its copy index, which the table ascend reuses)
+          const uint32_t qo = ((uint32_t)p->ktab.size() + 31u) & ~31u;
           const uint32_t q1o = qo + 32u * S;
           const uint32_t need_end = q1o + 2u * (K - 1u) * S;
           bool ok = 4ull * need_end + 16384ull <= (1ull << 16);

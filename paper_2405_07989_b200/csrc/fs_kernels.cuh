@@ -800,7 +800,7 @@ __device__ __forceinline__ void t2q_ascend(Lane<D> &st, const Consts &c, uint32_
     sync_k<D, 1>(st, budget);
     if (st.k == q2) {
       cnt += w.z;
-      st.rho = qbase_lane + (w.y & 0xffffu);
+      st.rho = (w.y & 0xffffu) + (st.rho & (16u * 7u));  // sigma_j's entry in the lane's copy
       st.A = K * (w.y >> 16);
       st.k -= w.w;
     } else {
@@ -1158,7 +1158,7 @@ __global__ void __launch_bounds__(kBlock, (CONS == kConsRowsAny || CONS == FS_CO
   constexpr int UNROLL = CONS == FS_CONSUMER_ROWS                               ? kRowsPerHalf
                          : (CONS == kConsCountClosed || CONS == kConsHistClosed) ? FS_CC_GROUP
                                                                                  : 4;
-  extern __shared__ __align__(16) unsigned char smem[];
+  extern __shared__ __align__(128) unsigned char smem[];  // (128: fs_host.cu qtab alignment)
   __shared__ unsigned int hist_guard;
   const Consts &c = P.c;
 
@@ -1174,7 +1174,8 @@ __global__ void __launch_bounds__(kBlock, (CONS == kConsRowsAny || CONS == FS_CO
   // count-only group table (closed tail): its link words get the table's shared address
   const bool cfast = KTAB && CONS == kConsCountClosed && c.cadv_off != 0 && ktab_base < 16384u;
   const bool hfast = KTAB && CONS == kConsHistClosed && c.cadv_off != 0 && P.hist_smem && ktab_base < 16384u;
-  const bool qfast = cfast && c.qtab_off != 0;  // count in state form (cq_group)
+  // count in state form (cq_group); its table ascend needs the table 128 B aligned (fs_host.cu)
+  const bool qfast = cfast && c.qtab_off != 0 && ((ktab_base + 4u * c.qtab_off) & 127u) == 0u;
   const bool t2fast = cfast && D >= 4 && c.t2_off != 0 && (!qfast || c.t2q_off != 0);
   const bool t2h = hfast && D >= 4 && c.t2_off != 0;  // histogram: one-level ascend by table
   const bool hqf = hfast && P.hist_hq && c.hq_off != 0;  // histogram in state form (hq_group)
@@ -1216,6 +1217,12 @@ __global__ void __launch_bounds__(kBlock, (CONS == kConsRowsAny || CONS == FS_CO
     if (cfast && c.t2q_off != 0u && D >= 4 && i >= c.t2q_off && i < c.t2q_off + 4u * FS_QK * c.g[D >= 4 ? D - 3 : 0] &&
         ((i - c.t2q_off) & 3u) == 0u)
       v += ktab_base;
+    // (word 1's state field 128 sigma_j becomes the address of sigma_j's copy-0 entry: the
+    // ascend adds the lane's copy offset from its current state address -- the tables fit the
+    // first 64 KB, so the 16-bit field cannot carry into Q_j)
+    if (cfast && c.t2q_off != 0u && c.qtab_off != 0u && D >= 4 && i >= c.t2q_off &&
+        i < c.t2q_off + 4u * FS_QK * c.g[D >= 4 ? D - 3 : 0] && ((i - c.t2q_off) & 3u) == 1u)
+      v += ktab_base + 4u * c.qtab_off;
     ktab_s[i] = v;
   }
   if (HISTLIKE) {

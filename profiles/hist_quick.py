@@ -22,6 +22,11 @@ for walk in (L.FS_WALK_AUTO, L.FS_WALK_RESIDUE):
     p = api.Plan(inst.n, inst.gens, L.FS_CONSUMER_HIST, tail=L.FS_TAIL_CLOSED, gen_order=L.FS_GENORDER_AUTO,
                  walk=walk, stream=stream.cuda_stream)
     out = torch.zeros(api.hist_len(inst.n, inst.gens), dtype=torch.int64, device="cuda")
+    import time
+    t0 = time.time()
+    while time.time() - t0 < 1.0:  # warm the clocks up (about 1 s of launches)
+        p.count_async(out) if hasattr(p, "count_async") and p.consumer == L.FS_CONSUMER_COUNT else p.hist_async(out)
+        torch.cuda.synchronize()
     ts = []
     for r in range(7):
         a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
