@@ -511,9 +511,11 @@ FS_HD bool needs_refill(const Lane<D> &st, uint32_t budget) {
 // steps 2-11 at an index i < L (ascend() re-solves a_{i+1}..a_L greedily), then the new
 // node's entry (one ENTRY unit).  It never emits: the node's first row, if any, is emitted
 // by the next fast_step, so every emission happens with the warp converged.
-template <int D, bool NEED_AD, int ALPHA, class KT>
+// (CD = false: without the k >= 3 dead-subtree skip -- the kernels instantiate it only in their
+// NEXT-3 variants, so the common kernels keep the short ascend)
+template <int D, bool NEED_AD, int ALPHA, bool CD = true, class KT>
 FS_HD void slow_step(Lane<D> &st, const Consts &c, const KT &kt, uint32_t &budget) {
-  if (!advance_cd<D, ALPHA>(st, c, budget)) {
+  if (!(CD ? advance_cd<D, ALPHA>(st, c, budget) : advance<D>(st, c))) {
     budget = 0;  // end of stream
     return;
   }

@@ -8,5 +8,8 @@ int fs_dispatch_any(fs_plan *p, int B, const fs::KParams &kp, cudaStream_t s, bo
 }
 
 int fs_dispatch_any_closed(fs_plan *p, int B, const fs::KParams &kp, cudaStream_t s, bool q, uint32_t *g) {
-  (void)B; return fs::dispatch_kt<fs::kConsAnyClosed, 16>(p, kp, s, q, g);
+  // (B = 32: the NEXT-3 variant -- live-node step, k >= 3 dead-subtree skip)
+  (void)B;
+  return (p->c.h > 1u && p->c.radv_off) || p->c.cd_mask ? fs::dispatch_kt<fs::kConsAnyClosed, 32>(p, kp, s, q, g)
+                                                        : fs::dispatch_kt<fs::kConsAnyClosed, 16>(p, kp, s, q, g);
 }

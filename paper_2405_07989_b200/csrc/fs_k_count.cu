@@ -10,7 +10,8 @@
 int fs_dispatch_count_closed(fs_plan *p, int B, const fs::KParams &kp, cudaStream_t s, bool q, uint32_t *g) {
   (void)B;
   // B is meaningless for a count: the B = 32 instantiation walks live nodes only (NEXT-3)
-  return p->c.cadv2_skip ? fs::dispatch_kt<fs::kConsCountClosed, 32>(p, kp, s, q, g)
+  // (B = 32: the NEXT-3 variant -- live-node walk, k >= 3 dead-subtree skip)
+  return p->c.cadv2_skip || p->c.cd_mask ? fs::dispatch_kt<fs::kConsCountClosed, 32>(p, kp, s, q, g)
                          : fs::dispatch_kt<fs::kConsCountClosed, 16>(p, kp, s, q, g);
 }
 

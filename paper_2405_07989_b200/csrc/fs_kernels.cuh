@@ -1151,6 +1151,9 @@ __global__ void __launch_bounds__(kBlock, (CONS == kConsRowsAny || CONS == FS_CO
   constexpr bool HISTLIKE = CONS == FS_CONSUMER_HIST || CONS == kConsHistClosed;
   constexpr bool ANYLIKE = CONS == FS_CONSUMER_ANY || CONS == kConsAnyClosed;
   constexpr int ALPHA = (CONS == FS_CONSUMER_ROWS || CONS == kConsRowsAny) ? 0 : 1;
+  // the closed-tail consumers' NEXT-3 variant (B = 32): live-node walks when
+  // gcd(g_{d-1}, g_d) > 1 and the k >= 3 dead-subtree skip in the ascend (Consts::cd_mask)
+  constexpr bool N3 = B == 32 && (CONS == kConsCountClosed || CONS == kConsHistClosed || CONS == kConsAnyClosed);
   constexpr int INNER = Inner<CONS>::value;
   // ROWS: a lane completes at most one ring half in kHalf / row_bytes steps, so the warp
   // flushes pending halves once per that many steps.
@@ -1370,7 +1373,7 @@ __global__ void __launch_bounds__(kBlock, (CONS == kConsRowsAny || CONS == FS_CO
         cc_group2<D, (UNROLL % 2) == 0 ? UNROLL : 2>(st, c, ktab_base + 4u * c.cadv2_off, e_count.n);
       } else if (cfast) {
         cc_group<D, UNROLL>(st, c, ktab_base + 4u * c.cadv_off, e_count.n);
-      } else if (CONS == kConsAnyClosed && KTAB && c.radv_off != 0u) {  // live nodes only (NEXT-3)
+      } else if (N3 && CONS == kConsAnyClosed && KTAB && c.radv_off != 0u) {  // live nodes only (NEXT-3)
         const uint32_t rt = ktab_base + 4u * c.radv_off;
 #pragma unroll
         for (int u = 0; u < UNROLL; ++u) fast_step_closed_live<D>(st, c, rt, e_any);
@@ -1381,7 +1384,7 @@ __global__ void __launch_bounds__(kBlock, (CONS == kConsRowsAny || CONS == FS_CO
         hq_group<D, FS_HQ_GROUP>(st, hq_h1, hq_bm, hq_junk, e_hcl.n);
       } else if (hfast && c.hadv_off != 0u) {
         const uint32_t htab = ktab_base + 4u * c.hadv_off;
-        if (c.hadv_skip) {  // (gcd(g_{d-1}, g_d) > 1 implies s < g_d, t - s of either sign)
+        if (N3 && c.hadv_skip) {  // (gcd(g_{d-1}, g_d) > 1 implies s < g_d, t - s of either sign)
           if (c.dl > 0)
             hc_group8<D, UNROLL, 1, true>(st, c, htab, hck, e_hcl.n);
           else if (c.dl < 0)
@@ -1440,7 +1443,7 @@ __global__ void __launch_bounds__(kBlock, (CONS == kConsRowsAny || CONS == FS_CO
           if (t2h && t2_can_ascend<D>(st)) {
             t2_ascend_hist<D>(st, c, t2a, q2);
           } else {
-            ok = advance_cd<D, ALPHA>(st, c, budget);
+            ok = N3 ? advance_cd<D, ALPHA>(st, c, budget) : advance<D>(st, c);
             if (t2h) t2_sync<D>(st, c, t2base, t2a, q2);
           }
           if (ok)
@@ -1469,7 +1472,7 @@ __global__ void __launch_bounds__(kBlock, (CONS == kConsRowsAny || CONS == FS_CO
             sync_k<D, ALPHA>(st, budget);
             if (qfast) enter_q<D>(st, c, qbase_lane, q1base, e_count.n);
           } else {
-          slow_step<D, NEED_AD, ALPHA>(st, c, kt, budget);
+          slow_step<D, NEED_AD, ALPHA, N3>(st, c, kt, budget);
           if (CAND) enter_candidates<D>(st, c);
           sync_k<D, ALPHA>(st, budget);
           if (cfast) acc += take_entry_rows<D>(st, c);
