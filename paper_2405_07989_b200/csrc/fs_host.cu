@@ -745,8 +745,12 @@ int fs_validate_and_build(fs_plan *p, uint64_t n, const uint32_t *gens, int d, i
   if (c.alpha == 1u && d >= 4 && !p->U.empty()) {
     const int L = d - 2;
     const uint64_t N1 = n + 1, X0 = c.u0_len;
-    uint64_t w_run = c.qtab_off ? 80 : 12;
-    if (const char *ev = getenv("FS_RUN_COST")) w_run = strtoull(ev, nullptr, 10);  // tuning experiments only
+    // (experiments: -DFS_RUN_COST=<w> at build time; the library reads no environment)
+#ifdef FS_RUN_COST
+    const uint64_t w_run = FS_RUN_COST;
+#else
+    const uint64_t w_run = c.qtab_off ? 80 : 12;
+#endif
     // CW (same layout as U): levels L-1 .. 1 in full, level 0 compactly
     std::vector<uint64_t> arr(N1);
     for (uint64_t x = 0; x <= n; ++x) arr[x] = 1;  // one node
