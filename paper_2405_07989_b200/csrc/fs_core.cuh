@@ -481,14 +481,14 @@ FS_HD uint64_t cost_boundary(const Consts &c, const uint64_t *CW, uint64_t targe
   return units;
 }
 
-// Cost target of the start of slice j of an equal-cost guided slicing of [cb, ce): S0 slices
-// of 4c, S1 of 2c, then slices of c (S2 = S - S0 - S1 of them, c = (ce - cb) / (4 S2) when
-// 4 S0 + 2 S1 = 3 S2).
-FS_HD uint64_t cost_target(uint64_t cb, uint64_t ce, uint64_t S0, uint64_t S1, uint64_t S, uint64_t j) {
-  const uint64_t S2 = S - S0 - S1;
-  const uint64_t den = 4 * S0 + 2 * S1 + S2;
-  const uint64_t f = j < S0 ? 4 * j : j < S0 + S1 ? 4 * S0 + 2 * (j - S0) : 4 * S0 + 2 * S1 + (j - S0 - S1);
-  return cb + (uint64_t)((unsigned __int128)(ce - cb) * f / den);
+// Cost target of the start of slice j of an equal-cost guided slicing of [cb, ce): P phases of
+// Lp slices, phase k's slices of cost 2^(P-1-k) c with c = (ce - cb) / (Lp (2^P - 1)).
+FS_HD uint64_t cost_target(uint64_t cb, uint64_t ce, uint64_t Lp, uint64_t P, uint64_t S, uint64_t j) {
+  // P phases of Lp slices each; phase k's slices weigh 2^(P-1-k) (S = P Lp; slice S is the end)
+  (void)S;
+  const uint64_t k = j / Lp, i = j - k * Lp;
+  const uint64_t f = k >= P ? Lp * ((1ull << P) - 1) : Lp * ((1ull << P) - (1ull << (P - k))) + i * (1ull << (P - 1 - k));
+  return cb + (uint64_t)((unsigned __int128)(ce - cb) * f / (Lp * ((1ull << P) - 1)));
 }
 
 // After unrank(): node-unit plans (alpha = 1) start at the node's entry, which is consumed

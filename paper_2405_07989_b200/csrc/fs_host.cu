@@ -804,15 +804,20 @@ int fs_validate_and_build(fs_plan *p, uint64_t n, const uint32_t *gens, int d, i
   p->num_slices = span ? ceil_div_u64(span, T) : 0;
   if (!p->CW.empty() && e.slice_units == 0 && span && e.slicing != FS_SLICES_UNIFORM) {
     // Equal-cost, guided slices (node units): the rank's cost range is cut at run starts into
-    // S0 slices of cost 4c (the first half), S1 of 2c (the next quarter) and S2 of c (the last
-    // quarter), S2 = 3 per resident lane.  Equal cost balances lanes whatever the lex region
-    // (runs are short where a_1 is large, long where it is small); the large early slices keep
-    // refills (claim + slice entry, ~100 warp instructions) rare, and when the last 4c slice is
-    // claimed there are still 6c of smaller slices per lane queued behind it.  A slice's first
+    // P = 6 phases of one slice per resident lane each, every phase's slices half the cost of the
+    // previous phase's (the first take half the rank).  Equal cost balances lanes whatever the lex
+    // region (runs are short where a_1 is large, long where it is small); the large early slices
+    // keep refills (claim + slice entry, ~100 warp instructions) at 6 per lane, and the last
+    // slices are 1/63 of a lane's work, so the tail is short (round 1 / early round 2: 3 phases of
+    // 4c, 2c, c with 12c per lane -- a 3x longer last slice; W = 8 virtual ranks of C3 lost ~0.09
+    // ms per rank to it; finer slices in all phases cost more in refills than they saved).  A slice's first
     // node prefix and its node count come from the slice-start table (fs_build_slice_starts).
     // Slices are cut at run starts only, so this needs many more runs than lanes (C5, 231 runs of
     // ~3300 nodes, keeps uniform node slices, which split runs: 0.07 ms vs 0.36 ms).
-    const uint64_t S2 = 3 * kTargetLanes;
+#ifndef FS_GUIDED_PHASES
+#define FS_GUIDED_PHASES 6  // phases of the guided slices, each slice half the cost of the last phase's
+#endif
+    const uint64_t S2 = FS_GUIDED_PHASES * kTargetLanes;
     const uint64_t runs_share = (uint64_t)((u128)p->nodes_per_level[d - 3] * (p->cost_end - p->cost_begin) /
                                            std::max<uint64_t>(1, p->CW[0]));
     // a slice's node count (< its cost + one run) must fit the kernel's 32-bit budget
@@ -821,11 +826,15 @@ int fs_validate_and_build(fs_plan *p, uint64_t n, const uint32_t *gens, int d, i
     // automatic: for the closed-tail kernels, whose per-run cost the weights model (the per-row
     // kernels keep node slices: C3 per-row count 190 ms with them, 210 ms with cost slices)
     const bool closed_kernel = e.tail == FS_TAIL_CLOSED && (consumer == FS_CONSUMER_COUNT || consumer == FS_CONSUMER_HIST);
+    // P phases of Lp slices: the first slices take half of the rank's cost (2^(P-1) / (2^P - 1)),
+    // each later phase's slices half the cost of the phase before, so the last slices are
+    // short (a short tail) while the refills stay at P per lane
+    const uint64_t P = FS_GUIDED_PHASES, Lp = std::max<uint64_t>(1, s2 / P);
     if ((forced || (closed_kernel && runs_share >= 8 * kTargetLanes)) &&
-        (p->cost_end - p->cost_begin) / s2 + n + 1024 < (1ull << 31)) {
-      p->gn0 = s2 / 2;
-      p->gn1 = s2 / 2;
-      p->num_slices = p->gn0 + p->gn1 + s2;
+        (p->cost_end - p->cost_begin) / Lp + n + 1024 < (1ull << 31)) {
+      p->gn0 = Lp;
+      p->gn1 = P;
+      p->num_slices = P * Lp;
       p->cost_slices = true;
       p->T = std::max<uint64_t>(1, span / p->num_slices);  // reported average
     }
