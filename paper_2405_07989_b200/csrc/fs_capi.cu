@@ -251,7 +251,8 @@ int fs_plan_any_async(fs_plan *p, int pred, uint64_t pred_arg, int *found_dev, u
   }
   kp.found = found_dev;
   kp.witness = witness_dev;
-  // bit-reversed claim order: every region of the lex order is sampled early (early exit)
+  // claim order from both ends, bit-reversed inside each half (fs_kernels.cuh claim_slice): every
+  // region of the lex order, and both of its ends first, are sampled early (early exit)
   uint32_t bits = 0;
   while ((1ull << bits) < kp.num_slices) ++bits;
   kp.permute = 1;
