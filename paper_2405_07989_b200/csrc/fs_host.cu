@@ -397,7 +397,9 @@ int fs_validate_and_build(fs_plan *p, uint64_t n, const uint32_t *gens, int d, i
               p->ktab.resize(hqo, 0u);
               p->ktab.insert(p->ktab.end(), hq.begin(), hq.end());
               c.hq_off = hqo;
-              c.hq_bias = c.s - 1u;
+              // shared index bias: a first row's length is >= -(s - 1) on a rowless node and >= -7
+              // - (s - 1) on the up to 7 nodes a masked block walks past a run's end (a_L < 0)
+              c.hq_bias = c.s + 8u;
             }
           }
         }
@@ -1043,8 +1045,7 @@ void host_hist_tables_slice(const fs_plan *p, const KT &ktab, fs::Lane<D> &st, u
   constexpr uint32_t K = FS_HK, C = FS_HQ_COPIES, STR = 4u * FS_HIST_REP;
   uint32_t h = 0, h1 = 0, bP = 0, bM = 0;
   auto upd = [&](uint32_t addr, int64_t v) {
-    // (the last index is the kernel's junk word for masked nodes: never a real update)
-    if (addr % STR != 0u || addr / STR + 1u >= sh.size()) {
+    if (addr % STR != 0u || addr / STR >= sh.size()) {
       bad = true;
       return;
     }
@@ -1075,10 +1076,10 @@ void host_hist_tables_slice(const fs_plan *p, const KT &ktab, fs::Lane<D> &st, u
       if (kk <= K * v) break;
       const uint32_t *w = W + h, *w1 = W + h1;
       for (uint32_t i = 0; i < K; ++i) {
-        if (K * v + i >= kk) continue;  // masked (the kernel's junk word)
         const uint32_t pm = w1[i / 2u] >> (16u * (i % 2u));
-        upd(bP + STR * (uint32_t)(int32_t)(int8_t)(pm & 0xffu), 1);
-        upd(bM + STR * (uint32_t)(int32_t)(int8_t)((pm >> 8) & 0xffu), -1);
+        const uint32_t aP = bP + STR * (uint32_t)(int32_t)(int8_t)(pm & 0xffu);
+        upd(aP, 1);  // masked nodes (past the run or slice): -1 on the same index, net zero
+        upd(K * v + i < kk ? bM + STR * (uint32_t)(int32_t)(int8_t)((pm >> 8) & 0xffu) : aP, -1);
       }
       h = w[0] / 4u;
       h1 = w[3] / 4u;
@@ -1583,8 +1584,11 @@ fs_hist_shape fs_hist_closed_shape(const fs_plan *p) {
                    ? (uint32_t)FS_HIST_REP : 1u;
   h.slen = h.diff_len + 1u;
   h.sbias = 0;
-  // (+ 1: a junk index, the target of masked nodes)
-  const uint64_t slen_hq = (uint64_t)p->c.hq_bias + p->hist_len + p->c.t + p->c.dstride + 2;
+  // (top: a node's first-row or lowest-row length is <= lsum + R_L / g_{d-1} + t; on a masked
+  // node up to 7 advances past a run's end R_L grows by up to 7 g_L: ceil(7 g_L / g_{d-1}) more)
+  const uint64_t gL = p->d >= 3 ? p->c.g[p->d - 3] : 0;
+  const uint64_t slen_hq =
+      (uint64_t)p->c.hq_bias + p->hist_len + p->c.t + p->c.dstride + (7 * gL + p->c.gA - 1) / p->c.gA + 1;
   if (p->c.hq_off && h.hist_rep == (uint32_t)FS_HIST_REP && slen_hq * FS_HIST_REP * 4 <= fs::kHistRepBytes) {
     h.hq = 1;
     h.slen = (uint32_t)slen_hq;

@@ -1073,23 +1073,24 @@ __device__ __forceinline__ void hc_group_dl(Lane<D> &st, const Consts &c, uint32
 // the next 8 puts +1 at bP + 128 P_i and -1 at bM + 128 M_i, with P_i / M_i signed bytes of the
 // entry's second vector -- per node two byte extracts (PRMT), two scaled adds (LEA) and two
 // shared reductions; no division, no multiply.  Blocks past the end of the run or slice are
-// skipped (one branch per block); inside the last block the nodes past the end are sent to
-// the lane's junk word (two selects per node), so no node needs a separate tail pass.
+// skipped (one branch per block); inside the last block a node past the end puts its -1 on its
+// own +1 index (one select per node; the shared array's margins hold those indices), so no node
+// needs a separate tail pass.
 template <int I>
-__device__ __forceinline__ void hq_node(uint32_t bP, uint32_t bM, uint32_t w, bool ok, uint32_t junk) {
+__device__ __forceinline__ void hq_node(uint32_t bP, uint32_t bM, uint32_t w, bool ok) {
   constexpr uint32_t kSelP = (2u * I) | ((2u * I + 8u) << 4) | ((2u * I + 8u) << 8) | ((2u * I + 8u) << 12);
   constexpr uint32_t kSelM = (2u * I + 1u) | ((2u * I + 9u) << 4) | ((2u * I + 9u) << 8) | ((2u * I + 9u) << 12);
   uint32_t p, m;
   asm("prmt.b32 %0, %1, 0, %2;" : "=r"(p) : "r"(w), "n"(kSelP));  // sign-extended byte 2I
   asm("prmt.b32 %0, %1, 0, %2;" : "=r"(m) : "r"(w), "n"(kSelM));  // sign-extended byte 2I + 1
-  const uint32_t aP = ok ? bP + (p << 7) : junk;
-  const uint32_t aM = ok ? bM + (m << 7) : junk;
+  const uint32_t aP = bP + (p << 7);
+  const uint32_t aM = ok ? bM + (m << 7) : aP;  // a masked node: +1 and -1 on one index
   asm volatile("red.shared.add.u32 [%0], %1;" ::"r"(aP), "r"(1u) : "memory");
   asm volatile("red.shared.add.u32 [%0], %1;" ::"r"(aM), "r"(0xffffffffu) : "memory");
 }
 
 template <int D, int G>
-__device__ __forceinline__ void hq_group(Lane<D> &st, uint32_t &h1, uint32_t &bM, uint32_t junk, uint32_t &nrows) {
+__device__ __forceinline__ void hq_group(Lane<D> &st, uint32_t &h1, uint32_t &bM, uint32_t &nrows) {
   constexpr uint32_t K = FS_HK;
   static_assert(K == 8, "two 16 B vectors per entry: 8 nodes of two signed bytes");
   static_assert(4u * FS_HIST_REP == 128u, "offsets are scaled by the 32 copies' 128 B index stride");
@@ -1101,14 +1102,14 @@ __device__ __forceinline__ void hq_group(Lane<D> &st, uint32_t &h1, uint32_t &bM
     if (kk > K * (uint32_t)v) {
       const uint4 w0 = lds128(h), w1 = lds128(hv);
       const uint32_t b = K * (uint32_t)v;
-      hq_node<0>(bP, m, w1.x, b + 0u < kk, junk);
-      hq_node<1>(bP, m, w1.x, b + 1u < kk, junk);
-      hq_node<0>(bP, m, w1.y, b + 2u < kk, junk);
-      hq_node<1>(bP, m, w1.y, b + 3u < kk, junk);
-      hq_node<0>(bP, m, w1.z, b + 4u < kk, junk);
-      hq_node<1>(bP, m, w1.z, b + 5u < kk, junk);
-      hq_node<0>(bP, m, w1.w, b + 6u < kk, junk);
-      hq_node<1>(bP, m, w1.w, b + 7u < kk, junk);
+      hq_node<0>(bP, m, w1.x, b + 0u < kk);
+      hq_node<1>(bP, m, w1.x, b + 1u < kk);
+      hq_node<0>(bP, m, w1.y, b + 2u < kk);
+      hq_node<1>(bP, m, w1.y, b + 3u < kk);
+      hq_node<0>(bP, m, w1.z, b + 4u < kk);
+      hq_node<1>(bP, m, w1.z, b + 5u < kk);
+      hq_node<0>(bP, m, w1.w, b + 6u < kk);
+      hq_node<1>(bP, m, w1.w, b + 7u < kk);
       h = w0.x;
       hv = w0.w;
       bP += w0.y;
@@ -1195,9 +1196,6 @@ __global__ void __launch_bounds__(kBlock, (CONS == kConsRowsAny || CONS == FS_CO
   const bool hqf = hfast && P.hist_hq && c.hq_off != 0;  // histogram in state form (hq_group)
   const uint32_t hq_lane = ktab_base + 4u * c.hq_off + 16u * (threadIdx.x & (FS_HQ_COPIES - 1u));
   uint32_t hq_bm = 0, hq_h1 = 0;  // state form: -1 base address (bP lives in st.A), second vector's address
-  // ... and its junk word (the last index of its copy), the target of masked nodes
-  const uint32_t hq_junk = (uint32_t)__cvta_generic_to_shared(hist_s) + 4u * (threadIdx.x & (FS_HIST_REP - 1u)) +
-                           4u * FS_HIST_REP * (P.diff_slen - 1u);
   const uint32_t t2base = ktab_base + 4u * (qfast ? c.t2q_off : c.t2_off);
   const uint32_t qbase_lane = ktab_base + 4u * c.qtab_off + 16u * (threadIdx.x & 7u);
   const uint32_t q1base = ktab_base + 4u * c.q1_off;
@@ -1392,7 +1390,7 @@ __global__ void __launch_bounds__(kBlock, (CONS == kConsRowsAny || CONS == FS_CO
 #pragma unroll
         for (int u = 0; u < UNROLL; ++u) fast_step_closed<D>(st, c, kt, budget, e_any);
       } else if (hqf) {
-        hq_group<D, FS_HQ_GROUP>(st, hq_h1, hq_bm, hq_junk, e_hcl.n);
+        hq_group<D, FS_HQ_GROUP>(st, hq_h1, hq_bm, e_hcl.n);
       } else if (hfast && c.hadv_off != 0u) {
         const uint32_t htab = ktab_base + 4u * c.hadv_off;
         if (N3 && c.hadv_skip) {  // (gcd(g_{d-1}, g_d) > 1 implies s < g_d, t - s of either sign)
