@@ -286,10 +286,10 @@ int fs_plan_enumerate_async(fs_plan *p, int B, void *out_dev, uint64_t cap) {
     kp.unit1 = p->unit_end;
     kp.starts = nullptr;  // the table holds the canonical slicing from unit_begin
   }
-  // canonical order (M1): no table -- measured slower with it (C2-XL 4.78 -> 4.97 ms, also
-  // with evict-first table loads, so not L2 pollution; cause not established), while M2
-  // (whole-warp blocks) gains (4.06 -> 3.93 ms)
-  if (p->ex.order == FS_ORDER_CANONICAL) kp.starts = nullptr;
+  // canonical order (M1): the table only with its 64-row slices (fs_host.cu); at 512 rows it
+  // measured slower (C2-XL 4.78 -> 4.97 ms, also with evict-first table loads, so not L2
+  // pollution; cause not established), while M2 (whole-warp blocks) gains (4.06 -> 3.93 ms)
+  if (p->ex.order == FS_ORDER_CANONICAL && p->T != 64) kp.starts = nullptr;
   kp.num_slices = (take + p->T - 1) / p->T;
   kp.num_claims = kp.num_slices;
   kp.rows_out = reinterpret_cast<unsigned char *>(out_dev);

@@ -56,6 +56,9 @@ constexpr uint32_t kHistRepBytes = 49152; // lane-private difference-array copie
 #ifndef FS_HQ_MAX_STATES
 #define FS_HQ_MAX_STATES 512  // g_{d-1} s bound for that table (48 FS_HQ_COPIES bytes per state)
 #endif
+#ifndef FS_M1_TABLE_MB
+#define FS_M1_TABLE_MB 1024  // slice-start table cap for canonical materialise at 64-row slices
+#endif
 #ifndef FS_HC_MINB
 #define FS_HC_MINB 1  // __launch_bounds__ min blocks per SM of the closed-tail histogram kernel (d <= 9)
 #endif

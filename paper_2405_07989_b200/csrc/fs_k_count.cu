@@ -107,7 +107,9 @@ int fs_build_slice_starts(fs_plan *p) {
   // row units: + the row offset; equal-cost slices: + the slice's node count
   const uint64_t words = p->num_slices * (uint64_t)(L + (p->c.alpha && !p->cost_slices ? 0 : 1));
   if (p->cost_slices) return build_cost_slice_starts(p, words);
-  if (words * 4u > (256ull << 20)) return FS_OK;  // the unrank path instead
+  // (at most 256 MB; canonical materialise at 64-row slices: FS_M1_TABLE_MB, fs_host.cu)
+  const bool m1 = p->consumer == FS_CONSUMER_ROWS && p->ex.order == FS_ORDER_CANONICAL && p->T == 64;
+  if (words * 4u > ((uint64_t)(m1 ? FS_M1_TABLE_MB : 256) << 20)) return FS_OK;  // the unrank path instead
   // stream-ordered allocation from the library's own memory pool on the device (created once
   // per device, thread-safe; it keeps up to 1 GB cached across plans so a one-shot fs_count does
   // not pay a synchronous cudaMalloc/cudaFree of tens of MB per call).  The device's default
