@@ -284,7 +284,11 @@ int fs_plan_enumerate_async(fs_plan *p, int B, void *out_dev, uint64_t cap) {
   if (incr) {  // the first `take` rows in increasing order = the last `take` canonical rows
     kp.unit0 = p->unit_end - take;
     kp.unit1 = p->unit_end;
-    kp.starts = nullptr;  // the table holds the canonical slicing from unit_begin
+    // the table (64-row slices) holds the mirrored slicing: entry nfull - 1 - idx for slice idx
+    if (p->T == 64 && kp.starts)
+      kp.starts_rev = (p->unit_end - p->unit_begin) / p->T;
+    else
+      kp.starts = nullptr;
   }
   // canonical order (M1): the table only with its 64-row slices (fs_host.cu); at 512 rows it
   // measured slower (C2-XL 4.78 -> 4.97 ms, also with evict-first table loads, so not L2
@@ -326,6 +330,8 @@ int fs_plan_enumerate_async(fs_plan *p, int B, void *out_dev, uint64_t cap) {
     return finish(p, fs_launch(p, fs::kConsRowsAny, B, kp, p->stream));
   }
   if (incr) {  // staged kernel in canonical order, then the rows reversed in place
+    kp.starts = nullptr;  // (a table of this plan holds the mirrored slicing)
+    kp.starts_rev = 0;
     rc = fs_launch(p, FS_CONSUMER_ROWS, B, kp, p->stream);
     if (rc != FS_OK) return rc;
     rc = fs_launch_rows_reverse(kp.rows_out, take, kp.row_bytes, p->stream);

@@ -801,13 +801,12 @@ int fs_validate_and_build(fs_plan *p, uint64_t n, const uint32_t *gens, int d, i
   // (M1): 64 rows (two 32-row flush groups per slice, so a warp's 32 segments of a flush are
   // 640 B apart), entered from the slice-start table (L + 1 words per 64 rows, +4 % bytes read)
   // when it fits FS_M1_TABLE_MB: C2-XL 4.79 -> 4.47 ms (T = 1088 -> 512 rows in round 1: 5.12
-  // -> 4.91 ms; 128 rows + table 4.62; 128 rows by unrank 5.16).  Increasing order keeps 512
-  // rows (its mirrored slices have no table; 64 rows by unrank: 6.3 vs 5.0 ms); order = any
-  // writes whole-warp blocks and keeps the larger slices (4.13 vs 4.26 ms).
+  // -> 4.91 ms; 128 rows + table 4.62; 128 rows by unrank 5.16).  Increasing order the same,
+  // from a table of its mirrored slicing (fs_build_slice_starts; 64 rows by unrank: 6.3 vs 5.0
+  // ms); order = any writes whole-warp blocks and keeps the larger slices (4.13 vs 4.26 ms).
   if (consumer == FS_CONSUMER_ROWS && e.slice_units == 0 && e.order != FS_ORDER_ANY) {
     const uint64_t t64 = ceil_div_u64(span, 64) * (uint64_t)(d - 1) * 4u;  // table bytes at T = 64
-    T = std::min<uint64_t>(T, e.order == FS_ORDER_CANONICAL && d >= 3 && t64 <= ((uint64_t)FS_M1_TABLE_MB << 20) ? 64
-                                                                                                          : 512);
+    T = std::min<uint64_t>(T, d >= 3 && t64 <= ((uint64_t)FS_M1_TABLE_MB << 20) ? 64 : 512);
   }
   if (consumer == FS_CONSUMER_ROWS) T = (T + 63) & ~63ull;  // slices start 128 B aligned
   p->T = T;

@@ -119,6 +119,7 @@ struct KParams {
   uint64_t filt_arg;
   int count_only;
   const uint32_t *starts;
+  uint64_t starts_rev;  // increasing-order materialise: the table's full slices (entry nfull - 1 - idx), else 0
   // audit (debug, count consumers with the closed tail): per-slice row counts, or nullptr
   unsigned long long *slice_counts;
 };

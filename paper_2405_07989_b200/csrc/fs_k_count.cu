@@ -108,7 +108,7 @@ int fs_build_slice_starts(fs_plan *p) {
   const uint64_t words = p->num_slices * (uint64_t)(L + (p->c.alpha && !p->cost_slices ? 0 : 1));
   if (p->cost_slices) return build_cost_slice_starts(p, words);
   // (at most 256 MB; canonical materialise at 64-row slices: FS_M1_TABLE_MB, fs_host.cu)
-  const bool m1 = p->consumer == FS_CONSUMER_ROWS && p->ex.order == FS_ORDER_CANONICAL && p->T == 64;
+  const bool m1 = p->consumer == FS_CONSUMER_ROWS && p->ex.order != FS_ORDER_ANY && p->T == 64;
   if (words * 4u > ((uint64_t)(m1 ? FS_M1_TABLE_MB : 256) << 20)) return FS_OK;  // the unrank path instead
   // stream-ordered allocation from the library's own memory pool on the device (created once
   // per device, thread-safe; it keeps up to 1 GB cached across plans so a one-shot fs_count does
@@ -133,7 +133,15 @@ int fs_build_slice_starts(fs_plan *p) {
   kp.gn0 = p->gn0;
   kp.gn1 = p->gn1;
   kp.num_slices = p->num_slices;
-  uint64_t blocks = (p->num_slices + 255) / 256;
+  if (m1 && p->ex.order == FS_ORDER_INCREASING) {
+    // the mirrored slicing of increasing order: its full slices end at unit_end, so entry k
+    // starts at unit_begin + (span mod T) + k T (the batch kernel reads entry nfull - 1 - idx)
+    const uint64_t span = p->unit_end - p->unit_begin;
+    kp.unit0 = p->unit_begin + span % p->T;
+    kp.num_slices = span / p->T;
+    if (kp.num_slices == 0) return FS_OK;
+  }
+  uint64_t blocks = (kp.num_slices + 255) / 256;
   if (blocks > 148ull * 16) blocks = 148ull * 16;
   switch (p->d) {
 #define FS_CASE(DD)                                                                                       \

@@ -280,9 +280,12 @@ __global__ void __launch_bounds__(kRbBlock, 1) fs_rows_batch_kernel(const KParam
     if (live) {
       // REV: slice idx = output rows [idx T, idx T + T) = canonical rows E - idx T - T ..
       const uint64_t u = REV ? P.unit1 - (idx + 1) * P.T : P.unit0 + idx * P.T;
-      // (the slice-start table holds the canonical slicing; REV anchors slices at the end)
-      const uint64_t off = (P.starts && !REV) ? start_from_table<D, true>(st, c, kt, P.starts + idx * (uint64_t)starts_stride<D>(c))
-                                              : unrank<D, true>(st, c, kt, u);
+      // (the slice-start table holds the canonical slicing, or for REV the mirrored one: its
+      // full slices end at unit_end, slice idx is entry starts_rev - 1 - idx)
+      const uint64_t te = REV ? P.starts_rev - 1u - idx : idx;
+      const uint64_t off = (P.starts && (!REV || P.starts_rev))
+                               ? start_from_table<D, true>(st, c, kt, P.starts + te * (uint64_t)starts_stride<D>(c))
+                               : unrank<D, true>(st, c, kt, u);
       st.cur -= (int32_t)((uint32_t)off * s);  // row units: skip to row `off` of the node
       ad = rb_solve_ad<D>(st, c);
     } else {
