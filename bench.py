@@ -482,7 +482,9 @@ def main():
                      "peak_source": ("measured: best INT32 microbenchmark (fs_micro.cu)" if measured_tops else
                                      "derived: 128 int lane-ops/clk/SM x 148 SMs x %.0f MHz" % sm_max),
                      "derived_issue_peak": derived_tops, "frac_of_derived": achieved / derived_tops,
-                     "ops_per_launch": ops, "ops_model": OPS_MODEL_DOC, "kernel_ms": ms_kern},
+                     "ops_per_launch": ops, "ops_model": OPS_MODEL_DOC, "kernel_ms": ms_kern,
+                     # (the counters are for the whole one-GPU launch)
+                     "executed": _executed(args.workload, ms_kern, peak_tops, derived_tops) if world == 1 else None},
         "gpu_launches": int(launches),
         "microbench": mb,
         "clocks": clocks,
@@ -549,6 +551,26 @@ def _time_ms(fn, stream, reps, barrier, max_over_ranks):
         torch.cuda.synchronize()
         ts.append(a.elapsed_time(b))
     return max_over_ranks(statistics.median(ts))
+
+
+def _executed(key, ms, peak_tops, issue_tops):
+    """Executed lane-instructions per launch of the same build (profiles/counters.json, from one
+    `ncu --set full` capture: sm__sass_thread_inst_executed_op_integer_pred_on.sum and all
+    sass thread instructions) over the kernel time measured here: the counter-based INT32 and
+    issue fractions beside the algorithmic one."""
+    prof = os.path.join(ROOT, "profiles", "counters.json")
+    try:
+        c = json.load(open(prof)).get(key)
+    except Exception:
+        c = None
+    if not c or not ms:
+        return None
+    s = ms / 1e3
+    return {"integer_lane_inst": c["integer_lane_inst"], "lane_inst": c["lane_inst"], "source": c["source"],
+            "int_tops": c["integer_lane_inst"] / s / 1e12, "frac_int": c["integer_lane_inst"] / s / 1e12 / peak_tops,
+            "frac_int_of_issue_peak": c["integer_lane_inst"] / s / 1e12 / issue_tops,
+            "frac_all": c["lane_inst"] / s / 1e12 / peak_tops,
+            "frac_all_of_issue_peak": c["lane_inst"] / s / 1e12 / issue_tops}
 
 
 def _traffic(key):
