@@ -155,16 +155,27 @@ enum { FS_WALK_AUTO = 0, FS_WALK_RESIDUE = 1 };
  * variants run exactly the configuration their fs_exec_t asks for.
  * --------------------------------------------------------------------------------- */
 
-/* |Z(n, gens)| into *count_out (host). */
+/* |Z(n, gens)| into *count_out (host).  Z(n, g) = {a in N^d : sum_i a_i g_i = n} is the
+ * factorization set of PAPER.md:29-31 (Sec. 1); the count is the paper's "incrementing a
+ * counter" consumer of the lexicographic stream (Sec. 2), over the stream of Alg. 3.1
+ * with the modulo optimisation and disjoint bounded slices (P:196-200,
+ * Sec. 4).  Errors: FS_EINVAL (d < 1 or > 16, gens NULL, a g_i = 0, count_out NULL),
+ * FS_ERANGE (n + max g >= 2^31, |Z| >= 2^63), FS_ECUDA / FS_ENODEV / FS_ENOMEM. */
 int fs_count(uint64_t n, const uint32_t *gens, int d, uint64_t *count_out);
 
 /* hist_dev[l] = #{a in Z : sum_i a_i = l} for l = 0 .. floor(n / min g); entries beyond
  * that up to hist_cap are zeroed.  hist_dev: device uint64[hist_cap],
- * hist_cap >= floor(n / min g) + 1 (else FS_EINVAL). */
+ * hist_cap >= floor(n / min g) + 1 (else FS_EINVAL).  The length set of the north_star
+ * ("length" = sum a_i; the paper names no length consumer -- a counter per
+ * length), over the same stream and slices as fs_count.  Errors as fs_count. */
 int fs_length_set(uint64_t n, const uint32_t *gens, int d, uint64_t *hist_dev, uint64_t hist_cap);
 
 /* *found_out = 1 iff some a in Z satisfies pred; if so and witness_or_null != NULL, one
- * such a (d host uint32; WHICH witness is unspecified) is written there. */
+ * such a (d host uint32; WHICH witness is unspecified) is written there.  The paper's
+ * "setting a boolean variable based on a predicate" consumer, with early exit: slices
+ * are claimed from both ends of the lex order inward (P:196-200 slices).  pred: FS_PRED_*;
+ * pred_arg: the length bound, or (i << 32) | k for a_i >= k.  Errors as fs_count, plus
+ * FS_EINVAL for an unknown pred or found_out NULL. */
 int fs_any(uint64_t n, const uint32_t *gens, int d, int pred, uint64_t pred_arg,
            int *found_out, uint32_t *witness_or_null);
 
@@ -172,7 +183,11 @@ int fs_any(uint64_t n, const uint32_t *gens, int d, int pred, uint64_t pred_arg,
  * out_dev: row-major, d coordinates per row, little-endian uint16 (B = 16) or uint32
  * (B = 32), no padding (row r at byte r * d * B/8).  Returns |Z| (>= 0, snprintf
  * convention: truncation is not an error) or an FS_E* code.  out_dev must be 16-byte
- * aligned. */
+ * aligned (device memory, caller-owned).  The paper's "saving the factorizations" consumer
+ * (its per-thread buffers, are replaced by exact DP row offsets); the order
+ * is the paper's decreasing lexicographic order.  Errors as fs_count, plus FS_EINVAL
+ * for B not 16 | 32 or out_dev NULL with cap > 0, FS_ERANGE for B = 16 with a coordinate
+ * above 65535. */
 int64_t fs_enumerate(uint64_t n, const uint32_t *gens, int d, int B, void *out_dev, uint64_t cap);
 
 /* ---------------------------------------------------------------------------------
