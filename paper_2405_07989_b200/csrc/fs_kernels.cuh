@@ -19,17 +19,52 @@
 
 namespace fs {
 
+// FS_CHECK builds (tests only; compute-sanitizer is closed on the GPU pool): every shared-memory
+// table load / store / reduction of the kernels is checked against the CTA's dynamic shared
+// memory and every global row store against the launch's output range; a violation traps.
+#ifdef FS_CHECK
+}  // namespace fs
+#include <cstdio>
+namespace fs {
+extern __shared__ __align__(128) unsigned char fs_chk_dyn[];
+__device__ __forceinline__ void fs_chk_smem(uint32_t a, uint32_t n, int line) {
+  const uint32_t lo = (uint32_t)__cvta_generic_to_shared(fs_chk_dyn);
+  uint32_t sz;
+  asm("mov.u32 %0, %%dynamic_smem_size;" : "=r"(sz));
+  if (a < lo || a + n > lo + sz) {
+    printf("FS_CHECK shared [%u, +%u) outside [%u, %u) at line %d (block %d thread %d)\n", a, n, lo, lo + sz, line,
+           (int)blockIdx.x, (int)threadIdx.x);
+    __trap();
+  }
+}
+__device__ __forceinline__ void fs_chk_gmem(const void *p, const void *lo, uint64_t bytes, uint32_t n, int line) {
+  const char *q = static_cast<const char *>(p), *b = static_cast<const char *>(lo);
+  if (q < b || q + n > b + bytes) {
+    printf("FS_CHECK global offset %lld (+%u) outside [0, %llu) at line %d\n", (long long)(q - b), n,
+           (unsigned long long)bytes, line);
+    __trap();
+  }
+}
+#define FS_CHK_SMEM(a, n) fs_chk_smem((uint32_t)(a), (n), __LINE__)
+#define FS_CHK_GMEM(p, lo, bytes, n) fs_chk_gmem((p), (lo), (bytes), (n), __LINE__)
+#else
+#define FS_CHK_SMEM(a, n) ((void)0)
+#define FS_CHK_GMEM(p, lo, bytes, n) ((void)0)
+#endif
+
 // node tables in shared memory (copied once per CTA)
 struct KTabSmem {
   uint32_t base;  // shared-window address of the k0 table
   uint32_t adv;   // shared-window address of the advance table (8 B aligned)
   __device__ __forceinline__ uint32_t operator()(uint32_t rho, const Consts &) const {
     uint32_t v;
+    FS_CHK_SMEM(base + rho * 4u, 4);
     asm("ld.shared.u32 %0, [%1];" : "=r"(v) : "r"(base + rho * 4u));
     return v;
   }
   __device__ __forceinline__ Adv step(uint32_t rho, const Consts &) const {
     uint32_t w0, w1;
+    FS_CHK_SMEM(adv + rho * 8u, 8);
     asm("ld.shared.v2.u32 {%0, %1}, [%2];" : "=r"(w0), "=r"(w1) : "r"(adv + rho * 8u));
     return adv_unpack(w0, w1);
   }
@@ -151,6 +186,8 @@ struct EmitHistClosed {
     uint32_t lo, hi, v;
     hist_diff_updates<D>(st, c, rows, lo, hi, v);
     if (smem) {
+      FS_CHK_SMEM(__cvta_generic_to_shared(&diff[lo * rep]), 4);
+      FS_CHK_SMEM(__cvta_generic_to_shared(&diff[hi * rep]), 4);
       atomicAdd(&diff[lo * rep], v);
       atomicAdd(&diff[hi * rep], 0u - v);
     } else {
@@ -170,9 +207,10 @@ struct EmitHist {
   __device__ __forceinline__ void cond(bool em, const Lane<D> &st, const Consts &c) {
     if (!em) return;
     const uint32_t l = cur_lsum<D>(st) + (uint32_t)st.cur + row_ad<D>(st, c);  // length = sum_i a_i
-    if (smem)
+    if (smem) {
+      FS_CHK_SMEM(__cvta_generic_to_shared(&bins[l]), 4);
       atomicAdd(&bins[l], 1u);
-    else
+    } else
       atomicAdd(&gbins[l], 1ull);
     ++n;
   }
@@ -340,18 +378,22 @@ __device__ __forceinline__ uint32_t lanemask_lt() {
 #endif
 // shared-memory stores/loads by 32-bit shared-window address
 __device__ __forceinline__ void sts16(uint32_t a, uint32_t v) {
+  FS_CHK_SMEM(a, 2);
   asm volatile("st.shared.u16 [%0], %1;" ::"r"(a), "h"((unsigned short)v) : "memory");
 }
 __device__ __forceinline__ void sts32(uint32_t a, uint32_t v) {
+  FS_CHK_SMEM(a, 4);
   asm volatile("st.shared.u32 [%0], %1;" ::"r"(a), "r"(v) : "memory");
 }
 __device__ __forceinline__ uint4 lds128(uint32_t a) {
   uint4 v;
+  FS_CHK_SMEM(a, 16);
   asm volatile("ld.shared.v4.u32 {%0, %1, %2, %3}, [%4];" : "=r"(v.x), "=r"(v.y), "=r"(v.z), "=r"(v.w) : "r"(a) : "memory");
   return v;
 }
 __device__ __forceinline__ uint32_t lds16(uint32_t a) {
   unsigned short v;
+  FS_CHK_SMEM(a, 2);
   asm volatile("ld.shared.u16 %0, [%1];" : "=h"(v) : "r"(a) : "memory");
   return v;
 }
@@ -571,6 +613,7 @@ template <int D, class NodeEmit>
 __device__ __forceinline__ void fast_step_closed_live(Lane<D> &st, const Consts &c, uint32_t rtab, NodeEmit &ne) {
   if (st.cur < 0 && st.k != 0u) {
     uint32_t w0, w1, w2, w3;
+    FS_CHK_SMEM(rtab + 16u * st.rho, 16);
     asm("ld.shared.v4.u32 {%0, %1, %2, %3}, [%4];" : "=r"(w0), "=r"(w1), "=r"(w2), "=r"(w3) : "r"(rtab + 16u * st.rho));
     (void)w2;
     if (w3 <= st.k) {
@@ -745,6 +788,7 @@ __device__ __forceinline__ void enter_q_from(Lane<D> &st, uint32_t sig128, uint3
   const uint32_t r = st.k & (K - 1u);
   if (r) {
     uint32_t w0, w1;
+    FS_CHK_SMEM(q1base + 8u * ((K - 1u) * (sig128 >> 7) + r - 1u), 8);
     asm("ld.shared.v2.u32 {%0, %1}, [%2];"
         : "=r"(w0), "=r"(w1)
         : "r"(q1base + 8u * ((K - 1u) * (sig128 >> 7) + r - 1u)));
@@ -774,6 +818,7 @@ __device__ __forceinline__ void cq_group(Lane<D> &st, uint32_t &cnt) {
 #pragma unroll
   for (int v = 0; v < G / (int)K; ++v) {
     uint32_t w0, w1, w2, w3;
+    FS_CHK_SMEM(h, 16);
     asm("ld.shared.v4.u32 {%0, %1, %2, %3}, [%4];" : "=r"(w0), "=r"(w1), "=r"(w2), "=r"(w3) : "r"(h));
     (void)w3;
     h = w0;
@@ -819,6 +864,7 @@ __device__ __forceinline__ void t2q_ascend(Lane<D> &st, const Consts &c, uint32_
       const uint32_t A0 = divq(r2, c.dvA), rho0 = r2 - A0 * c.gA;
       const uint32_t q0 = divq(A0, c.dvS), a0 = A0 - q0 * c.s;
       uint32_t k0;
+      FS_CHK_SMEM(ktab_base + 4u * rho0, 4);
       asm("ld.shared.u32 %0, [%1];" : "=r"(k0) : "r"(ktab_base + 4u * rho0));  // k0 table
       cnt += q0 + (a0 >= k0 ? 1u : 0u);
       enter_q_from<D>(st, 128u * (rho0 * c.s + a0), q0, qbase_lane, q1base, cnt);
@@ -836,6 +882,7 @@ __device__ __forceinline__ void cc_group(Lane<D> &st, const Consts &c, uint32_t 
 #pragma unroll
     for (int u = 0; u < G; ++u) {
       uint32_t w0, w1;
+      FS_CHK_SMEM(h, 8);
       asm("ld.shared.v2.u32 {%0, %1}, [%2];" : "=r"(w0), "=r"(w1) : "r"(h));
       h = w0 & ((1u << kCAdvShift) - 1u);
       A += w0 >> kCAdvShift;
@@ -872,7 +919,9 @@ __device__ __forceinline__ void cc_group2_skip(Lane<D> &st, const Consts &c, uin
 #pragma unroll
     for (int v = 0; v < G / 2; ++v) {
       uint32_t w0, w1, w2, w3, w4, w5, w6, w7;
+      FS_CHK_SMEM(h, 16);
       asm("ld.shared.v4.u32 {%0, %1, %2, %3}, [%4];" : "=r"(w0), "=r"(w1), "=r"(w2), "=r"(w3) : "r"(h));
+      FS_CHK_SMEM(h + 16u, 16);
       asm("ld.shared.v4.u32 {%0, %1, %2, %3}, [%4];" : "=r"(w4), "=r"(w5), "=r"(w6), "=r"(w7) : "r"(h + 16u));
       (void)w6;
       (void)w7;
@@ -904,6 +953,7 @@ __device__ __forceinline__ void cc_group2(Lane<D> &st, const Consts &c, uint32_t
 #pragma unroll
     for (int v = 0; v < G / 2; ++v) {
       uint32_t w0, w1, w2, w3;
+      FS_CHK_SMEM(h, 16);
       asm("ld.shared.v4.u32 {%0, %1, %2, %3}, [%4];" : "=r"(w0), "=r"(w1), "=r"(w2), "=r"(w3) : "r"(h));
       h = w0;  // the link alone (no mask): the ALU pipe is the busy one
       int32_t x1 = (int32_t)(A + w1), x2 = (int32_t)(A + w2);
@@ -967,11 +1017,13 @@ __device__ __forceinline__ void hc_group(Lane<D> &st, const Consts &c, uint32_t 
       uint32_t w0, w1, w2;
       if (PACKED) {
         uint32_t p1;
+        FS_CHK_SMEM(h, 8);
         asm("ld.shared.v2.u32 {%0, %1}, [%2];" : "=r"(w0), "=r"(p1) : "r"(h));
         w1 = p1 & 0xffffu;  // s - k0 >= 1: no residue lacks a row
         w2 = p1 >> 16;      // ad0 - k0 + 2^15
       } else {
         uint32_t w3;
+        FS_CHK_SMEM(h, 16);
         asm("ld.shared.v4.u32 {%0, %1, %2, %3}, [%4];" : "=r"(w0), "=r"(w1), "=r"(w2), "=r"(w3) : "r"(h));
         (void)w3;
       }
@@ -983,13 +1035,19 @@ __device__ __forceinline__ void hc_group(Lane<D> &st, const Consts &c, uint32_t 
         n += rows;
         const uint32_t a0 = base0 + k.dstr * (A + w2 - (uint32_t)u);  // l0 (t < s: l0 + s - t)
         if (DLS > 0) {
+          FS_CHK_SMEM(a0, 4);
           asm volatile("red.shared.add.u32 [%0], %1;" ::"r"(a0), "r"(1u) : "memory");
+          FS_CHK_SMEM(a0 + rows * k.sstr, 4);
           asm volatile("red.shared.add.u32 [%0], %1;" ::"r"(a0 + rows * k.sstr), "r"(0xffffffffu) : "memory");
         } else if (DLS < 0) {
+          FS_CHK_SMEM(a0 - rows * k.sstr, 4);
           asm volatile("red.shared.add.u32 [%0], %1;" ::"r"(a0 - rows * k.sstr), "r"(1u) : "memory");
+          FS_CHK_SMEM(a0, 4);
           asm volatile("red.shared.add.u32 [%0], %1;" ::"r"(a0), "r"(0xffffffffu) : "memory");
         } else {
+          FS_CHK_SMEM(a0, 4);
           asm volatile("red.shared.add.u32 [%0], %1;" ::"r"(a0), "r"(rows) : "memory");
+          FS_CHK_SMEM(a0 + k.dstr, 4);
           asm volatile("red.shared.add.u32 [%0], %1;" ::"r"(a0 + k.dstr), "r"(0u - rows) : "memory");
         }
       }
@@ -1020,6 +1078,7 @@ __device__ __forceinline__ void hc_group8(Lane<D> &st, const Consts &c, uint32_t
 #pragma unroll
     for (int u = 0; u < G; ++u) {
       uint32_t w0, w1, w2, w3;
+      FS_CHK_SMEM(h, 16);
       asm("ld.shared.v4.u32 {%0, %1, %2, %3}, [%4];" : "=r"(w0), "=r"(w1), "=r"(w2), "=r"(w3) : "r"(h));
       h = w0;
       if (SKIP) {
@@ -1035,13 +1094,19 @@ __device__ __forceinline__ void hc_group8(Lane<D> &st, const Consts &c, uint32_t
         n += rows;
         const uint32_t a0 = base0 + k.dstr * (A + w3 - (SKIP ? cum - 1u : (uint32_t)u));  // l0 (t < s: l0 + s - t)
         if (DLS > 0) {
+          FS_CHK_SMEM(a0, 4);
           asm volatile("red.shared.add.u32 [%0], %1;" ::"r"(a0), "r"(1u) : "memory");
+          FS_CHK_SMEM(a0 + rows * k.sstr, 4);
           asm volatile("red.shared.add.u32 [%0], %1;" ::"r"(a0 + rows * k.sstr), "r"(0xffffffffu) : "memory");
         } else if (DLS < 0) {
+          FS_CHK_SMEM(a0 - rows * k.sstr, 4);
           asm volatile("red.shared.add.u32 [%0], %1;" ::"r"(a0 - rows * k.sstr), "r"(1u) : "memory");
+          FS_CHK_SMEM(a0, 4);
           asm volatile("red.shared.add.u32 [%0], %1;" ::"r"(a0), "r"(0xffffffffu) : "memory");
         } else {
+          FS_CHK_SMEM(a0, 4);
           asm volatile("red.shared.add.u32 [%0], %1;" ::"r"(a0), "r"(rows) : "memory");
+          FS_CHK_SMEM(a0 + k.dstr, 4);
           asm volatile("red.shared.add.u32 [%0], %1;" ::"r"(a0 + k.dstr), "r"(0u - rows) : "memory");
         }
       }
@@ -1085,7 +1150,9 @@ __device__ __forceinline__ void hq_node(uint32_t bP, uint32_t bM, uint32_t w, bo
   asm("prmt.b32 %0, %1, 0, %2;" : "=r"(m) : "r"(w), "n"(kSelM));  // sign-extended byte 2I + 1
   const uint32_t aP = bP + (p << 7);
   const uint32_t aM = ok ? bM + (m << 7) : aP;  // a masked node: +1 and -1 on one index
+  FS_CHK_SMEM(aP, 4);
   asm volatile("red.shared.add.u32 [%0], %1;" ::"r"(aP), "r"(1u) : "memory");
+  FS_CHK_SMEM(aM, 4);
   asm volatile("red.shared.add.u32 [%0], %1;" ::"r"(aM), "r"(0xffffffffu) : "memory");
 }
 

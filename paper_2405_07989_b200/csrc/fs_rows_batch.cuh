@@ -69,10 +69,12 @@ struct RowsBatchGeom {
 };
 
 __device__ __forceinline__ void sts128(uint32_t a, uint32_t x, uint32_t y, uint32_t z, uint32_t w) {
+  FS_CHK_SMEM(a, 16);
   asm volatile("st.shared.v4.u32 [%0], {%1, %2, %3, %4};" ::"r"(a), "r"(x), "r"(y), "r"(z), "r"(w) : "memory");
 }
 __device__ __forceinline__ uint4 lds128_nv(uint32_t a) {
   uint4 v;
+  FS_CHK_SMEM(a, 16);
   asm volatile("ld.shared.v4.u32 {%0, %1, %2, %3}, [%4];" : "=r"(v.x), "=r"(v.y), "=r"(v.z), "=r"(v.w) : "r"(a));
   return v;
 }
@@ -221,7 +223,7 @@ __global__ void __launch_bounds__(kRbBlock, 1) fs_rows_batch_kernel(const KParam
   using G = RowsBatchGeom<D, B>;
   constexpr bool ANY = MODE == 1, REV = MODE == 2;
   constexpr int L = D - 2;
-  extern __shared__ __align__(16) unsigned char smem[];
+  extern __shared__ __align__(128) unsigned char smem[];  // (128: the same start as every kernel's dynamic array)
   const Consts &c = P.c;
   uint32_t *ktab_s = reinterpret_cast<uint32_t *>(smem);
   const uint32_t kt_words = (c.ktab_len + 3u) & ~3u;
@@ -265,6 +267,9 @@ __global__ void __launch_bounds__(kRbBlock, 1) fs_rows_batch_kernel(const KParam
   uint32_t ad = 0;
   typename RA::Ent wn = ra.load(0u, c);
   const uint32_t groups = (uint32_t)(P.T / (uint64_t)G::GR);
+#ifdef FS_CHECK
+  const uint64_t out_bytes = (ANY ? P.rank_rows : P.unit1 - P.unit0) * (uint64_t)G::RB;  // (FS_CHECK)
+#endif
 
 
   for (;;) {
@@ -384,10 +389,13 @@ __global__ void __launch_bounds__(kRbBlock, 1) fs_rows_batch_kernel(const KParam
           for (int ph = 0; ph < G::NPH; ++ph) {
             const uint32_t b = blk * kBStep + (uint32_t)((32 * ph) / G::C);
             const uint4 v = lds128_nv(wstage + b * G::STRIDE + so[G::kPhase ? ph : 0]);
-            if (ANY)
+            if (ANY) {
+              FS_CHK_GMEM(gdst + 512u * (blk * G::NPH + (uint32_t)ph), P.rows_out, out_bytes, 16);
               __stcs(reinterpret_cast<uint4 *>(gdst + 512u * (blk * G::NPH + (uint32_t)ph)), v);
-            else
+            } else {
+              FS_CHK_GMEM(gdst + b * SS + go[G::kPhase ? ph : 0], P.rows_out, out_bytes, 16);
               __stcs(reinterpret_cast<uint4 *>(gdst + b * SS + go[G::kPhase ? ph : 0]), v);
+            }
           }
         }
       } else if (ANY) {
@@ -396,7 +404,10 @@ __global__ void __launch_bounds__(kRbBlock, 1) fs_rows_batch_kernel(const KParam
         for (int it = 0; it < G::C; ++it) {
           const uint32_t q = (uint32_t)it * 32u + (uint32_t)lane;
           const uint32_t l = q / (uint32_t)G::C, part = q - l * (uint32_t)G::C;
-          if (l < nlive) __stcs(dst + q, lds128_nv(wstage + l * G::STRIDE + part * 16u));
+          if (l < nlive) {
+            FS_CHK_GMEM(dst + q, P.rows_out, out_bytes, 16);
+            __stcs(dst + q, lds128_nv(wstage + l * G::STRIDE + part * 16u));
+          }
         }
       } else {
         // REV: group grp of slice j = output rows [jT + T - (grp+1) GR, jT + T - grp GR)
@@ -406,8 +417,10 @@ __global__ void __launch_bounds__(kRbBlock, 1) fs_rows_batch_kernel(const KParam
         for (int it = 0; it < G::C; ++it) {
           const uint32_t q = (uint32_t)it * 32u + (uint32_t)lane;
           const uint32_t l = q / (uint32_t)G::C, part = q - l * (uint32_t)G::C;
-          if (l < nlive)
+          if (l < nlive) {
+            FS_CHK_GMEM(dst + l * SS + part * 16u, P.rows_out, out_bytes, 16);
             __stcs(reinterpret_cast<uint4 *>(dst + l * SS + part * 16u), lds128_nv(wstage + l * G::STRIDE + part * 16u));
+          }
         }
       }
       __syncwarp();
