@@ -45,6 +45,9 @@ int fsdbg_unrank(const fs_plan *plan, uint64_t unit, uint32_t *prefix_out, int64
  * quotient they produce for x (x < 2^31). */
 int fsdbg_magic(uint32_t g, uint32_t *m_out, uint32_t *sh_out);
 uint32_t fsdbg_magic_div(uint32_t x, uint32_t g);
+/* The any-predicate's claim order (fs_core.cuh claim_slice): the slice claim idx maps to, of S
+ * slices with 2^bits >= S claims; ~0 for a claim that maps to no slice. */
+uint64_t fsdbg_claim_slice(uint64_t idx, uint32_t bits, uint64_t S);
 
 /* Roofline microbenchmarks on the current device.  kind 0: IADD3 chains, 1: IMAD chains,
  * 2: 1:1 IADD3/IMAD mix, 3: LOP3 chains -> *result_out = INT32 lane-ops per clock per SM

@@ -103,6 +103,7 @@ EXPORTS = {
     "fsdbg_unrank": (ctypes.c_int, [vp, u64, u32p, ctypes.POINTER(ctypes.c_int64)]),
     "fsdbg_magic": (ctypes.c_int, [ctypes.c_uint32, u32p, u32p]),
     "fsdbg_magic_div": (ctypes.c_uint32, [ctypes.c_uint32, ctypes.c_uint32]),
+    "fsdbg_claim_slice": (ctypes.c_uint64, [ctypes.c_uint64, ctypes.c_uint32, ctypes.c_uint64]),
     "fsdbg_total_launches": (ctypes.c_uint64, []),
     "fsdbg_count_slices": (ctypes.c_int, [vp, vp, vp]),
     "fsdbg_slice_start": (ctypes.c_int, [vp, u64, u64p, u32p]),

@@ -481,6 +481,27 @@ FS_HD uint64_t cost_boundary(const Consts &c, const uint64_t *CW, uint64_t targe
   return units;
 }
 
+FS_HD uint64_t bitrev_bits(uint64_t x, uint32_t bits) {
+#ifdef __CUDA_ARCH__
+  return bits ? (__brevll(x) >> (64 - bits)) : 0ull;
+#else
+  uint64_t r = 0;
+  for (uint32_t i = 0; i < bits; ++i) r |= ((x >> i) & 1ull) << (bits - 1u - i);
+  return r;
+#endif
+}
+
+// Any-predicate claim order (KParams::permute): both ends of the lex order early.  Even claims
+// walk the front half of the S slices in bit-reversed order, odd claims the back half mirrored
+// -- claim 0 is the lex-first slice, claim 1 the lex-last, then the middles -- so a witness
+// near either end (C5 P_first / P_late) is met in the first wave and every region is sampled
+// early.  A bijection of [0, S) over the 2^bits claims; the rest map to ~0 (skipped).
+FS_HD uint64_t claim_slice(uint64_t idx, uint32_t bits, uint64_t S) {
+  const uint64_t j = bitrev_bits(idx >> 1, bits ? bits - 1u : 0u);
+  if (idx & 1ull) return j < (S >> 1) ? S - 1ull - j : ~0ull;
+  return j < ((S + 1ull) >> 1) ? j : ~0ull;
+}
+
 // Cost target of the start of slice j of an equal-cost guided slicing of [cb, ce): P phases of
 // Lp slices, phase k's slices of cost 2^(P-1-k) c with c = (ce - cb) / (Lp (2^P - 1)).
 FS_HD uint64_t cost_target(uint64_t cb, uint64_t ce, uint64_t Lp, uint64_t P, uint64_t S, uint64_t j) {

@@ -1574,6 +1574,7 @@ extern "C" int fsdbg_magic(uint32_t g, uint32_t *m_out, uint32_t *sh_out) {
 }
 
 extern "C" uint32_t fsdbg_magic_div(uint32_t x, uint32_t g) { return fs::divq(x, fs_make_div(g)); }
+extern "C" uint64_t fsdbg_claim_slice(uint64_t idx, uint32_t bits, uint64_t S) { return fs::claim_slice(idx, bits, S); }
 
 // The closed-tail histogram's launch shape.  32-bit shared difference bins only while one
 // inner-loop iteration of a CTA (256 lanes x FS_CC_GROUP nodes, <= 2^29 at < 2^17 rows per node)

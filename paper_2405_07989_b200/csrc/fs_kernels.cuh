@@ -631,20 +631,6 @@ __device__ __forceinline__ void fast_step_closed_live(Lane<D> &st, const Consts 
   if (em) st.cur = -1;
 }
 
-__device__ __forceinline__ uint64_t bitrev_bits(uint64_t x, uint32_t bits) {
-  return bits ? (__brevll(x) >> (64 - bits)) : 0ull;
-}
-
-// Any-predicate claim order (KParams::permute): both ends of the lex order early.  Even claims
-// walk the front half of the S slices in bit-reversed order, odd claims the back half mirrored
-// -- claim 0 is the lex-first slice, claim 1 the lex-last, then the middles -- so a witness
-// near either end (C5 P_first / P_late) is met in the first wave and every region is sampled
-// early.  A bijection of [0, S) over the 2^bits claims; the rest map to ~0 (skipped).
-__device__ __forceinline__ uint64_t claim_slice(uint64_t idx, uint32_t bits, uint64_t S) {
-  const uint64_t j = bitrev_bits(idx >> 1, bits ? bits - 1u : 0u);
-  if (idx & 1ull) return j < (S >> 1) ? S - 1ull - j : ~0ull;
-  return j < ((S + 1ull) >> 1) ? j : ~0ull;
-}
 
 // Count with the closed tail, group form (Consts::cadv_off != 0): the entered node's rows
 // are taken at once, so a group step is only "advance and count": k (= min(budget, a_L)

@@ -433,3 +433,23 @@ def test_dead_subtree_skip(oracle_mod, case):
     lmax = max((i for i, v in enumerate(want["hist"]) if v), default=0)
     f, _ = host_any(n, g, L.FS_PRED_LEN_GE, lmax, tail=L.FS_TAIL_CLOSED, gen_order=go, slice_units=3)
     assert f == bool(want["count"])
+
+
+def test_any_claim_order():
+    """The any-predicate's claim order (fs_core.cuh claim_slice, compiled into libfsgpu): for
+    every slice count S the 2^bits claims map onto [0, S) exactly once (no slice skipped or
+    taken twice), claim 0 is the lex-first slice and claim 1 the lex-last, and both halves are
+    walked in bit-reversed order (claims 2, 3 are the middles)."""
+    f = L.lib().fsdbg_claim_slice
+    none = (1 << 64) - 1
+    for S in list(range(1, 130)) + [1000, 4097, 65536, 100003]:
+        bits = max(0, (S - 1).bit_length())
+        got = [f(i, bits, S) for i in range(1 << bits)]
+        live = [g for g in got if g != none]
+        assert sorted(live) == list(range(S)), S
+        if S >= 2:
+            assert got[0] == 0 and got[1] == S - 1
+        if S >= 8:  # the middles (the back half holds floor(S/2) slices)
+            mid = 1 << (bits - 2)
+            assert got[2] == (mid if mid < (S + 1) // 2 else none)
+            assert got[3] == (S - 1 - mid if mid < S // 2 else none)
