@@ -1037,12 +1037,13 @@ struct HostNodeSink {
   }
 };
 
-// The state-form histogram (fs_kernels.cuh hq_group / hq_tail / enter_h) replayed on the host
+// The state-form histogram (fs_kernels.cuh hq_group / enter_h) replayed on the host
 // for one lane and one slice, reading the same table words (links are byte offsets from the
 // table start; copy j = lane mod FS_HQ_COPIES), with the kernel's shared index arithmetic: every
 // update lands in `sh` (one lane-copy of the shared array, index = address / stride), and the
-// replay fails (bad) if an address leaves the array or is not index-aligned.  Ascends take the
-// generic slow_step (the kernel's t2 ascend table is pinned separately).
+// replay fails (bad) if an address leaves the array or is not index-aligned (masked nodes of a
+// block included).  Ascends take the generic ascend (the kernel's t2 ascend table is pinned
+// separately).
 template <int D, class KT>
 void host_hist_tables_slice(const fs_plan *p, const KT &ktab, fs::Lane<D> &st, uint32_t &budget, uint32_t j,
                             std::vector<int64_t> &sh, bool &bad) {
