@@ -146,11 +146,13 @@ __global__ void fs_slice_starts_kernel(const KParams P, uint32_t *out) {
 }
 
 #ifndef FS_CC_INNER
-// closed-tail count: steps between the warp's slice-refill checks.  128 (vs 64): fewer votes
-// per node (C3 12.63 -> 12.51 ms; W = 8 shards 1.83 -> 1.78 ms); a tiny instance pays a longer
-// idle tail after its last slices (C5, 0.77 M nodes: 0.045 -> 0.067 ms).  (A runtime bound
+// closed-tail count: steps between the warp's slice-refill checks (16 groups of the state form).
+// Round 1 (pair form): 128 vs 64, fewer votes per node (C3 12.63 -> 12.51 ms).  Round 2 (state
+// form, geometric guided slices; C3 one A/B, W = 1 / virtual W = 8 rank): 64 -> 3.87 / 0.613 ms,
+// 128 -> 3.68 / 0.566, 256 -> 3.58 / 0.544, 512 -> 3.53 / 0.539, 1024 -> 3.51 / 0.550 ms.  A tiny
+// instance pays a longer idle tail after its last slices (C5, 0.77 M nodes).  (A runtime bound
 // instead of this constant cost the count loop 9 %.)
-#define FS_CC_INNER 128
+#define FS_CC_INNER 512
 #endif
 template <int CONS>
 struct Inner {
