@@ -9,10 +9,13 @@
 
 int fs_dispatch_count_closed(fs_plan *p, int B, const fs::KParams &kp, cudaStream_t s, bool q, uint32_t *g) {
   (void)B;
-  // B is meaningless for a count: the B = 32 instantiation walks live nodes only (NEXT-3)
-  // (B = 32: the NEXT-3 variant -- live-node walk, k >= 3 dead-subtree skip)
-  return p->c.cadv2_skip || p->c.cd_mask ? fs::dispatch_kt<fs::kConsCountClosed, 32>(p, kp, s, q, g)
-                         : fs::dispatch_kt<fs::kConsCountClosed, 16>(p, kp, s, q, g);
+  // B is meaningless for a count.  B = 16: the state-form walk over equal-cost guided slices,
+  // refill checks every FS_CC_INNER steps.  B = 32: the NEXT-3 variant (live-node walk, k >= 3
+  // dead-subtree skip) and every plan with uniform slices (small instances: few runs per lane,
+  // short slices), refill checks every 128 steps.
+  const bool b16 = p->cost_slices && !p->c.cadv2_skip && !p->c.cd_mask;
+  return b16 ? fs::dispatch_kt<fs::kConsCountClosed, 16>(p, kp, s, q, g)
+             : fs::dispatch_kt<fs::kConsCountClosed, 32>(p, kp, s, q, g);
 }
 
 int fs_dispatch_count_skip(fs_plan *p, int B, const fs::KParams &kp, cudaStream_t s, bool q, uint32_t *g,

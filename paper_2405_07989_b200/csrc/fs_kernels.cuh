@@ -154,9 +154,11 @@ __global__ void fs_slice_starts_kernel(const KParams P, uint32_t *out) {
 // instead of this constant cost the count loop 9 %.)
 #define FS_CC_INNER 512
 #endif
-template <int CONS>
+// (the count's B = 32 variant -- small or uniform slices, NEXT-3 -- checks every 128 steps: a
+// lane that finishes a slice of a few hundred nodes would otherwise idle for most of 512)
+template <int CONS, int B = 16>
 struct Inner {
-  static constexpr int value = CONS == kConsCountClosed ? FS_CC_INNER : 64;
+  static constexpr int value = CONS == kConsCountClosed ? (B == 16 ? FS_CC_INNER : 128) : 64;
 };
 
 // ---------------------------------------------------------------- consumers
@@ -1221,7 +1223,7 @@ __global__ void __launch_bounds__(kBlock, (CONS == kConsRowsAny || CONS == FS_CO
   // the closed-tail consumers' NEXT-3 variant (B = 32): live-node walks when
   // gcd(g_{d-1}, g_d) > 1 and the k >= 3 dead-subtree skip in the ascend (Consts::cd_mask)
   constexpr bool N3 = B == 32 && (CONS == kConsCountClosed || CONS == kConsHistClosed || CONS == kConsAnyClosed);
-  constexpr int INNER = Inner<CONS>::value;
+  constexpr int INNER = Inner<CONS, B>::value;
   // ROWS: a lane completes at most one ring half in kHalf / row_bytes steps, so the warp
   // flushes pending halves once per that many steps.
   constexpr int kRowsPerHalf = (int)(kHalf / (D * (B / 8))) > 0 ? (int)(kHalf / (D * (B / 8))) : 1;
@@ -1245,7 +1247,8 @@ __global__ void __launch_bounds__(kBlock, (CONS == kConsRowsAny || CONS == FS_CO
   const bool cfast = KTAB && CONS == kConsCountClosed && c.cadv_off != 0 && ktab_base < 16384u;
   const bool hfast = KTAB && CONS == kConsHistClosed && c.cadv_off != 0 && P.hist_smem && ktab_base < 16384u;
   // count in state form (cq_group); its table ascend needs the table 128 B aligned (fs_host.cu)
-  const bool qfast = cfast && c.qtab_off != 0 && ((ktab_base + 4u * c.qtab_off) & 127u) == 0u;
+  // (the state form only in the count's B = 16 kernel: its B = 32 variant walks the residue form)
+  const bool qfast = B == 16 && cfast && c.qtab_off != 0 && ((ktab_base + 4u * c.qtab_off) & 127u) == 0u;
   const bool t2fast = cfast && D >= 4 && c.t2_off != 0 && (!qfast || c.t2q_off != 0);
   const bool t2h = hfast && D >= 4 && c.t2_off != 0;  // histogram: one-level ascend by table
   const bool hqf = hfast && P.hist_hq && c.hq_off != 0;  // histogram in state form (hq_group)
@@ -1429,7 +1432,8 @@ __global__ void __launch_bounds__(kBlock, (CONS == kConsRowsAny || CONS == FS_CO
       // ascend; the rare slow lanes run the generic successor step together.
       if (CONS == kConsCountClosed && B == 16 && qfast) {
         cq_group<D, FS_CQ_GROUP>(st, e_count.n);
-      } else if (CONS == kConsCountClosed && B == 32 && cfast && c.cadv2_off != 0u && (UNROLL % 2) == 0) {
+      } else if (CONS == kConsCountClosed && B == 32 && cfast && c.cadv2_off != 0u && c.cadv2_skip &&
+                 (UNROLL % 2) == 0) {
         // (the count ignores B: its B = 32 instantiation is the live-node walk, Consts::cadv2_skip,
         // so the common kernel carries none of that code)
         cc_group2_skip<D, (UNROLL % 2) == 0 ? UNROLL : 2>(st, c, ktab_base + 4u * c.cadv2_off, e_count.n);

@@ -527,7 +527,10 @@ def _next3_instances():
     rng = random.Random(31)
     out = [W.Instance("cd2a", 700, (11, 13, 17, 18, 24)), W.Instance("cd2b", 500, (7, 9, 10, 4, 6)),
            W.Instance("cd3a", 600, (5, 7, 6, 9, 12)), W.Instance("cd3b", 420, (7, 5, 12, 18, 30, 24)),
-           W.Instance("cd4", 300, (9, 8, 12, 16, 20, 4)), W.Instance("cdall", 360, (6, 10, 14, 22))]
+           W.Instance("cd4", 300, (9, 8, 12, 16, 20, 4)), W.Instance("cdall", 360, (6, 10, 14, 22)),
+           # g_{d-1} > 64 with a common divisor: no live-node pair table, the NEXT-3 kernel
+           # variant walks the plain pair table (a routing bug found in round 2)
+           W.Instance("cdwide", 900, (5, 7, 6, 66, 132)), W.Instance("cdwide2", 800, (3, 11, 70, 140, 210))]
     while len(out) < 20:
         d = rng.randint(4, 7)
         f = rng.choice((2, 3, 4, 6))
