@@ -5,9 +5,11 @@
 
 int fs_dispatch_hist_closed(fs_plan *p, int B, const fs::KParams &kp, cudaStream_t s, bool q, uint32_t *g) {
   (void)B;
-  // (B = 32: the NEXT-3 variant -- live-node table walk, k >= 3 dead-subtree skip)
-  return p->c.hadv_skip || p->c.cd_mask ? fs::dispatch_kt<fs::kConsHistClosed, 32>(p, kp, s, q, g)
-                                        : fs::dispatch_kt<fs::kConsHistClosed, 16>(p, kp, s, q, g);
+  // (B = 16: equal-cost guided slices, refill checks every FS_HC_INNER steps; B = 32: the NEXT-3
+  // variant -- live-node table walk, k >= 3 dead-subtree skip -- and uniform-slice plans, 64)
+  const bool b16 = p->cost_slices && !p->c.hadv_skip && !p->c.cd_mask;
+  return b16 ? fs::dispatch_kt<fs::kConsHistClosed, 16>(p, kp, s, q, g)
+             : fs::dispatch_kt<fs::kConsHistClosed, 32>(p, kp, s, q, g);
 }
 
 // Closed-tail histogram finalize: hist[l] = sum of diff[k] over k <= l, k = l mod dstride (a

@@ -156,9 +156,17 @@ __global__ void fs_slice_starts_kernel(const KParams P, uint32_t *out) {
 #endif
 // (the count's B = 32 variant -- small or uniform slices, NEXT-3 -- checks every 128 steps: a
 // lane that finishes a slice of a few hundred nodes would otherwise idle for most of 512)
+#ifndef FS_HC_INNER
+// closed-tail histogram, B = 16 kernel (equal-cost guided slices): steps between the warp's
+// refill checks.  C4, one A/B: 64 -> 17.33 ms, 128 -> 16.90, 256 -> 16.69, 512 -> 16.60 (W = 8
+// virtual rank at 256: 2.35 -> 2.25 ms); uniform-slice plans run the B = 32 kernel (64)
+#define FS_HC_INNER 256
+#endif
 template <int CONS, int B = 16>
 struct Inner {
-  static constexpr int value = CONS == kConsCountClosed ? (B == 16 ? FS_CC_INNER : 128) : 64;
+  static constexpr int value = CONS == kConsCountClosed ? (B == 16 ? FS_CC_INNER : 128)
+                               : CONS == kConsHistClosed && B == 16 ? FS_HC_INNER
+                                                                    : 64;
 };
 
 // ---------------------------------------------------------------- consumers
